@@ -1,0 +1,87 @@
+"""Winograd-level oracle pieces, in exact Python integers -- TEST INFRASTRUCTURE.
+
+* ``opcount(n, l)`` -- the arithmetic-operation count behind PAPER.md Table 1
+  (l.245-253): the classical algorithm on n x n matrices costs n^3
+  multiplications and n^2 (n-1) additions, 2n^3 - n^2 in total (l.239:
+  "MM(n) = 2n^3 ... means ... 2n^3 + O(n^2)"); one Winograd level replaces it
+  by 7 half-size products plus 15 half-size additions (Winograd's variant,
+  l.235-243; Table 2 lists its 8 pre-additions S1..S4, T1..T4 and 7 post-
+  additions U1..U7).  Pinned against all 25 printed cells of Table 1.
+
+* ``schedule_table2(...)`` -- PAPER.md Table 2 (l.263-276), "Schedule for
+  operation C <- alpha A x B + beta C with 3 temporaries", executed step by
+  step over Z on quadrants.  Step 16 is printed "P4 = alpha A12 T4 - beta C21";
+  Appendix A.2 (l.935) and the algebra require A22 (reading R9).
+  ``step16_operand`` selects which, so the tests can show the printed form is
+  wrong and the fixed form equals alpha*A*B + beta*C.
+
+Parity status: pinned (tests/test_oracle_pins.py::test_table1_*, test_table2_*).
+"""
+from __future__ import annotations
+
+
+def opcount(n: int, l: int) -> int:
+    """Field operations for n x n times n x n with l Winograd levels (Table 1)."""
+    if l == 0:
+        return 2 * n ** 3 - n ** 2
+    if n % 2:
+        raise ValueError("n must be even at every Winograd level")
+    h = n // 2
+    return 7 * opcount(h, l - 1) + 15 * h * h
+
+
+def _mm(X, Y):
+    k = len(Y)
+    return [[sum(X[i][t] * Y[t][j] for t in range(k)) for j in range(len(Y[0]))]
+            for i in range(len(X))]
+
+
+def _add(X, Y, s=1):
+    return [[x + s * y for x, y in zip(rx, ry)] for rx, ry in zip(X, Y)]
+
+
+def _scale(a, X):
+    return [[a * x for x in r] for r in X]
+
+
+def _quad(M, r, c):
+    h, w = len(M) // 2, len(M[0]) // 2
+    return [row[c * w:(c + 1) * w] for row in M[r * h:(r + 1) * h]]
+
+
+def schedule_table2(alpha, A, B, beta, C, step16_operand="A22"):
+    """One Winograd level of Table 2 over Z; returns the new C (lists of ints).
+
+    A is m x k, B is k x n, C is m x n, all even dimensions.  The three
+    temporaries X1, X2, X3 of the "loc." column are kept as named variables.
+    """
+    A11, A12, A21, A22 = _quad(A, 0, 0), _quad(A, 0, 1), _quad(A, 1, 0), _quad(A, 1, 1)
+    B11, B12, B21, B22 = _quad(B, 0, 0), _quad(B, 0, 1), _quad(B, 1, 0), _quad(B, 1, 1)
+    C11, C12, C21, C22 = _quad(C, 0, 0), _quad(C, 0, 1), _quad(C, 1, 0), _quad(C, 1, 1)
+    A4 = {"A22": A22, "A12": A12}[step16_operand]
+
+    X1 = _add(A21, A22)                               # 1  S1 = A21 + A22
+    X2 = _add(B12, B11, -1)                           # 2  T1 = B12 - B11
+    X3 = _scale(alpha, _mm(X1, X2))                   # 3  P5 = alpha S1 T1
+    C22 = _add(X3, _scale(beta, C22))                 # 4  C22 = P5 + beta C22
+    C12 = _add(X3, _scale(beta, C12))                 # 5  C12 = P5 + beta C12
+    X1 = _add(X1, A11, -1)                            # 6  S2 = S1 - A11
+    X2 = _add(B22, X2, -1)                            # 7  T2 = B22 - T1
+    X3 = _scale(alpha, _mm(A11, B11))                 # 8  P1 = alpha A11 B11
+    C11 = _add(X3, _scale(beta, C11))                 # 9  C11 = P1 + beta C11
+    X3 = _add(_scale(alpha, _mm(X1, X2)), X3)         # 10 U2 = alpha S2 T2 + P1
+    C11 = _add(_scale(alpha, _mm(A12, B21)), C11)     # 11 U1 = alpha A12 B21 + C11
+    X1 = _add(A12, X1, -1)                            # 12 S4 = A12 - S2
+    X2 = _add(X2, B21, -1)                            # 13 T4 = T2 - B21
+    C12 = _add(_scale(alpha, _mm(X1, B22)), C12)      # 14 C12 = alpha S4 B22 + C12
+    C12 = _add(X3, C12)                               # 15 U5 = U2 + C12
+    C21 = _add(_scale(alpha, _mm(A4, X2)), _scale(beta, C21), -1)  # 16 P4 = alpha A22 T4 - beta C21
+    X1 = _add(A11, A21, -1)                           # 17 S3 = A11 - A21
+    X2 = _add(B22, B12, -1)                           # 18 T3 = B22 - B12
+    X3 = _add(_scale(alpha, _mm(X1, X2)), X3)         # 19 U3 = alpha S3 T3 + U2
+    C22 = _add(X3, C22)                               # 20 U7 = U3 + C22
+    C21 = _add(X3, C21, -1)                           # 21 U6 = U3 - C21
+
+    top = [r1 + r2 for r1, r2 in zip(C11, C12)]
+    bot = [r1 + r2 for r1, r2 in zip(C21, C22)]
+    return top + bot
