@@ -1,0 +1,171 @@
+/*
+ * ffgemm.h -- C ABI of the B200 (sm_100a) fgemm library: exact modular matrix
+ * multiplication over a word-size prime field,
+ *
+ *     C <- (alpha * op(A) * op(B) + beta * C) mod p,        results in [0, p).
+ *
+ * The operation is the paper's fgemm ("we named our routine
+ * over a word-size finite field fgemm"; Table 2 caption l.276, "operation
+ * C <- alpha A x B + beta C").  The paper computes it over Z with a numerical
+ * BLAS kernel and delayed modular reduction (Sec. 2.1.2, l.139-159, Eq. (1)/(2));
+ * this library does the same with int8 "limbs" on the 5th-generation tensor
+ * cores (tcgen05.mma.kind::i8, exact int32 accumulation in TMEM), blocking k
+ * by the Eq. (2) analogue of the int32 accumulator.
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  - Storage is row-major with a leading dimension (elements), as in
+ *    SPEC.md l.22-26 / l.89.  op(A) is m x k: transA = 'N'/'n' means A is
+ *    stored m x k with lda >= max(1,k); 'T'/'t' means A is stored k x m with
+ *    lda >= max(1,m).  Likewise op(B) is k x n with ldb, and C is m x n with
+ *    ldc >= max(1,n).  Indices and sizes are 64-bit; elements are int32.
+ *  - Inputs are meant to be canonical residues in [0,p) (BASELINE.json
+ *    north_star (1)); any int32 is accepted and reduced (Euclidean) mod p
+ *    (reading R3).  alpha and beta are reduced mod p (reading R4);
+ *    alpha = p-1 means -1.  Output is always canonical [0,p).
+ *  - beta = 0 (mod p): C is write-only and never read (BLAS convention,
+ *    reading R5).  k = 0 or alpha = 0 (mod p): C <- beta*C mod p.
+ *    m = 0 or n = 0: no-op.
+ *  - p: 2 <= p < 2^31 (primality is not required: the result is exact in
+ *    the ring Z/pZ).
+ *  - Device pointers ("dev") must be device memory of the current CUDA device;
+ *    they are owned by the caller.  A and B are read only; C is updated in
+ *    place and must not overlap A or B.  Work is asynchronous with respect to
+ *    the host (like cuBLAS): errors from kernels surface at the next sync.
+ *  - Return value: 0 on success.  A negative value -i means argument i is
+ *    invalid, in BLAS xerbla order of ff_gemm's signature (1 p, 2 transA,
+ *    3 transB, 4 m, 5 n, 6 k, 8 A, 9 lda, 10 B, 11 ldb, 13 C, 14 ldc;
+ *    15+ for the extra arguments of the _ex / split entry points).  A positive
+ *    value is one of the FF_ERR_* runtime codes below.  ff_strerror() names it.
+ *  - There is no CPU fallback: without an sm_100 device every compute entry
+ *    point returns FF_ERR_ARCH (or FF_ERR_CUDA).
+ */
+#ifndef FFGEMM_H
+#define FFGEMM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FF_OK 0
+#define FF_ERR_CUDA 1     /* a CUDA runtime/driver call failed */
+#define FF_ERR_NOMEM 2    /* device or pinned allocation failed / workspace too small */
+#define FF_ERR_ARCH 3     /* current device is not sm_100 (B200) */
+#define FF_ERR_OPTS 4     /* ff_opts invalid (e.g. kb_override above the safe bound) */
+#define FF_ERR_INTERNAL 5 /* planner could not represent p (should not happen for p < 2^31) */
+
+/* Limb schemes.  S: balanced signed digits in [-128,127];
+ * T: two's-complement bytes (low limbs u8 in [0,255], top limb s8). */
+#define FF_SCHEME_AUTO 0
+#define FF_SCHEME_S 1
+#define FF_SCHEME_T 2
+
+/* Options for the _ex / split entry points.  Zero-initialise and set fields;
+ * a NULL pointer means all defaults. */
+typedef struct ff_opts {
+    int32_t winograd;       /* -1 auto, 0 never, 1 one Winograd level (Table 2) */
+    int32_t scheme;         /* FF_SCHEME_*; AUTO picks the fewest limbs, S on ties */
+    int64_t kb_override;    /* 0: planner k-block; else k-block length in elements,
+                               rounded down to a multiple of 128; must not exceed the
+                               safe bound (else FF_ERR_OPTS).  Forces mid-k reductions. */
+    int32_t debug_saturate; /* 1: set the MMA saturate bit (test builds only; a clamp
+                               then shows as a mismatch instead of a silent wrap) */
+    int32_t reserved[7];
+} ff_opts;
+
+/* The plan the library derives from (p, k, opts): host-only, no GPU needed. */
+typedef struct ff_plan_info {
+    uint32_t p;
+    int32_t L;               /* limbs per residue, 1..4 */
+    int32_t scheme;          /* FF_SCHEME_S or FF_SCHEME_T */
+    int32_t groups;          /* 2L-1 weight groups w = i+j */
+    int32_t limb_signed[4];  /* 1 if limb i is s8, 0 if u8 */
+    int32_t digit_max[4];    /* D_i = max |limb i| over all centred residues */
+    int64_t group_bound[7];  /* B_w = sum_{i+j=w} D_i D_j  (per unit of k) */
+    int64_t group_bound_max; /* max_w B_w */
+    int64_t kb_max;          /* floor((2^31-1-(p-1)/2) / max_w B_w): Eq. (2) analogue */
+    int64_t kb;              /* k-block actually used (multiple of 128, <= kb_max) */
+    int64_t k_pad;           /* k rounded up to a multiple of 16 (limb plane row length) */
+    int64_t num_kblocks;     /* ceil(k / kb); 1 for every BASELINE config */
+    int32_t centre_max;      /* (p-1)/2 */
+    int32_t reserved[5];
+} ff_plan_info;
+
+/* Library version (major*10000 + minor*100 + patch). Host only. */
+int ff_version(void);
+
+/* Name of a return code. Host only; never NULL. */
+const char *ff_strerror(int code);
+
+/* 0 if `device` is an sm_100 GPU usable by this library, else FF_ERR_ARCH /
+ * FF_ERR_CUDA. */
+int ff_device_check(int device);
+
+/* Derive the plan for (p, k, opts) (Eq. (2), l.155, generalised to
+ * limbs: DESIGN.md §4.2).  Host only.  Returns -1 (p), -6 (k) or FF_ERR_OPTS. */
+int ff_plan_query(uint32_t p, int64_t k, const ff_opts *opts, ff_plan_info *out);
+
+/* Core call, on the legacy default stream with a library-owned cached
+ * workspace (not thread-safe across host threads).  A, B, C: dev. */
+int ff_gemm(uint32_t p, char transA, char transB, int64_t m, int64_t n, int64_t k,
+            uint32_t alpha, const int32_t *A, int64_t lda, const int32_t *B, int64_t ldb,
+            uint32_t beta, int32_t *C, int64_t ldc);
+
+/* Bytes of device workspace ff_gemm_ex needs for this problem. Host only. */
+size_t ff_gemm_workspace_size(uint32_t p, char transA, char transB, int64_t m, int64_t n,
+                              int64_t k, const ff_opts *opts);
+
+/* As ff_gemm, on `stream` (a cudaStream_t; NULL = legacy default), with
+ * options and a caller workspace (dev, >= ff_gemm_workspace_size bytes,
+ * 256-byte aligned; NULL = library pool).  Reentrant with distinct workspaces.
+ * Extra argument codes: -15 opts, -16 workspace. */
+int ff_gemm_ex(uint32_t p, char transA, char transB, int64_t m, int64_t n, int64_t k,
+               uint32_t alpha, const int32_t *A, int64_t lda, const int32_t *B, int64_t ldb,
+               uint32_t beta, int32_t *C, int64_t ldc, const ff_opts *opts,
+               void *workspace, size_t workspace_bytes, void *stream);
+
+/* As ff_gemm, but A, B and C are HOST pointers (pinned for full PCIe speed;
+ * pageable works).  Copies in, computes on the current device, copies C back
+ * and synchronises before returning.  Device buffers are library-owned and
+ * cached.  This is the end-to-end entry point the bench's "e2e" number uses. */
+int ff_gemm_host(uint32_t p, char transA, char transB, int64_t m, int64_t n, int64_t k,
+                 uint32_t alpha, const int32_t *A, int64_t lda, const int32_t *B, int64_t ldb,
+                 uint32_t beta, int32_t *C, int64_t ldc, const ff_opts *opts);
+
+/* ---- split entry points (multi-GPU row-panel path) ----------
+ * Limb planes: int8, layout [L][rows][k_pad] (plane l, row r, column kk at
+ * byte l*rows*k_pad + r*k_pad + kk), where L and k_pad come from
+ * ff_plan_query(p, k, opts) and rows is the operand's row count in K-major
+ * form (m for op(A), n for op(B)^T).  Size: L*rows*k_pad bytes, dev,
+ * 16-byte aligned. */
+
+/* Encode `rows` K-major rows of an operand into limb planes: row r, column
+ * kk of the K-major view is X[r*ldx + kk] if kmajor_src = 1 (op(A) with
+ * transA='N', or op(B)^T with transB='T'), else X[kk*ldx + r] (the
+ * transposed cases).  Columns k..k_pad-1 are written as zero.
+ * X: dev int32; limbs: dev.  Codes: -1 p, -2 k, -4 rows, -5 X, -6 ldx, -7 limbs. */
+int ff_encode(uint32_t p, int64_t k, const ff_opts *opts, int kmajor_src, int64_t rows,
+              const int32_t *X, int64_t ldx, int8_t *limbs, void *stream);
+
+/* C (m x n, ldc) <- (alpha * op(A) * op(B) + beta * C) mod p from limb planes
+ * produced by ff_encode with the same (p, k, opts): A_limbs has m rows,
+ * B_limbs has n rows.  Codes: -1 p, -2 m, -3 n, -4 k, -7 A_limbs, -8 B_limbs,
+ * -10 C, -11 ldc. */
+int ff_gemm_limbs(uint32_t p, int64_t m, int64_t n, int64_t k, const ff_opts *opts,
+                  uint32_t alpha, const int8_t *A_limbs, const int8_t *B_limbs,
+                  uint32_t beta, int32_t *C, int64_t ldc, void *stream);
+
+/* ---- synthetic inputs (device twin of ffgen/__init__.py) -----------------
+ * X[r*ld + c] = v[index0 + r*cols + c] for r < rows, c < cols, where v is the
+ * (seed, stream_id) sequence of ffgen: v[i] = (mix64(key + (i+1)*GAMMA) >> 11)
+ * mod p, key = mix64(seed*16 + stream_id).  X: dev. */
+int ff_fill_uniform(int32_t *X, int64_t rows, int64_t cols, int64_t ld, uint32_t p,
+                    uint64_t seed, uint32_t stream_id, int64_t index0, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FFGEMM_H */

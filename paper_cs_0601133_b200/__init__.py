@@ -1,0 +1,13 @@
+"""B200-native fgemm: exact C <- (alpha op(A) op(B) + beta C) mod p on sm_100a tensor cores.
+
+The product is the CUDA library ``lib/libffgemm.so`` (C ABI: include/ffgemm.h);
+this package is its thin binding (``ffgemm``) plus the multi-GPU row-panel
+driver (``sharded``).  Importing it without the built library raises.
+"""
+from .ffgemm import (EXPORTED, FFError, fgemm, ff_device_check, ff_encode, ff_fill_uniform,  # noqa: F401
+                     ff_gemm, ff_gemm_ex, ff_gemm_host, ff_gemm_limbs, ff_gemm_workspace_size,
+                     ff_opts, ff_plan_query, ff_strerror, ff_version, LIB_PATH)
+
+__all__ = ["fgemm", "ff_gemm", "ff_gemm_ex", "ff_gemm_host", "ff_gemm_limbs", "ff_encode",
+           "ff_fill_uniform", "ff_plan_query", "ff_gemm_workspace_size", "ff_strerror",
+           "ff_version", "ff_device_check", "ff_opts", "FFError", "EXPORTED", "LIB_PATH"]

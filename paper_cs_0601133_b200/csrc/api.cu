@@ -1,0 +1,314 @@
+// api.cu -- the C ABI (include/ffgemm.h): argument checking, quick returns,
+// workspace management and the launch sequence encode(A), encode(B), gemm_tc.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+
+#include "internal.h"
+
+namespace ff {
+
+namespace {
+
+constexpr int kMaxDev = 64;
+
+int g_sms[kMaxDev];
+int g_arch_ok[kMaxDev];  // 0 unknown, 1 ok, 2 not sm_100
+
+struct Buf {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+};
+Buf g_ws[kMaxDev];
+Buf g_host_a[kMaxDev], g_host_b[kMaxDev], g_host_c[kMaxDev];
+std::mutex g_mu;
+
+int cur_dev() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d < 0 || d >= kMaxDev ? 0 : d;
+}
+
+int arch_check(int dev) {
+    if (dev < 0 || dev >= kMaxDev) return FF_ERR_ARCH;
+    if (g_arch_ok[dev] == 0) {
+        int major = 0, minor = 0;
+        if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess) {
+            cudaGetLastError();
+            return FF_ERR_CUDA;
+        }
+        g_arch_ok[dev] = (major == 10 && minor == 0) ? 1 : 2;
+    }
+    return g_arch_ok[dev] == 1 ? 0 : FF_ERR_ARCH;
+}
+
+int ensure(Buf& b, size_t bytes) {
+    if (b.bytes >= bytes) return 0;
+    if (b.ptr) {
+        cudaDeviceSynchronize();
+        cudaFree(b.ptr);
+        b.ptr = nullptr;
+        b.bytes = 0;
+    }
+    if (cudaMalloc(&b.ptr, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return FF_ERR_NOMEM;
+    }
+    b.bytes = bytes;
+    return 0;
+}
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+bool is_n(char t) { return t == 'N' || t == 'n'; }
+bool is_t(char t) { return t == 'T' || t == 't'; }
+
+int validate(uint32_t p, char transA, char transB, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda,
+             const void* B, int64_t ldb, const void* C, int64_t ldc) {
+    if (p < 2 || p >= (1u << 31)) return -1;
+    if (!is_n(transA) && !is_t(transA)) return -2;
+    if (!is_n(transB) && !is_t(transB)) return -3;
+    if (m < 0) return -4;
+    if (n < 0) return -5;
+    if (k < 0) return -6;
+    if (!A && m > 0 && k > 0) return -8;
+    const int64_t a_cols = is_n(transA) ? k : m;
+    if (lda < (a_cols > 1 ? a_cols : 1)) return -9;
+    if (!B && k > 0 && n > 0) return -10;
+    const int64_t b_cols = is_n(transB) ? n : k;
+    if (ldb < (b_cols > 1 ? b_cols : 1)) return -11;
+    if (!C && m > 0 && n > 0) return -13;
+    if (ldc < (n > 1 ? n : 1)) return -14;
+    return 0;
+}
+
+size_t ws_bytes(const Plan& pl, int64_t m, int64_t n) {
+    const size_t L = static_cast<size_t>(pl.info.L), kp = static_cast<size_t>(pl.info.k_pad);
+    return align256(L * static_cast<size_t>(m) * kp) + align256(L * static_cast<size_t>(n) * kp);
+}
+
+int cuda_rc(cudaError_t e) { return e == cudaSuccess ? 0 : FF_ERR_CUDA; }
+
+// The whole path on device pointers.
+int run(const Plan& pl, char transA, char transB, int64_t m, int64_t n, int64_t k, const int32_t* A,
+        int64_t lda, const int32_t* B, int64_t ldb, int32_t* C, int64_t ldc, void* ws, cudaStream_t st) {
+    if (k == 0 || pl.mp.alpha == 0) return cuda_rc(launch_scale_c(pl.mp, m, n, C, ldc, st));
+    int8_t* al = static_cast<int8_t*>(ws);
+    int8_t* bl = al + align256(static_cast<size_t>(pl.info.L) * m * pl.info.k_pad);
+    int e = cuda_rc(launch_encode(pl, is_n(transA) ? 1 : 0, m, k, A, lda, al, st));
+    if (e) return e;
+    e = cuda_rc(launch_encode(pl, is_t(transB) ? 1 : 0, n, k, B, ldb, bl, st));
+    if (e) return e;
+    return launch_gemm_tc(pl, m, n, k, al, bl, C, ldc, st);
+}
+
+}  // namespace
+
+int num_sms() {
+    const int d = cur_dev();
+    if (g_sms[d] == 0) {
+        int v = 0;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d) != cudaSuccess || v <= 0) {
+            cudaGetLastError();
+            v = 148;
+        }
+        g_sms[d] = v;
+    }
+    return g_sms[d];
+}
+
+}  // namespace ff
+
+using namespace ff;
+
+extern "C" {
+
+int ff_version(void) { return 100; }
+
+const char* ff_strerror(int code) {
+    switch (code) {
+        case FF_OK: return "success";
+        case FF_ERR_CUDA: return "CUDA runtime/driver error";
+        case FF_ERR_NOMEM: return "out of device memory or workspace too small";
+        case FF_ERR_ARCH: return "device is not an sm_100 (B200) GPU";
+        case FF_ERR_OPTS: return "invalid ff_opts";
+        case FF_ERR_INTERNAL: return "internal planner error";
+        default: break;
+    }
+    if (code < 0) {
+        switch (-code) {
+            case 1: return "invalid argument 1 (p)";
+            case 2: return "invalid argument 2 (transA)";
+            case 3: return "invalid argument 3 (transB)";
+            case 4: return "invalid argument 4 (m)";
+            case 5: return "invalid argument 5 (n)";
+            case 6: return "invalid argument 6 (k)";
+            case 8: return "invalid argument 8 (A)";
+            case 9: return "invalid argument 9 (lda)";
+            case 10: return "invalid argument 10 (B)";
+            case 11: return "invalid argument 11 (ldb)";
+            case 13: return "invalid argument 13 (C)";
+            case 14: return "invalid argument 14 (ldc)";
+            case 16: return "invalid argument 16 (workspace)";
+            default: return "invalid argument";
+        }
+    }
+    return "unknown error";
+}
+
+int ff_device_check(int device) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return FF_ERR_CUDA;
+    }
+    if (device < 0 || device >= n) return FF_ERR_ARCH;
+    return arch_check(device);
+}
+
+int ff_plan_query(uint32_t p, int64_t k, const ff_opts* opts, ff_plan_info* out) {
+    if (!out) return -4;
+    Plan pl;
+    int e = make_plan(p, k, opts, &pl);
+    if (e) return e;
+    *out = pl.info;
+    return 0;
+}
+
+size_t ff_gemm_workspace_size(uint32_t p, char transA, char transB, int64_t m, int64_t n, int64_t k,
+                              const ff_opts* opts) {
+    (void)transA;
+    (void)transB;
+    if (m < 0 || n < 0 || k < 0) return 0;
+    Plan pl;
+    if (make_plan(p, k, opts, &pl)) return 0;
+    return ws_bytes(pl, m, n);
+}
+
+int ff_gemm_ex(uint32_t p, char transA, char transB, int64_t m, int64_t n, int64_t k, uint32_t alpha,
+               const int32_t* A, int64_t lda, const int32_t* B, int64_t ldb, uint32_t beta, int32_t* C,
+               int64_t ldc, const ff_opts* opts, void* workspace, size_t workspace_bytes, void* stream) {
+    int e = validate(p, transA, transB, m, n, k, A, lda, B, ldb, C, ldc);
+    if (e) return e;
+    if (m == 0 || n == 0) return 0;
+    Plan pl;
+    e = make_plan(p, k, opts, &pl);
+    if (e) return e;
+    if (opts && opts->winograd == 1) return FF_ERR_OPTS;  // one-level Winograd: see DESIGN.md §7
+    set_scalars(&pl, alpha, beta);
+    const int dev = cur_dev();
+    e = arch_check(dev);
+    if (e) return e;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t need = ws_bytes(pl, m, n);
+    if (workspace) {
+        if (workspace_bytes < need || (reinterpret_cast<uintptr_t>(workspace) & 255)) return -16;
+        return run(pl, transA, transB, m, n, k, A, lda, B, ldb, C, ldc, workspace, st);
+    }
+    std::lock_guard<std::mutex> lk(g_mu);
+    e = ensure(g_ws[dev], need);
+    if (e) return e;
+    return run(pl, transA, transB, m, n, k, A, lda, B, ldb, C, ldc, g_ws[dev].ptr, st);
+}
+
+int ff_gemm(uint32_t p, char transA, char transB, int64_t m, int64_t n, int64_t k, uint32_t alpha,
+            const int32_t* A, int64_t lda, const int32_t* B, int64_t ldb, uint32_t beta, int32_t* C, int64_t ldc) {
+    return ff_gemm_ex(p, transA, transB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, nullptr, nullptr, 0,
+                      nullptr);
+}
+
+int ff_gemm_host(uint32_t p, char transA, char transB, int64_t m, int64_t n, int64_t k, uint32_t alpha,
+                 const int32_t* A, int64_t lda, const int32_t* B, int64_t ldb, uint32_t beta, int32_t* C,
+                 int64_t ldc, const ff_opts* opts) {
+    int e = validate(p, transA, transB, m, n, k, A, lda, B, ldb, C, ldc);
+    if (e) return e;
+    if (m == 0 || n == 0) return 0;
+    Plan pl;
+    e = make_plan(p, k, opts, &pl);
+    if (e) return e;
+    const int dev = cur_dev();
+    e = arch_check(dev);
+    if (e) return e;
+    // Dense device copies of the stored operands (rows x cols as stored).
+    const int64_t ar = is_n(transA) ? m : k, ac = is_n(transA) ? k : m;
+    const int64_t br = is_n(transB) ? k : n, bc = is_n(transB) ? n : k;
+    std::lock_guard<std::mutex> lk(g_mu);
+    if ((e = ensure(g_host_a[dev], sizeof(int32_t) * (size_t)(ar * ac > 0 ? ar * ac : 1)))) return e;
+    if ((e = ensure(g_host_b[dev], sizeof(int32_t) * (size_t)(br * bc > 0 ? br * bc : 1)))) return e;
+    if ((e = ensure(g_host_c[dev], sizeof(int32_t) * (size_t)(m * n)))) return e;
+    Plan tmp = pl;
+    if ((e = ensure(g_ws[dev], ws_bytes(tmp, m, n)))) return e;
+    int32_t* dA = static_cast<int32_t*>(g_host_a[dev].ptr);
+    int32_t* dB = static_cast<int32_t*>(g_host_b[dev].ptr);
+    int32_t* dC = static_cast<int32_t*>(g_host_c[dev].ptr);
+    cudaStream_t st = 0;
+    if (ar * ac > 0 && cudaMemcpy2DAsync(dA, ac * 4, A, lda * 4, ac * 4, ar, cudaMemcpyHostToDevice, st))
+        return FF_ERR_CUDA;
+    if (br * bc > 0 && cudaMemcpy2DAsync(dB, bc * 4, B, ldb * 4, bc * 4, br, cudaMemcpyHostToDevice, st))
+        return FF_ERR_CUDA;
+    set_scalars(&pl, alpha, beta);
+    if (pl.mp.beta != 0 &&
+        cudaMemcpy2DAsync(dC, n * 4, C, ldc * 4, n * 4, m, cudaMemcpyHostToDevice, st))
+        return FF_ERR_CUDA;
+    e = run(pl, transA, transB, m, n, k, dA, ac > 1 ? ac : 1, dB, bc > 1 ? bc : 1, dC, n, g_ws[dev].ptr, st);
+    if (e) return e;
+    if (cudaMemcpy2DAsync(C, ldc * 4, dC, n * 4, n * 4, m, cudaMemcpyDeviceToHost, st)) return FF_ERR_CUDA;
+    return cudaStreamSynchronize(st) == cudaSuccess ? 0 : FF_ERR_CUDA;
+}
+
+int ff_encode(uint32_t p, int64_t k, const ff_opts* opts, int kmajor_src, int64_t rows, const int32_t* X,
+              int64_t ldx, int8_t* limbs, void* stream) {
+    if (p < 2 || p >= (1u << 31)) return -1;
+    if (k < 0) return -2;
+    if (rows < 0) return -4;
+    if (!X && rows > 0 && k > 0) return -5;
+    if (ldx < 1 || (kmajor_src && ldx < k) || (!kmajor_src && ldx < rows)) return -6;
+    if ((!limbs && rows > 0 && k > 0) || (reinterpret_cast<uintptr_t>(limbs) & 15)) return -7;
+    Plan pl;
+    int e = make_plan(p, k, opts, &pl);
+    if (e) return e;
+    e = arch_check(cur_dev());
+    if (e) return e;
+    return cuda_rc(launch_encode(pl, kmajor_src, rows, k, X, ldx, limbs, static_cast<cudaStream_t>(stream)));
+}
+
+int ff_gemm_limbs(uint32_t p, int64_t m, int64_t n, int64_t k, const ff_opts* opts, uint32_t alpha,
+                  const int8_t* A_limbs, const int8_t* B_limbs, uint32_t beta, int32_t* C, int64_t ldc,
+                  void* stream) {
+    if (p < 2 || p >= (1u << 31)) return -1;
+    if (m < 0) return -2;
+    if (n < 0) return -3;
+    if (k < 0) return -4;
+    if (m == 0 || n == 0) return 0;
+    if (k > 0 && (!A_limbs || (reinterpret_cast<uintptr_t>(A_limbs) & 15))) return -7;
+    if (k > 0 && (!B_limbs || (reinterpret_cast<uintptr_t>(B_limbs) & 15))) return -8;
+    if (!C) return -10;
+    if (ldc < (n > 1 ? n : 1)) return -11;
+    Plan pl;
+    int e = make_plan(p, k, opts, &pl);
+    if (e) return e;
+    set_scalars(&pl, alpha, beta);
+    e = arch_check(cur_dev());
+    if (e) return e;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (k == 0 || pl.mp.alpha == 0) return cuda_rc(launch_scale_c(pl.mp, m, n, C, ldc, st));
+    return launch_gemm_tc(pl, m, n, k, A_limbs, B_limbs, C, ldc, st);
+}
+
+int ff_fill_uniform(int32_t* X, int64_t rows, int64_t cols, int64_t ld, uint32_t p, uint64_t seed,
+                    uint32_t stream_id, int64_t index0, void* stream) {
+    if (rows < 0) return -2;
+    if (cols < 0) return -3;
+    if (ld < (cols > 1 ? cols : 1)) return -4;
+    if (p < 2 || p >= (1u << 31)) return -5;
+    if (!X && rows * cols > 0) return -1;
+    int e = arch_check(cur_dev());
+    if (e) return e;
+    return cuda_rc(launch_fill_uniform(X, rows, cols, ld, p, seed, stream_id, index0,
+                                       static_cast<cudaStream_t>(stream)));
+}
+
+}  // extern "C"

@@ -1,0 +1,63 @@
+// internal.h -- host-side structures shared by the library's translation units.
+#pragma once
+#include <cstdint>
+#include <cstddef>
+#include <cuda_runtime.h>
+
+#include "../../include/ffgemm.h"
+
+namespace ff {
+
+constexpr int kMaxLimbs = 4;
+constexpr int kMaxGroups = 2 * kMaxLimbs - 1;
+constexpr int kBK = 128;        // bytes (= int8 elements) of K per pipeline stage (one 128B swizzle row)
+constexpr int kMmaK = 32;       // K per tcgen05.mma.kind::i8 instruction
+constexpr int kTileM = 128;     // rows of op(A) per CTA tile (= TMEM lanes)
+constexpr int kTileN = 256;     // columns of C per CTA tile (= TMEM columns per accumulator)
+
+// Residue-arithmetic constants for one p (all 32-bit; see modp.cuh for the
+// algorithms: Barrett for int32 -> [0,p), Shoup for a*w mod p).
+struct ModP {
+    uint32_t p;
+    uint32_t half;        // (p-1)/2: centred residues are in [-half, half]
+    uint32_t mu;          // floor(2^32 / p)
+    uint32_t off31;       // 2^31 mod p
+    uint32_t w256;        // 256 mod p
+    uint32_t w256_sh;     // floor(w256 * 2^32 / p)
+    uint32_t alpha, alpha_sh;
+    uint32_t beta, beta_sh;
+};
+
+struct Plan {
+    ff_plan_info info;
+    ModP mp;
+    int npairs;                      // L*L
+    int pair_i[kMaxLimbs * kMaxLimbs];
+    int pair_j[kMaxLimbs * kMaxLimbs];
+    int group_first[kMaxGroups];     // pairs of group w are [group_first[w], group_first[w]+group_len[w])
+    int group_len[kMaxGroups];
+    bool saturate;
+};
+
+// planner.cpp
+int make_plan(uint32_t p, int64_t k, const ff_opts* opts, Plan* out);
+void set_scalars(Plan* pl, uint32_t alpha, uint32_t beta);
+
+// encode.cu
+cudaError_t launch_encode(const Plan& pl, int kmajor_src, int64_t rows, int64_t k,
+                          const int32_t* X, int64_t ldx, int8_t* limbs, cudaStream_t st);
+cudaError_t launch_scale_c(const ModP& mp, int64_t m, int64_t n, int32_t* C, int64_t ldc,
+                           cudaStream_t st);
+
+// gemm_tc.cu
+int launch_gemm_tc(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A_limbs,
+                   const int8_t* B_limbs, int32_t* C, int64_t ldc, cudaStream_t st);
+
+// gen.cu
+cudaError_t launch_fill_uniform(int32_t* X, int64_t rows, int64_t cols, int64_t ld, uint32_t p,
+                                uint64_t seed, uint32_t stream_id, int64_t index0,
+                                cudaStream_t st);
+
+int num_sms();
+
+}  // namespace ff

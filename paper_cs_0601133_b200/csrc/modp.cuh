@@ -1,0 +1,45 @@
+// modp.cuh -- 32-bit residue arithmetic used by the encoder and the GEMM epilogue.
+//
+// The paper's "floating point inverse" representation:
+// "precompute the inverse of the characteristic p ... only two floating point
+// multiplications and some rounding are necessary.  However, floating point
+// rounding may induce a +-1 error and then an adjustment is required".  We use
+// the integer form of that idea: a precomputed fixed-point inverse (Barrett's
+// mu = floor(2^32/p), Shoup's w' = floor(w 2^32/p)), one __umulhi, and one
+// conditional correction.  Valid for 2 <= p < 2^31.
+#pragma once
+#include <cstdint>
+
+#include "internal.h"
+
+namespace ff {
+
+// Any int32 -> its Euclidean residue in [0, p).
+// x = a + 2^31 in [0, 2^32); q = floor(x mu / 2^32) is floor(x/p) or one less,
+// so x - q p is in [0, 2p); then remove 2^31 mod p.
+__device__ __forceinline__ uint32_t residue_i32(int32_t a, const ModP& M) {
+    const uint32_t x = static_cast<uint32_t>(a) ^ 0x80000000u;
+    const uint32_t q = __umulhi(x, M.mu);
+    uint32_t r = x - q * M.p;
+    if (r >= M.p) r -= M.p;
+    return r >= M.off31 ? r - M.off31 : r + (M.p - M.off31);
+}
+
+// a * w mod p for a, w in [0, p), w_sh = floor(w 2^32 / p)  (Shoup).
+__device__ __forceinline__ uint32_t mulmod_shoup(uint32_t a, uint32_t w, uint32_t w_sh, uint32_t p) {
+    const uint32_t q = __umulhi(a, w_sh);
+    uint32_t r = a * w - q * p;
+    return r >= p ? r - p : r;
+}
+
+// [0,p) -> centred [-(p-1)/2, (p-1)/2]  (balanced representation).
+__device__ __forceinline__ int32_t centre(uint32_t r, const ModP& M) {
+    return r > M.half ? static_cast<int32_t>(r) - static_cast<int32_t>(M.p) : static_cast<int32_t>(r);
+}
+
+__device__ __forceinline__ uint32_t addmod(uint32_t a, uint32_t b, uint32_t p) {
+    const uint32_t s = a + b;  // < 2p < 2^32
+    return s >= p ? s - p : s;
+}
+
+}  // namespace ff

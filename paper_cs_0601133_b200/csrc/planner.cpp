@@ -1,0 +1,161 @@
+// planner.cpp -- host planner: limb scheme, digit bounds, k-block length.
+//
+// The paper bounds delayed reduction by the accumulator width: for centred
+// residues, lambda ((p-1)/2)^2 < 2^(gamma-1) (Eq. (2)), so
+// that ceil(n/lambda) reductions suffice per dot product (l.159).  Here the
+// products are of int8 limbs d_i in [-D_i, D_i] and the accumulator is the
+// s32 TMEM cell (gamma = 32), which also carries one centred residue written
+// back between k-blocks / weight groups (|carry| <= (p-1)/2).  So a k-block
+// of kb terms of weight group w = i+j is safe iff
+//
+//      kb * B_w + (p-1)/2 <= 2^31 - 1,      B_w = sum_{i+j=w} D_i D_j,
+//
+// giving kb_max = floor((2^31 - 1 - (p-1)/2) / max_w B_w)  (
+// the "one extra carried term" form matches the paper's own t_update values,
+// l.524-527, which satisfy (t+1)(p-1)^2 < 2^53 exactly).
+#include <cstring>
+
+#include "internal.h"
+
+namespace ff {
+
+namespace {
+
+// Digit stripping.  Both maps are monotone non-decreasing in
+// c, so the range of the top digit is [top(-half), top(half)].
+//   S: d = ((c+128) mod 256) - 128, c <- (c - d)/256 = floor((c+128)/256)
+//   T: d = c mod 256 (u8),          c <- floor(c/256)
+int64_t floor_div(int64_t a, int64_t b) {
+    int64_t q = a / b;
+    if ((a % b) != 0 && ((a < 0) != (b < 0))) --q;
+    return q;
+}
+
+int64_t strip(int64_t c, int scheme) {
+    return scheme == FF_SCHEME_S ? floor_div(c + 128, 256) : floor_div(c, 256);
+}
+
+int64_t top_digit(int64_t c, int L, int scheme) {
+    for (int i = 0; i + 1 < L; ++i) c = strip(c, scheme);
+    return c;
+}
+
+bool feasible(int64_t half, int64_t neg, int L, int scheme) {
+    int64_t hi = top_digit(half, L, scheme), lo = top_digit(-neg, L, scheme);
+    return hi <= 127 && lo >= -128;
+}
+
+int min_limbs(int64_t half, int64_t neg, int scheme) {
+    for (int L = 1; L <= kMaxLimbs; ++L)
+        if (feasible(half, neg, L, scheme)) return L;
+    return 0;
+}
+
+uint32_t shoup(uint32_t w, uint32_t p) {
+    return (uint32_t)(((uint64_t)w << 32) / p);
+}
+
+}  // namespace
+
+int make_plan(uint32_t p, int64_t k, const ff_opts* opts, Plan* out) {
+    if (p < 2 || p >= (1u << 31)) return -1;
+    if (k < 0) return -6;
+    ff_opts o;
+    std::memset(&o, 0, sizeof(o));
+    if (opts) o = *opts;
+    if (o.scheme < FF_SCHEME_AUTO || o.scheme > FF_SCHEME_T) return FF_ERR_OPTS;
+    if (o.winograd < -1 || o.winograd > 1) return FF_ERR_OPTS;
+    if (o.kb_override < 0) return FF_ERR_OPTS;
+
+    Plan pl;
+    std::memset(&pl, 0, sizeof(pl));
+    ff_plan_info& I = pl.info;
+    // Centred residues lie in [-neg, half]: neg = half for odd p, half + 1 for p = 2.
+    const int64_t half = (int64_t)(p - 1) / 2;
+    const int64_t neg = (int64_t)(p - 1) - half;
+    const int64_t cmax = neg > half ? neg : half;
+    I.p = p;
+    I.centre_max = (int32_t)cmax;
+
+    const int LS = min_limbs(half, neg, FF_SCHEME_S), LT = min_limbs(half, neg, FF_SCHEME_T);
+    int scheme = o.scheme;
+    if (scheme == FF_SCHEME_AUTO) scheme = (LS != 0 && (LT == 0 || LS <= LT)) ? FF_SCHEME_S : FF_SCHEME_T;
+    const int L = scheme == FF_SCHEME_S ? LS : LT;
+    if (L == 0) return FF_ERR_INTERNAL;
+    I.L = L;
+    I.scheme = scheme;
+    I.groups = 2 * L - 1;
+
+    // Digit magnitude bounds D_i.
+    for (int i = 0; i < L; ++i) {
+        const bool top = (i == L - 1);
+        if (top) {
+            int64_t hi = top_digit(half, L, scheme), lo = top_digit(-neg, L, scheme);
+            I.digit_max[i] = (int32_t)(hi > -lo ? hi : -lo);
+            I.limb_signed[i] = 1;
+        } else {
+            I.digit_max[i] = scheme == FF_SCHEME_S ? 128 : 255;
+            I.limb_signed[i] = scheme == FF_SCHEME_S ? 1 : 0;
+        }
+    }
+    int64_t bmax = 0;
+    for (int w = 0; w < I.groups; ++w) {
+        int64_t b = 0;
+        for (int i = 0; i < L; ++i) {
+            int j = w - i;
+            if (j >= 0 && j < L) b += (int64_t)I.digit_max[i] * I.digit_max[j];
+        }
+        I.group_bound[w] = b;
+        if (b > bmax) bmax = b;
+    }
+    I.group_bound_max = bmax;
+    I.kb_max = bmax > 0 ? (((int64_t)1 << 31) - 1 - cmax) / bmax : ((int64_t)1 << 40);
+    int64_t kb = I.kb_max;
+    if (o.kb_override > 0) {
+        if (o.kb_override > I.kb_max || o.kb_override < kBK) return FF_ERR_OPTS;
+        kb = o.kb_override;
+    }
+    kb = (kb / kBK) * kBK;
+    if (kb < kBK) return FF_ERR_INTERNAL;
+    I.kb = kb;
+    I.k_pad = (k + 15) / 16 * 16;
+    I.num_kblocks = k > 0 ? (k + kb - 1) / kb : 0;
+
+    // Pairs (i,j) ordered by weight group, highest w first (Horner order).
+    int np = 0;
+    for (int w = I.groups - 1; w >= 0; --w) {
+        pl.group_first[w] = np;
+        for (int i = 0; i < L; ++i) {
+            int j = w - i;
+            if (j >= 0 && j < L) {
+                pl.pair_i[np] = i;
+                pl.pair_j[np] = j;
+                ++np;
+            }
+        }
+        pl.group_len[w] = np - pl.group_first[w];
+    }
+    pl.npairs = np;
+    pl.saturate = o.debug_saturate != 0;
+
+    ModP& M = pl.mp;
+    M.p = p;
+    M.half = (uint32_t)half;
+    M.mu = (uint32_t)((((uint64_t)1) << 32) / p);
+    M.off31 = (uint32_t)((((uint64_t)1) << 31) % p);
+    M.w256 = 256u % p;
+    M.w256_sh = shoup(M.w256, p);
+    *out = pl;
+    set_scalars(out, 1, 0);
+    return 0;
+}
+
+void set_scalars(Plan* pl, uint32_t alpha, uint32_t beta) {
+    const uint32_t p = pl->mp.p;
+    pl->mp.alpha = alpha % p;
+    pl->mp.beta = beta % p;
+    pl->mp.alpha_sh = shoup(pl->mp.alpha, p);
+    pl->mp.beta_sh = shoup(pl->mp.beta, p);
+}
+
+}  // namespace ff

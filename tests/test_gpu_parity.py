@@ -1,0 +1,341 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle,
+element by element, bit-exact (integer work: no tolerance).
+
+Small/medium sizes run the full oracle; the BASELINE configs at full size are
+checked on sampled rows (computed one by one by the oracle) plus Freivalds'
+test on the whole output.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import ffgen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+CONFIG_PRIMES = [251, 65521, 8388593, 67108859]
+SMALL_PRIMES = [2, 3, 5, 7, 257, 65279, 65537, 16711423, 2 ** 31 - 1]
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+    import paper_cs_0601133_b200 as ff
+    assert torch.cuda.is_available()
+    assert ff.ff_device_check(0) == 0, "device 0 is not sm_100"
+    torch.cuda.set_device(0)
+    return torch, ff
+
+
+def _dev(torch, x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def _stored(rng, rows, cols, p, ld_extra=0, lo=0):
+    buf = rng.integers(lo, p, size=(rows, cols + ld_extra), dtype=np.int64).astype(np.int32)
+    return buf
+
+
+def _run_gpu(torch, ff, p, tA, tB, m, n, k, alpha, Abuf, Bbuf, beta, Cbuf, opts=None):
+    """Run through the C ABI on device copies of the stored buffers (ld = buffer width)."""
+    A, B, C = _dev(torch, Abuf), _dev(torch, Bbuf), _dev(torch, Cbuf)
+    ff.ff_gemm_ex(p, tA, tB, m, n, k, alpha, A, Abuf.shape[1], B, Bbuf.shape[1], beta, C,
+                  Cbuf.shape[1], opts)
+    torch.cuda.synchronize()
+    return C.cpu().numpy()
+
+
+def _check(p, tA, tB, m, n, k, alpha, Abuf, Bbuf, beta, Cbuf, got):
+    a_cols = k if tA == "N" else m
+    b_cols = n if tB == "N" else k
+    want = oracle.fgemm(p, tA, tB, alpha, Abuf[:, :a_cols], Bbuf[:, :b_cols], beta,
+                        Cbuf[:, :n], m=m, n=n, k=k)
+    np.testing.assert_array_equal(got[:m, :n], want)
+    # the leading-dimension padding of C is never written
+    np.testing.assert_array_equal(got[:, n:], Cbuf[:, n:])
+
+
+# ---------------------------------------------------------------- generator twin
+
+def test_fill_uniform_matches_numpy_generator(env):
+    torch, ff = env
+    for p, seed, stream, rows, cols, ld, i0 in [(65521, 1, 0, 37, 53, 60, 0),
+                                               (67108859, 5, 2, 300, 129, 129, 0),
+                                               (251, 3, 1, 10, 1000, 1000, 777)]:
+        X = torch.full((rows, ld), -7, dtype=torch.int32, device="cuda")
+        ff.ff_fill_uniform(X, rows, cols, ld, p, seed, stream, i0)
+        torch.cuda.synchronize()
+        got = X.cpu().numpy()
+        want = ffgen.uniform_flat(p, seed, stream, i0, rows * cols).reshape(rows, cols)
+        np.testing.assert_array_equal(got[:, :cols], want)
+        assert (got[:, cols:] == -7).all()
+
+
+# ---------------------------------------------------------------- encoder
+
+def _decode(limbs, info):
+    """Host decode of limb planes: sum_i d_i 256^i with the plan's signedness."""
+    L = info["L"]
+    acc = np.zeros(limbs.shape[1:], dtype=np.int64)
+    for i in range(L - 1, -1, -1):
+        d = limbs[i].astype(np.int64)
+        d = np.where(d < 0, d + 256, d) if not info["limb_signed"][i] else d
+        acc = acc * 256 + d
+    return acc
+
+
+@pytest.mark.parametrize("p", CONFIG_PRIMES + [2, 3, 257, 65537, 2 ** 31 - 1])
+@pytest.mark.parametrize("kmajor", [1, 0])
+def test_encoder_roundtrip(env, p, kmajor):
+    torch, ff = env
+    rng = np.random.default_rng(p % 997 + kmajor)
+    rows, k = 150, 333      # ragged: not multiples of the 64/16 encoder tiles
+    info = ff.ff_plan_query(p, k)
+    x = rng.integers(-2 ** 31, 2 ** 31, size=(rows, k), dtype=np.int64).astype(np.int32)
+    x[0, :min(k, p)] = np.arange(min(k, p))                       # include 0..p-1 verbatim
+    src = x if kmajor else np.ascontiguousarray(x.T)
+    X = _dev(torch, src)
+    limbs = torch.full((info["L"], rows, info["k_pad"]), 99, dtype=torch.int8, device="cuda")
+    ff.ff_encode(p, k, None, kmajor, rows, X, src.shape[1], limbs)
+    torch.cuda.synchronize()
+    lb = limbs.cpu().numpy()
+    r = np.mod(x.astype(np.int64), p)
+    c = np.where(r > (p - 1) // 2, r - p, r)
+    np.testing.assert_array_equal(_decode(lb, info)[:, :k], c)
+    assert (lb[:, :, k:] == 0).all()                              # zero K padding
+    for i in range(info["L"]):
+        d = lb[i].astype(np.int64)
+        if not info["limb_signed"][i]:
+            d = np.where(d < 0, d + 256, d)
+        assert np.abs(d).max() <= info["digit_max"][i]
+
+
+@pytest.mark.parametrize("p", CONFIG_PRIMES)
+def test_encoder_exhaustive_residues(env, p):
+    """decode(encode(r)) = centre(r) for every residue r in [0, p) (p <= 2^26)."""
+    torch, ff = env
+    k = 4096
+    rows = (p + k - 1) // k
+    vals = np.arange(rows * k, dtype=np.int64) % p
+    X = _dev(torch, vals.astype(np.int32).reshape(rows, k))
+    info = ff.ff_plan_query(p, k)
+    limbs = torch.empty((info["L"], rows, info["k_pad"]), dtype=torch.int8, device="cuda")
+    ff.ff_encode(p, k, None, 1, rows, X, k, limbs)
+    torch.cuda.synchronize()
+    dec = _decode(limbs.cpu().numpy(), info).reshape(-1)
+    want = np.where(vals > (p - 1) // 2, vals - p, vals)
+    np.testing.assert_array_equal(dec, want)
+
+
+# ---------------------------------------------------------------- GEMM parity, small/medium
+
+SHAPES = [(1, 1, 1), (3, 5, 7), (128, 256, 128), (129, 257, 129), (200, 300, 1000),
+          (256, 512, 640), (77, 600, 33)]
+
+
+@pytest.mark.parametrize("p", CONFIG_PRIMES)
+@pytest.mark.parametrize("tA,tB", [("N", "N"), ("T", "N"), ("N", "T"), ("T", "T")])
+def test_gemm_vs_oracle_shapes(env, p, tA, tB):
+    torch, ff = env
+    rng = np.random.default_rng(p % 1009 + ord(tA) * 3 + ord(tB))
+    for si, (m, n, k) in enumerate(SHAPES):
+        ldx = si % 3
+        Abuf = _stored(rng, *((m, k) if tA == "N" else (k, m)), p, ldx)
+        Bbuf = _stored(rng, *((k, n) if tB == "N" else (n, k)), p, 2 * ldx)
+        Cbuf = _stored(rng, m, n, p, ldx + 1)
+        alpha = [1, p - 1, 3, int(rng.integers(0, p))][si % 4]
+        beta = [0, 1, p - 1, int(rng.integers(0, p))][(si + 1) % 4]
+        got = _run_gpu(torch, ff, p, tA, tB, m, n, k, alpha, Abuf, Bbuf, beta, Cbuf)
+        _check(p, tA, tB, m, n, k, alpha, Abuf, Bbuf, beta, Cbuf, got)
+
+
+@pytest.mark.parametrize("p", SMALL_PRIMES)
+def test_gemm_other_primes_and_noncanonical_inputs(env, p):
+    torch, ff = env
+    rng = np.random.default_rng(p % 10007)
+    m, n, k = 190, 300, 450
+    Abuf = rng.integers(-2 ** 31, 2 ** 31, size=(m, k), dtype=np.int64).astype(np.int32)
+    Bbuf = rng.integers(-2 ** 31, 2 ** 31, size=(k, n), dtype=np.int64).astype(np.int32)
+    Cbuf = rng.integers(-2 ** 31, 2 ** 31, size=(m, n), dtype=np.int64).astype(np.int32)
+    for alpha, beta in [(1, 0), (2 ** 32 - 1, 2 ** 32 - 1), (p - 1, 1)]:
+        got = _run_gpu(torch, ff, p, "N", "N", m, n, k, alpha, Abuf, Bbuf, beta, Cbuf)
+        _check(p, "N", "N", m, n, k, alpha, Abuf, Bbuf, beta, Cbuf, got)
+
+
+@pytest.mark.parametrize("p,scheme", [(65521, 2), (65521, 1), (8388593, 1), (67108859, 1),
+                                      (251, 1), (8388593, 2)])
+def test_kb_override_forces_mid_k_reductions(env, p, scheme):
+    """Shrunk k-block ("overflow safety under shrunk gamma" analogue):
+    several mid-k reductions per weight group must not change the result."""
+    torch, ff = env
+    rng = np.random.default_rng(11)
+    m, n, k = 130, 260, 1000
+    Abuf, Bbuf, Cbuf = _stored(rng, m, k, p), _stored(rng, k, n, p), _stored(rng, m, n, p)
+    opts = {"kb_override": 128, "scheme": scheme}
+    assert ff.ff_plan_query(p, k, opts)["num_kblocks"] == 8
+    got = _run_gpu(torch, ff, p, "N", "N", m, n, k, 5, Abuf, Bbuf, 7, Cbuf, opts)
+    _check(p, "N", "N", m, n, k, 5, Abuf, Bbuf, 7, Cbuf, got)
+
+
+def _adversarial_residue(p, info):
+    """A residue whose limbs attain the digit bound of every limb (|d_i| = D_i)."""
+    L = info["L"]
+    if info["scheme"] == "T":
+        # low bytes 255, top byte -128  (p = 65521: c = -32513, residue 33008)
+        c = -128 * 256 ** (L - 1) + sum(255 * 256 ** i for i in range(L - 1))
+    else:
+        top = -info["digit_max"][-1]
+        c = top * 256 ** (L - 1) + sum(-128 * 256 ** i for i in range(L - 1))
+        while c < -((p - 1) // 2):       # stay inside the centred range
+            top += 1
+            c += 256 ** (L - 1)
+    assert -((p - 1) // 2) <= c <= (p - 1) // 2
+    return c % p
+
+
+@pytest.mark.parametrize("p", CONFIG_PRIMES)
+def test_accumulator_at_the_bound_closed_form(env, p):
+    """All entries = a digit-extreme residue v, k = the planner's largest k-block
+    (and 2 k-blocks + a ragged tail): every entry must be k v^2 mod p."""
+    torch, ff = env
+    info = ff.ff_plan_query(p, 1)
+    v = _adversarial_residue(p, info)
+    if p == 65521:
+        assert v == 33008
+    for k in (info["kb"], 2 * info["kb"] + 45):
+        m, n = 128, 256
+        A = torch.full((m, k), v, dtype=torch.int32, device="cuda")
+        B = torch.full((k, n), v, dtype=torch.int32, device="cuda")
+        C = torch.empty((m, n), dtype=torch.int32, device="cuda")
+        for sat in (0, 1):
+            ff.ff_gemm_ex(p, "N", "N", m, n, k, 1, A, k, B, n, 0, C, n, {"debug_saturate": sat})
+            torch.cuda.synchronize()
+            assert (C == (k * v * v) % p).all().item(), (p, k, sat)
+
+
+def test_quick_returns_and_degenerate(env):
+    torch, ff = env
+    p = 65521
+    rng = np.random.default_rng(3)
+    Cbuf = _stored(rng, 70, 90, p, 3)
+    A = _stored(rng, 70, 0 + 1, p)
+    B = _stored(rng, 1, 90, p)
+    # k = 0: C <- beta C
+    got = _run_gpu(torch, ff, p, "N", "N", 70, 90, 0, 5, A, B, 3, Cbuf)
+    np.testing.assert_array_equal(got[:, :90], (3 * Cbuf[:, :90].astype(np.int64)) % p)
+    # alpha = 0: C <- beta C
+    got = _run_gpu(torch, ff, p, "N", "N", 70, 90, 1, 0, A, B, 2, Cbuf)
+    np.testing.assert_array_equal(got[:, :90], (2 * Cbuf[:, :90].astype(np.int64)) % p)
+    # beta = 0: C is not read (garbage in, exact product out)
+    junk = np.full_like(Cbuf, -1)
+    got = _run_gpu(torch, ff, p, "N", "N", 70, 90, 1, 1, A, B, 0, junk)
+    _check(p, "N", "N", 70, 90, 1, 1, A, B, 0, junk, got)
+    # m = 0 / n = 0: no-op
+    C = _dev(torch, Cbuf)
+    ff.ff_gemm_ex(p, "N", "N", 0, 90, 5, 1, C, 5, C, 93, 1, C, 93)
+    ff.ff_gemm_ex(p, "N", "N", 70, 0, 5, 1, C, 5, C, 1, 1, C, 93)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(C.cpu().numpy(), Cbuf)
+
+
+def test_identity_permutation_on_gpu(env):
+    torch, ff = env
+    p = 67108859
+    rng = np.random.default_rng(4)
+    n = 300
+    sigma = rng.permutation(n)
+    P = np.zeros((n, n), dtype=np.int32)
+    P[np.arange(n), sigma] = 1
+    B = _stored(rng, n, 270, p)
+    got = _run_gpu(torch, ff, p, "N", "N", n, 270, n, 1, P, B, 0, np.zeros((n, 270), np.int32))
+    np.testing.assert_array_equal(got, B[sigma])
+
+
+def test_host_entry_point(env):
+    torch, ff = env
+    p = 8388593
+    rng = np.random.default_rng(5)
+    m, n, k = 333, 444, 555
+    A, B, C = _stored(rng, k, m, p, 1), _stored(rng, k, n, p, 2), _stored(rng, m, n, p, 3)
+    out = C.copy()
+    ff.ff_gemm_host(p, "T", "N", m, n, k, 3, A, A.shape[1], B, B.shape[1], 1, out, out.shape[1])
+    _check(p, "T", "N", m, n, k, 3, A, B, 1, C, out)
+
+
+def test_split_entry_points_chunked_B(env):
+    """Encode once, multiply by column chunks of B (the multi-GPU building block)."""
+    torch, ff = env
+    p = 65521
+    rng = np.random.default_rng(6)
+    m, n, k = 300, 700, 900
+    A, B, C = _stored(rng, m, k, p), _stored(rng, k, n, p), _stored(rng, m, n, p)
+    info = ff.ff_plan_query(p, k)
+    L, kp = info["L"], info["k_pad"]
+    dA, dB, dC = _dev(torch, A), _dev(torch, B), _dev(torch, C)
+    Al = torch.empty((L, m, kp), dtype=torch.int8, device="cuda")
+    ff.ff_encode(p, k, None, 1, m, dA, k, Al)
+    for n0, n1 in [(0, 256), (256, 300), (300, 700)]:
+        Bl = torch.empty((L, n1 - n0, kp), dtype=torch.int8, device="cuda")
+        ff.ff_encode(p, k, None, 0, n1 - n0, dB[:, n0:], n, Bl)
+        ff.ff_gemm_limbs(p, m, n1 - n0, k, None, 7, Al, Bl, 2, dC[:, n0:], n)
+    torch.cuda.synchronize()
+    want = oracle.fgemm(p, "N", "N", 7, A, B, 2, C)
+    np.testing.assert_array_equal(dC.cpu().numpy(), want)
+
+
+# ---------------------------------------------------------------- BASELINE configs, full size
+
+CONFIGS = {
+    # name: (p, m, n, k, transA, transB, alpha, beta, seed)
+    "c1": (65521, 512, 512, 512, "N", "N", 1, 0, 1),
+    "c2": (8388593, 4096, 4096, 4096, "N", "N", 3, 1, 2),
+    "c3": (251, 8192, 8192, 16384, "T", "N", 1, 0, 3),
+    "c4": (65521, 32768, 32768, 8192, "N", "N", 1, 0, 4),
+    "c5": (67108859, 16384, 16384, 16384, "N", "N", 67108858, 1, 5),
+}
+
+
+def _make_config(torch, ff, name):
+    p, m, n, k, tA, tB, alpha, beta, seed = CONFIGS[name]
+    ar, ac = (m, k) if tA == "N" else (k, m)
+    br, bc = (k, n) if tB == "N" else (n, k)
+    A = torch.empty((ar, ac), dtype=torch.int32, device="cuda")
+    B = torch.empty((br, bc), dtype=torch.int32, device="cuda")
+    C = torch.empty((m, n), dtype=torch.int32, device="cuda")
+    ff.ff_fill_uniform(A, ar, ac, ac, p, seed, ffgen.STREAM_A)
+    ff.ff_fill_uniform(B, br, bc, bc, p, seed, ffgen.STREAM_B)
+    if beta:
+        ff.ff_fill_uniform(C, m, n, n, p, seed, ffgen.STREAM_C)
+    return A, B, C
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
+def test_baseline_config_sampled_rows_and_freivalds(env, name):
+    torch, ff = env
+    p, m, n, k, tA, tB, alpha, beta, seed = CONFIGS[name]
+    A, B, C = _make_config(torch, ff, name)
+    Cin = C.cpu().numpy() if beta else None
+    ff.fgemm(p, A, B, C, alpha, beta, tA, tB)
+    torch.cuda.synchronize()
+    out = C.cpu().numpy()
+    Ah, Bh = A.cpu().numpy(), B.cpu().numpy()
+    # inputs are exactly the seeded generator's (no CUDA-side value is trusted)
+    np.testing.assert_array_equal(Ah[:3], ffgen.uniform_matrix(p, seed, 0, *Ah.shape, row0=0, nrows=3))
+    rng = np.random.default_rng(seed)
+    rows = sorted(set([0, m - 1, 127, 128, m // 2] + rng.integers(0, m, size=5).tolist()))
+    want = oracle.fgemm_rows(p, tA, tB, alpha, Ah, Bh, beta,
+                             Cin[rows] if beta else None, rows, m, n, k)
+    np.testing.assert_array_equal(out[rows], want)
+    # Freivalds (t = 4): C_out x = alpha A (B x) + beta C_in x  (mod p), x random
+    for t in range(4):
+        x = ffgen.uniform_vector(p, seed, 8 + t, n)
+        lhs = oracle.matvec(p, "N", out, x).astype(np.int64)
+        bx = oracle.matvec(p, tB, Bh, x)
+        abx = oracle.matvec(p, tA, Ah, bx).astype(np.int64)
+        rhs = (alpha % p) * abx % p
+        if beta:
+            rhs = (rhs + (beta % p) * oracle.matvec(p, "N", Cin, x).astype(np.int64)) % p
+        np.testing.assert_array_equal(lhs, rhs)
+    assert out.min() >= 0 and out.max() < p

@@ -1,0 +1,170 @@
+"""Host-side checks of the CUDA library (no GPU needed): it loads, exports
+every symbol include/ffgemm.h declares, validates arguments in BLAS xerbla
+order, and its planner reproduces the delayed-reduction bounds derived
+independently here from the paper's Eq. (2)."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def ff():
+    from paper_cs_0601133_b200 import build
+    build.build()
+    import paper_cs_0601133_b200 as ff
+    return ff
+
+
+def _declared_symbols():
+    src = open(os.path.join(ROOT, "include", "ffgemm.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(ff_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_every_declared_symbol_is_exported(ff):
+    lib = ctypes.CDLL(ff.LIB_PATH)
+    declared = _declared_symbols()
+    assert len(declared) >= 11
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert set(declared) == set(ff.EXPORTED)
+
+
+def test_binary_is_sm100a_tcgen05(ff):
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", ff.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-lelf", ff.LIB_PATH],
+                                       capture_output=True, text=True).stdout
+    for mnemonic in ("UTCIMMA", "UTMALDG", "LDTM", "STTM"):
+        assert mnemonic in out, mnemonic
+
+
+def test_version_and_strerror(ff):
+    assert ff.ff_version() >= 100
+    for code in (0, 1, 2, 3, 4, 5, -1, -9, -14, 99):
+        assert isinstance(ff.ff_strerror(code), str) and ff.ff_strerror(code)
+
+
+@pytest.mark.parametrize("args,code", [
+    ((1, b"N", b"N", 2, 2, 2), -1),            # p < 2
+    ((2 ** 31, b"N", b"N", 2, 2, 2), -1),      # p >= 2^31
+    ((5, b"X", b"N", 2, 2, 2), -2),
+    ((5, b"N", b"Q", 2, 2, 2), -3),
+    ((5, b"N", b"N", -1, 2, 2), -4),
+    ((5, b"N", b"N", 2, -1, 2), -5),
+    ((5, b"N", b"N", 2, 2, -1), -6),
+])
+def test_argument_errors_in_xerbla_order(ff, args, code):
+    lib = ctypes.CDLL(ff.LIB_PATH)
+    lib.ff_gemm.argtypes = ff.ffgemm._lib.ff_gemm.argtypes
+    p, ta, tb, m, n, k = args
+    dummy = 4096
+    assert lib.ff_gemm(p, ta, tb, m, n, k, 1, dummy, 8, dummy, 8, 0, dummy, 8) == code
+
+
+def test_ld_and_null_errors(ff):
+    g = ff.ffgemm._lib.ff_gemm
+    d = 4096
+    assert g(5, b"N", b"N", 4, 3, 6, 1, None, 6, d, 3, 0, d, 3) == -8
+    assert g(5, b"N", b"N", 4, 3, 6, 1, d, 5, d, 3, 0, d, 3) == -9     # lda < k
+    assert g(5, b"T", b"N", 4, 3, 6, 1, d, 3, d, 3, 0, d, 3) == -9     # lda < m
+    assert g(5, b"N", b"N", 4, 3, 6, 1, d, 6, None, 3, 0, d, 3) == -10
+    assert g(5, b"N", b"N", 4, 3, 6, 1, d, 6, d, 2, 0, d, 3) == -11    # ldb < n
+    assert g(5, b"N", b"T", 4, 3, 6, 1, d, 6, d, 5, 0, d, 3) == -11    # ldb < k
+    assert g(5, b"N", b"N", 4, 3, 6, 1, d, 6, d, 3, 0, None, 3) == -13
+    assert g(5, b"N", b"N", 4, 3, 6, 1, d, 6, d, 3, 0, d, 2) == -14
+    # m = 0 or n = 0 is a successful no-op that never touches the GPU
+    assert g(5, b"N", b"N", 0, 3, 6, 1, None, 6, d, 3, 0, None, 3) == 0
+
+
+# ---------------------------------------------------------------- planner vs Eq. (2)
+
+def _balanced_digits(c, L):
+    """Test-side digit split, written from the definition c = sum d_i 256^i with
+    d_i in [-128, 127] chosen as the residue of c mod 256 nearest to zero."""
+    out = []
+    for _ in range(L):
+        d = ((c + 128) % 256) - 128
+        out.append(d)
+        c = (c - d) // 256
+    return out, c
+
+
+def _twos_digits(c, L):
+    out = []
+    for i in range(L - 1):
+        out.append(c % 256)
+        c //= 256
+    out.append(c)
+    return out, 0 if -128 <= c <= 127 else c
+
+
+def _centred_all(p):
+    r = np.arange(p, dtype=np.int64)
+    return np.where(r > (p - 1) // 2, r - p, r)
+
+
+@pytest.mark.parametrize("p,L,scheme,D,kb_max", [
+    (65521, 2, "T", [255, 128], 32896),          # c1, c4
+    (8388593, 3, "S", [128, 128, 64], 65408),    # c2
+    (251, 1, "S", [125], 137438),                # c3
+    (67108859, 4, "S", [128, 128, 128, 2], 43008),  # c5
+])
+def test_planner_matches_paper_bound(ff, p, L, scheme, D, kb_max):
+    info = ff.ff_plan_query(p, 1000)
+    assert info["L"] == L and info["scheme"] == scheme
+    assert info["digit_max"] == D
+    # Eq. (2) with gamma = 32 for the s32 accumulator, per weight group, plus one
+    # centred carry: kb * max_w B_w + (p-1)/2 <= 2^31 - 1.
+    B = [sum(D[i] * D[w - i] for i in range(L) if 0 <= w - i < L) for w in range(2 * L - 1)]
+    assert info["group_bound"] == B
+    half = (p - 1) // 2
+    assert info["kb_max"] == kb_max == (2 ** 31 - 1 - half) // max(B)
+    assert kb_max * max(B) + half <= 2 ** 31 - 1 < (kb_max + 1) * max(B) + half
+    assert info["kb"] % 128 == 0 and info["kb"] <= kb_max
+    # every config fits one k-block ("none of the 5 needs it")
+    for k in (512, 4096, 8192, 16384):
+        assert ff.ff_plan_query(p, k)["num_kblocks"] == 1
+
+
+@pytest.mark.parametrize("p", [2, 3, 5, 251, 257, 65279, 65521, 65537])
+def test_digit_bounds_exhaustive_small_primes(ff, p):
+    info = ff.ff_plan_query(p, 64)
+    L = info["L"]
+    split = _balanced_digits if info["scheme"] == "S" else _twos_digits
+    seen = [0] * L
+    for c in _centred_all(p).tolist():
+        d, rest = split(c, L)
+        assert rest == 0, (p, c)
+        assert sum(di * 256 ** i for i, di in enumerate(d)) == c
+        seen = [max(s, abs(di)) for s, di in zip(seen, d)]
+    # the planner's bound is attained (tight) for the top digit and safe elsewhere
+    assert seen[-1] == info["digit_max"][-1]
+    assert all(s <= dm for s, dm in zip(seen, info["digit_max"]))
+    # minimality of L: one limb fewer cannot represent all residues
+    if L > 1:
+        for other in (_balanced_digits, _twos_digits):
+            assert any(other(c, L - 1)[1] != 0 for c in _centred_all(p).tolist())
+
+
+def test_scheme_choice_rule(ff):
+    # S is used unless only T reaches the smaller L:
+    assert ff.ff_plan_query(65279, 8)["scheme"] == "S"   # 2 balanced digits reach +-32639
+    assert ff.ff_plan_query(65521, 8)["scheme"] == "T"   # centred +-32760 needs T for L=2
+    assert ff.ff_plan_query(65521, 8, {"scheme": 1})["L"] == 3
+    assert ff.ff_plan_query(2 ** 31 - 1, 8)["L"] == 4
+
+
+def test_kb_override_rules(ff):
+    info = ff.ff_plan_query(65521, 5000, {"kb_override": 1000})
+    assert info["kb"] == 896 and info["num_kblocks"] == 6
+    with pytest.raises(ff.FFError):
+        ff.ff_plan_query(65521, 5000, {"kb_override": 40000})   # above the safe bound
+    with pytest.raises(ff.FFError):
+        ff.ff_plan_query(65521, 5000, {"kb_override": 64})      # below one stage
