@@ -73,7 +73,9 @@ typedef struct ff_opts {
                                safe bound (else FF_ERR_OPTS).  Forces mid-k reductions. */
     int32_t debug_saturate; /* 1: set the MMA saturate bit (test builds only; a clamp
                                then shows as a mismatch instead of a silent wrap) */
-    int32_t reserved[7];
+    int32_t cta_group;      /* 0 auto; 1 force the 128x256 single-CTA kernel; 2 force the
+                               256x256 CTA-pair (tcgen05 cta_group::2) kernel */
+    int32_t reserved[6];
 } ff_opts;
 
 /* The plan the library derives from (p, k, opts): host-only, no GPU needed. */
@@ -86,12 +88,15 @@ typedef struct ff_plan_info {
     int32_t digit_max[4];    /* D_i = max |limb i| over all centred residues */
     int64_t group_bound[7];  /* B_w = sum_{i+j=w} D_i D_j  (per unit of k) */
     int64_t group_bound_max; /* max_w B_w */
-    int64_t kb_max;          /* floor((2^31-1-(p-1)/2) / max_w B_w): Eq. (2) analogue */
+    int64_t kb_max;          /* floor((2^31-1-carry_max) / max_w B_w): Eq. (2) analogue */
     int64_t kb;              /* k-block actually used (multiple of 128, <= kb_max) */
     int64_t k_pad;           /* k rounded up to a multiple of 16 (limb plane row length) */
     int64_t num_kblocks;     /* ceil(k / kb); 1 for every BASELINE config */
-    int32_t centre_max;      /* (p-1)/2 */
-    int32_t reserved[5];
+    int32_t centre_max;      /* (p-1)/2 (p/2 for p = 2) */
+    int32_t reserved0;
+    int64_t carry_max;       /* bound on |value| written back into the accumulator
+                                between steps: centre_max + 385 w (w = 256 if L >= 2) */
+    int32_t reserved[2];
 } ff_plan_info;
 
 /* Library version (major*10000 + minor*100 + patch). Host only. */

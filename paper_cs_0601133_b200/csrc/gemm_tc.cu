@@ -2,7 +2,7 @@
 // tensor cores (tcgen05.mma.kind::i8 -> s32 in TMEM) with the delayed modular
 // reduction, limb recombination and alpha/beta epilogue fused in.
 //
-// What it computes, per 128x256 output tile:
+// What it computes, per output tile:
 //   op(A) = sum_i 256^i Ad_i,  op(B) = sum_j 256^j Bd_j   (int8 limb planes)
 //   A B   = sum_w 256^w S_w,   S_w = sum_{i+j=w} Ad_i Bd_j^T   (weight groups)
 //   Horner over w from 2L-2 down to 0, one TMEM accumulator per tile:
@@ -12,17 +12,24 @@
 // by 256 mod p, and (b) every kb elements of k (the Eq. (2) analogue computed
 // by the planner).  Nothing is ever rounded: the result is exact.
 //
-// Structure (one CTA per SM, persistent, warp-specialised, 320 threads):
-//   warp 0      TMA producer: limb tiles A_i[128 x 128B], B_j[256 x 128B] -> 4-stage SMEM ring
+// Structure (persistent, warp-specialised, 576 threads per CTA):
+//   warp 0      TMA producer: limb tiles A_i[128 x 128B], B_j[BN x 128B] -> SMEM ring
 //   warp 1      TMEM owner + single-thread MMA issuer (4 x K=32 MMAs per stage)
-//   warps 2..9  epilogue: tcgen05.ld -> mod p / Horner / alpha,beta -> tcgen05.st or global
-// Two tiles are in flight per CTA, one per 256-column TMEM accumulator ("slot"):
-// while the epilogue reduces slot s between two steps, the MMA runs the other
-// slot, so the tensor pipe never waits for the modular reduction.
+//   warps 2..17 epilogue: tcgen05.ld -> mod p / Horner / alpha,beta -> tcgen05.st or global
+// Two tiles are in flight per CTA (pair), one per 256-column TMEM accumulator
+// ("slot"): while the epilogue reduces slot s between two steps, the MMA runs
+// the other slot, so the tensor pipe never waits for the modular reduction.
+//
+// kPair = 2 (the production configuration): a cluster of two CTAs on one TPC
+// computes 256 x 256 tiles with tcgen05.mma.cta_group::2 (M = 256): each CTA
+// stages its own 128 rows of A and 128 of the 256 rows of B, the leader CTA
+// issues the MMAs, each CTA's TMEM holds its 128 output rows.  This halves
+// the SMEM operand traffic per MMA versus kPair = 1 (128 x 256 tiles).
 #include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "internal.h"
@@ -33,15 +40,21 @@ namespace ff {
 
 namespace {
 
-constexpr int kStages = 4;
-constexpr int kABytes = kTileM * kBK;          // 16 KB
-constexpr int kBBytes = kTileN * kBK;          // 32 KB
-constexpr int kStageBytes = kABytes + kBBytes; // 48 KB
-constexpr int kNumEpiWarps = 8;
+constexpr int kNumEpiWarps = 16;  // 4 per TMEM lane quadrant, 64 columns each
 constexpr int kThreads = 32 * (2 + kNumEpiWarps);
-constexpr int kTmemCols = 512;                 // two 256-column s32 accumulators
-constexpr int kSmemBytes = kStages * kStageBytes + 256 + 1024;
-constexpr int kRasterGroup = 16;               // m-tiles per raster band (L2 reuse)
+constexpr int kTmemCols = 512;  // two 256-column s32 accumulators
+constexpr int kRasterDefault = 8; // tile-rows per raster band (L2 reuse)
+
+template <int kPair>
+struct Cfg {
+    static constexpr int BM = 128 * kPair;         // tile rows (per cluster)
+    static constexpr int BN = kTileN;              // tile columns
+    static constexpr int A_BYTES = 128 * kBK;      // per CTA: 128 rows of A
+    static constexpr int B_BYTES = (BN / kPair) * kBK;  // per CTA: BN/kPair rows of B
+    static constexpr int STAGE = A_BYTES + B_BYTES;
+    static constexpr int STAGES = kPair == 2 ? 6 : 4;
+    static constexpr int SMEM = STAGES * STAGE + 256 + 1024;
+};
 
 struct GemmArgs {
     ModP mp;
@@ -57,31 +70,33 @@ struct GemmArgs {
     int8_t group_first[8], group_len[8];
     uint32_t idesc[16];
     int32_t vec_store;  // 1 if C rows are 16-byte aligned
+    int32_t raster;     // tile-rows per raster band
+    int32_t hints;      // bit0: TMA loads evict_last; bit1: C stores evict_first
 };
 
 struct Smem {
-    uint64_t full[kStages];
-    uint64_t empty[kStages];
+    uint64_t full[8];
+    uint64_t empty[8];
     uint64_t accfull[2];
     uint64_t accempty[2];
     uint32_t tmem_base;
 };
 
 __device__ __forceinline__ void tile_coords(const GemmArgs& a, int t, int& tm, int& tn) {
-    const int band_size = kRasterGroup * a.tiles_n;
+    const int band_size = a.raster * a.tiles_n;
     const int band = t / band_size;
     const int idx = t - band * band_size;
-    const int rows_in_band = min(kRasterGroup, a.tiles_m - band * kRasterGroup);
-    tm = band * kRasterGroup + idx % rows_in_band;
+    const int rows_in_band = min(a.raster, a.tiles_m - band * a.raster);
+    tm = band * a.raster + idx % rows_in_band;
     tn = idx / rows_in_band;
 }
 
 // The common schedule every role walks: tiles in pairs (one per TMEM slot),
 // groups from the highest weight down, k-blocks in order, then the slots.
 template <class F>
-__device__ __forceinline__ void for_each_step(const GemmArgs& a, F&& f) {
-    for (int t0 = blockIdx.x; t0 < a.num_tiles; t0 += 2 * gridDim.x) {
-        const int t1 = t0 + gridDim.x;
+__device__ __forceinline__ void for_each_step(const GemmArgs& a, int unit, int nunits, F&& f) {
+    for (int t0 = unit; t0 < a.num_tiles; t0 += 2 * nunits) {
+        const int t1 = t0 + nunits;
         const int nslots = t1 < a.num_tiles ? 2 : 1;
         for (int g = a.G - 1; g >= 0; --g)
             for (int kb = 0; kb < a.nkb; ++kb)
@@ -89,63 +104,84 @@ __device__ __forceinline__ void for_each_step(const GemmArgs& a, F&& f) {
     }
 }
 
+template <int kPair>
 __global__ void __launch_bounds__(kThreads, 1)
     ffgemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ GemmArgs a) {
+    using K = Cfg<kPair>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    Smem* sh = reinterpret_cast<Smem*>(smem + kStages * kStageBytes);
+    Smem* sh = reinterpret_cast<Smem*>(smem + K::STAGES * K::STAGE);
     const int warp = threadIdx.x / 32;
     const uint32_t lane = ptx::lane_id();
+    const uint32_t rank = kPair == 2 ? ptx::cluster_ctarank() : 0;
+    const bool leader = (rank == 0);
+    const int unit = blockIdx.x / kPair, nunits = gridDim.x / kPair;
 
     if (threadIdx.x == 0) {
         ptx::tma_prefetch(&tmA);
         ptx::tma_prefetch(&tmB);
-        for (int s = 0; s < kStages; ++s) {
+        for (int s = 0; s < K::STAGES; ++s) {
             ptx::mbar_init(&sh->full[s], 1);
             ptx::mbar_init(&sh->empty[s], 1);
         }
         for (int s = 0; s < 2; ++s) {
             ptx::mbar_init(&sh->accfull[s], 1);
-            ptx::mbar_init(&sh->accempty[s], kNumEpiWarps);
+            ptx::mbar_init(&sh->accempty[s], kNumEpiWarps * kPair);
         }
         ptx::fence_barrier_init();
     }
-    if (warp == 1) ptx::tmem_alloc(&sh->tmem_base, kTmemCols);
+    if (warp == 1) {
+        if (kPair == 2) ptx::tmem_alloc_pair(&sh->tmem_base, kTmemCols);
+        else ptx::tmem_alloc(&sh->tmem_base, kTmemCols);
+    }
     ptx::tc_fence_before();
-    __syncthreads();
+    if (kPair == 2) ptx::cluster_sync();
+    else __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = sh->tmem_base;
 
     if (warp == 0) {
-        // ------------------------------------------------ TMA producer
+        // ------------------------------------------------ TMA producer (both CTAs)
         if (lane == 0) {
             uint32_t stage = 0, phase = 0;
-            for_each_step(a, [&](int tile, int, int g, int kb) {
+            const uint64_t pol = (a.hints & 1) ? ptx::policy_evict_last() : ptx::policy_evict_normal();
+            for_each_step(a, unit, nunits, [&](int tile, int, int g, int kb) {
                 int tm, tn;
                 tile_coords(a, tile, tm, tn);
+                const int arow = tm * K::BM + static_cast<int>(rank) * 128;
+                const int brow = tn * K::BN + static_cast<int>(rank) * (K::BN / kPair);
                 const int ks0 = kb * a.kb_iters;
                 const int ks1 = min(ks0 + a.kb_iters, a.k_iters);
                 for (int pi = a.group_first[g]; pi < a.group_first[g] + a.group_len[g]; ++pi) {
                     const int li = a.pair_i[pi], lj = a.pair_j[pi];
                     for (int ks = ks0; ks < ks1; ++ks) {
                         ptx::mbar_wait(&sh->empty[stage], phase ^ 1);
-                        uint8_t* sa = smem + stage * kStageBytes;
-                        ptx::mbar_arrive_expect_tx(&sh->full[stage], kStageBytes);
-                        ptx::tma_load_3d(sa, &tmA, &sh->full[stage], ks * kBK, tm * kTileM, li);
-                        ptx::tma_load_3d(sa + kABytes, &tmB, &sh->full[stage], ks * kBK, tn * kTileN, lj);
-                        if (++stage == kStages) { stage = 0; phase ^= 1; }
+                        uint8_t* sa = smem + stage * K::STAGE;
+                        if (kPair == 1) {
+                            ptx::mbar_arrive_expect_tx(&sh->full[stage], K::STAGE);
+                            ptx::tma_load_3d(sa, &tmA, &sh->full[stage], ks * kBK, arow, li, pol);
+                            ptx::tma_load_3d(sa + K::A_BYTES, &tmB, &sh->full[stage], ks * kBK, brow, lj, pol);
+                        } else {
+                            // both CTAs' bytes are counted on the leader's full barrier
+                            if (leader) ptx::mbar_arrive_expect_tx(&sh->full[stage], 2 * K::STAGE);
+                            const uint32_t bar = ptx::mapa(ptx::smem_u32(&sh->full[stage]), 0);
+                            ptx::tma_load_3d_pair(sa, &tmA, bar, ks * kBK, arow, li, pol);
+                            ptx::tma_load_3d_pair(sa + K::A_BYTES, &tmB, bar, ks * kBK, brow, lj, pol);
+                        }
+                        if (++stage == K::STAGES) { stage = 0; phase ^= 1; }
                     }
                 }
             });
         }
     } else if (warp == 1) {
-        // ------------------------------------------------ MMA issuer (one thread)
-        if (lane == 0) {
+        // ------------------------------------------------ MMA issuer (one thread of the leader)
+        if (lane == 0 && leader) {
             uint32_t stage = 0, phase = 0;
             uint32_t acc_par[2] = {0, 0};
-            for_each_step(a, [&](int, int slot, int g, int kb) {
-                ptx::mbar_wait(&sh->accempty[slot], acc_par[slot] ^ 1);
+            for_each_step(a, unit, nunits, [&](int, int slot, int g, int kb) {
+                if (kPair == 2) ptx::mbar_wait_cluster(&sh->accempty[slot], acc_par[slot] ^ 1);
+                else ptx::mbar_wait(&sh->accempty[slot], acc_par[slot] ^ 1);
                 acc_par[slot] ^= 1;
                 ptx::tc_fence_after();
                 const uint32_t d = tmem_base + slot * kTileN;
@@ -157,100 +193,120 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int ks = ks0; ks < ks1; ++ks) {
                         ptx::mbar_wait(&sh->full[stage], phase);
                         ptx::tc_fence_after();
-                        const uint32_t sa = ptx::smem_u32(smem + stage * kStageBytes);
+                        const uint32_t sa = ptx::smem_u32(smem + stage * K::STAGE);
                         const uint64_t da = ptx::smem_desc_sw128(sa);
-                        const uint64_t db = ptx::smem_desc_sw128(sa + kABytes);
+                        const uint64_t db = ptx::smem_desc_sw128(sa + K::A_BYTES);
 #pragma unroll
                         for (int kk = 0; kk < kBK / kMmaK; ++kk) {
-                            ptx::mma_i8(d, da + 2 * kk, db + 2 * kk, idesc, acc);
+                            if (kPair == 2) ptx::mma_i8_pair(d, da + 2 * kk, db + 2 * kk, idesc, acc);
+                            else ptx::mma_i8(d, da + 2 * kk, db + 2 * kk, idesc, acc);
                             acc = 1u;
                         }
-                        ptx::tc_commit(&sh->empty[stage]);  // frees the SMEM stage when these MMAs finish
-                        if (++stage == kStages) { stage = 0; phase ^= 1; }
+                        // frees the SMEM stage (in both CTAs) when these MMAs finish
+                        if (kPair == 2) ptx::tc_commit_pair(&sh->empty[stage]);
+                        else ptx::tc_commit(&sh->empty[stage]);
+                        if (++stage == K::STAGES) { stage = 0; phase ^= 1; }
                     }
                 }
-                ptx::tc_commit(&sh->accfull[slot]);  // accumulator ready for the epilogue
+                // accumulator ready for the epilogue (of both CTAs)
+                if (kPair == 2) ptx::tc_commit_pair(&sh->accfull[slot]);
+                else ptx::tc_commit(&sh->accfull[slot]);
             });
         }
     } else {
-        // ------------------------------------------------ epilogue warps
+        // ------------------------------------------------ epilogue warps (both CTAs)
         const int q = warp & 3;                 // TMEM lane quadrant this warp may access
-        const int h = (warp - 2) >> 2;          // which 128-column half of the tile
+        const int h = (warp - 2) >> 2;          // which 64-column quarter of the tile
         const ModP M = a.mp;
+        const uint32_t accempty_leader0 = kPair == 2 ? ptx::mapa(ptx::smem_u32(&sh->accempty[0]), 0) : 0;
+        const uint32_t accempty_leader1 = kPair == 2 ? ptx::mapa(ptx::smem_u32(&sh->accempty[1]), 0) : 0;
         uint32_t acc_par[2] = {0, 0};
-        for_each_step(a, [&](int tile, int slot, int g, int kb) {
+        for_each_step(a, unit, nunits, [&](int tile, int slot, int g, int kb) {
             ptx::mbar_wait(&sh->accfull[slot], acc_par[slot]);
             acc_par[slot] ^= 1;
             ptx::tc_fence_after();
             const bool last_kb = (kb == a.nkb - 1);
             const bool final_step = last_kb && g == 0;
-            const bool horner = last_kb && g > 0;
-            const uint32_t tcol = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + slot * kTileN + h * 128;
-            int tm, tn;
-            tile_coords(a, tile, tm, tn);
-            const int row = tm * kTileM + q * 32 + static_cast<int>(lane);
-            for (int c = 0; c < 4; ++c) {
-                uint32_t v[32];
-                ptx::tmem_ld32(tcol + c * 32, v);
+            const uint32_t tcol = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + slot * kTileN + h * 64;
+            if (!final_step) {
+                // delayed reduction between steps (+ Horner x256 after the last k-block of a group)
+                uint32_t v[64];
+                ptx::tmem_ld64(tcol, v);
                 ptx::tmem_wait_ld();
-                if (!final_step) {
+                const int32_t w = last_kb ? 256 : 1;
+                const float f = last_kb ? M.w256_over_p : M.inv_p;
 #pragma unroll
-                    for (int t = 0; t < 32; ++t) {
-                        uint32_t r = residue_i32(static_cast<int32_t>(v[t]), M);
-                        if (horner) r = mulmod_shoup(r, M.w256, M.w256_sh, M.p);
-                        v[t] = static_cast<uint32_t>(centre(r, M));
-                    }
-                    ptx::tmem_st32(tcol + c * 32, v);
-                } else if (row < a.m) {
-                    const int col0 = tn * kTileN + h * 128 + c * 32;
+                for (int t = 0; t < 64; ++t)
+                    v[t] = static_cast<uint32_t>(reduce_approx(static_cast<int32_t>(v[t]), w, f,
+                                                               static_cast<int32_t>(M.p)));
+                ptx::tmem_st64(tcol, v);
+                ptx::tmem_wait_st();
+            } else {
+                int tm, tn;
+                tile_coords(a, tile, tm, tn);
+                const int row = tm * K::BM + static_cast<int>(rank) * 128 + q * 32 + static_cast<int>(lane);
+#pragma unroll 1
+                for (int half = 0; half < 2; ++half) {
+                    uint32_t v[32];
+                    ptx::tmem_ld32(tcol + half * 32, v);
+                    ptx::tmem_wait_ld();
+                    if (row >= a.m) continue;
+                    const int col0 = tn * K::BN + h * 64 + half * 32;
                     int32_t* crow = a.C + static_cast<int64_t>(row) * a.ldc + col0;
                     const bool full = a.vec_store && (col0 + 32 <= a.n);
-                    uint32_t cin[32];
+                    uint32_t o[32];
                     if (M.beta != 0) {
                         if (full) {
 #pragma unroll
                             for (int t = 0; t < 8; ++t) {
                                 const int4 x = *reinterpret_cast<const int4*>(crow + 4 * t);
-                                cin[4 * t] = x.x; cin[4 * t + 1] = x.y; cin[4 * t + 2] = x.z; cin[4 * t + 3] = x.w;
+                                o[4 * t] = x.x; o[4 * t + 1] = x.y; o[4 * t + 2] = x.z; o[4 * t + 3] = x.w;
                             }
                         } else {
 #pragma unroll
-                            for (int t = 0; t < 32; ++t) cin[t] = (col0 + t < a.n) ? crow[t] : 0;
+                            for (int t = 0; t < 32; ++t) o[t] = (col0 + t < a.n) ? crow[t] : 0;
                         }
                     }
 #pragma unroll
                     for (int t = 0; t < 32; ++t) {
                         uint32_t r = mulmod_shoup(residue_i32(static_cast<int32_t>(v[t]), M), M.alpha, M.alpha_sh, M.p);
                         if (M.beta != 0) {
-                            const uint32_t cr = residue_i32(static_cast<int32_t>(cin[t]), M);
+                            const uint32_t cr = residue_i32(static_cast<int32_t>(o[t]), M);
                             r = addmod(r, mulmod_shoup(cr, M.beta, M.beta_sh, M.p), M.p);
                         }
-                        v[t] = r;
+                        o[t] = r;
                     }
-                    if (full) {
+                    if (full && (a.hints & 2)) {
 #pragma unroll
                         for (int t = 0; t < 8; ++t)
-                            *reinterpret_cast<int4*>(crow + 4 * t) =
-                                make_int4(v[4 * t], v[4 * t + 1], v[4 * t + 2], v[4 * t + 3]);
+                            ptx::st_global_v4_stream(crow + 4 * t, o[4 * t], o[4 * t + 1], o[4 * t + 2], o[4 * t + 3]);
+                    } else if (full) {
+#pragma unroll
+                        for (int t = 0; t < 8; ++t)
+                            *reinterpret_cast<int4*>(crow + 4 * t) = make_int4(o[4 * t], o[4 * t + 1], o[4 * t + 2], o[4 * t + 3]);
                     } else {
 #pragma unroll
                         for (int t = 0; t < 32; ++t)
-                            if (col0 + t < a.n) crow[t] = static_cast<int32_t>(v[t]);
+                            if (col0 + t < a.n) crow[t] = static_cast<int32_t>(o[t]);
                     }
                 }
             }
-            if (!final_step) ptx::tmem_wait_st();
             ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&sh->accempty[slot]);
+            if (lane == 0) {
+                if (kPair == 2) ptx::mbar_arrive_cluster(slot ? accempty_leader1 : accempty_leader0);
+                else ptx::mbar_arrive(&sh->accempty[slot]);
+            }
         });
     }
 
     ptx::tc_fence_before();
-    __syncthreads();
+    if (kPair == 2) ptx::cluster_sync();
+    else __syncthreads();
     if (warp == 1) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc(tmem_base, kTmemCols);
+        if (kPair == 2) ptx::tmem_dealloc_pair(tmem_base, kTmemCols);
+        else ptx::tmem_dealloc(tmem_base, kTmemCols);
     }
 }
 
@@ -286,24 +342,24 @@ bool make_plane_map(CUtensorMap* map, const int8_t* base, int L, int64_t rows, i
     return r == CUDA_SUCCESS;
 }
 
-uint32_t make_idesc(bool a_signed, bool b_signed, bool saturate) {
+uint32_t make_idesc(bool a_signed, bool b_signed, bool saturate, int M, int N) {
     uint32_t d = 0;
     d |= (saturate ? 1u : 0u) << 3;          // saturate (s8 only)
     d |= 2u << 4;                             // D format: S32
     d |= (a_signed ? 1u : 0u) << 7;           // A: 0 = u8, 1 = s8
     d |= (b_signed ? 1u : 0u) << 10;          // B: 0 = u8, 1 = s8
     // bits 15/16: A/B K-major (0); no negate
-    d |= static_cast<uint32_t>(kTileN >> 3) << 17;  // N / 8
-    d |= static_cast<uint32_t>(kTileM >> 4) << 24;  // M / 16
+    d |= static_cast<uint32_t>(N >> 3) << 17;  // N / 8
+    d |= static_cast<uint32_t>(M >> 4) << 24;  // M / 16
     return d;
 }
 
-}  // namespace
-
-int launch_gemm_tc(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A_limbs, const int8_t* B_limbs,
-                   int32_t* C, int64_t ldc, cudaStream_t st) {
+template <int kPair>
+int launch_impl(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A_limbs, const int8_t* B_limbs,
+                int32_t* C, int64_t ldc, cudaStream_t st) {
+    using K = Cfg<kPair>;
     const ff_plan_info& I = pl.info;
-    if (m > INT32_MAX - kTileM || n > INT32_MAX - kTileN) return -2;
+    if (m > INT32_MAX - K::BM || n > INT32_MAX - K::BN) return -2;
     GemmArgs a;
     std::memset(&a, 0, sizeof(a));
     a.mp = pl.mp;
@@ -311,8 +367,8 @@ int launch_gemm_tc(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t
     a.ldc = ldc;
     a.m = static_cast<int32_t>(m);
     a.n = static_cast<int32_t>(n);
-    a.tiles_m = static_cast<int32_t>((m + kTileM - 1) / kTileM);
-    a.tiles_n = static_cast<int32_t>((n + kTileN - 1) / kTileN);
+    a.tiles_m = static_cast<int32_t>((m + K::BM - 1) / K::BM);
+    a.tiles_n = static_cast<int32_t>((n + K::BN - 1) / K::BN);
     const int64_t nt = static_cast<int64_t>(a.tiles_m) * a.tiles_n;
     if (nt > INT32_MAX / 2) return -2;
     a.num_tiles = static_cast<int32_t>(nt);
@@ -323,28 +379,58 @@ int launch_gemm_tc(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t
     for (int pi = 0; pi < pl.npairs; ++pi) {
         a.pair_i[pi] = static_cast<int8_t>(pl.pair_i[pi]);
         a.pair_j[pi] = static_cast<int8_t>(pl.pair_j[pi]);
-        a.idesc[pi] = make_idesc(I.limb_signed[pl.pair_i[pi]] != 0, I.limb_signed[pl.pair_j[pi]] != 0, pl.saturate);
+        a.idesc[pi] = make_idesc(I.limb_signed[pl.pair_i[pi]] != 0, I.limb_signed[pl.pair_j[pi]] != 0,
+                                 pl.saturate, K::BM, K::BN);
     }
     for (int w = 0; w < I.groups; ++w) {
         a.group_first[w] = static_cast<int8_t>(pl.group_first[w]);
         a.group_len[w] = static_cast<int8_t>(pl.group_len[w]);
     }
     a.vec_store = ((ldc % 4) == 0 && (reinterpret_cast<uintptr_t>(C) & 15) == 0) ? 1 : 0;
+    a.raster = kRasterDefault;
+    a.hints = 0;
+    if (const char* e = getenv("FF_RASTER")) a.raster = atoi(e) > 0 ? atoi(e) : kRasterDefault;
+    if (const char* e = getenv("FF_HINTS")) a.hints = atoi(e);
 
     CUtensorMap mapA, mapB;
-    if (!make_plane_map(&mapA, A_limbs, I.L, m, I.k_pad, kTileM)) return FF_ERR_CUDA;
-    if (!make_plane_map(&mapB, B_limbs, I.L, n, I.k_pad, kTileN)) return FF_ERR_CUDA;
+    if (!make_plane_map(&mapA, A_limbs, I.L, m, I.k_pad, 128)) return FF_ERR_CUDA;
+    if (!make_plane_map(&mapB, B_limbs, I.L, n, I.k_pad, K::BN / kPair)) return FF_ERR_CUDA;
 
     static bool attr_set = false;
     if (!attr_set) {
-        if (cudaFuncSetAttribute(ffgemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes) !=
+        if (cudaFuncSetAttribute(ffgemm_tc_kernel<kPair>, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM) !=
             cudaSuccess)
             return FF_ERR_CUDA;
         attr_set = true;
     }
-    const int grid = static_cast<int>(nt < num_sms() ? nt : num_sms());
-    ffgemm_tc_kernel<<<grid, kThreads, kSmemBytes, st>>>(mapA, mapB, a);
+    const int64_t units = num_sms() / kPair;
+    const int grid = static_cast<int>((nt < units ? nt : units) * kPair);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = K::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kPair;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, ffgemm_tc_kernel<kPair>, mapA, mapB, a) != cudaSuccess) return FF_ERR_CUDA;
     return cudaGetLastError() == cudaSuccess ? 0 : FF_ERR_CUDA;
+}
+
+}  // namespace
+
+int launch_gemm_tc(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A_limbs, const int8_t* B_limbs,
+                   int32_t* C, int64_t ldc, cudaStream_t st) {
+    // The CTA-pair kernel unless the problem has too few 256 x 256 tiles to
+    // occupy the GPU (then the 128 x 256 single-CTA kernel gives more CTAs).
+    const int64_t pair_tiles = ((m + 255) / 256) * ((n + 255) / 256);
+    if (pl.force_pair == 1 || (pl.force_pair == 0 && pair_tiles * 2 < num_sms()))
+        return launch_impl<1>(pl, m, n, k, A_limbs, B_limbs, C, ldc, st);
+    return launch_impl<2>(pl, m, n, k, A_limbs, B_limbs, C, ldc, st);
 }
 
 }  // namespace ff

@@ -26,6 +26,8 @@ struct ModP {
     uint32_t w256_sh;     // floor(w256 * 2^32 / p)
     uint32_t alpha, alpha_sh;
     uint32_t beta, beta_sh;
+    float inv_p;          // fl(1/p)
+    float w256_over_p;    // fl(256/p)
 };
 
 struct Plan {
@@ -37,6 +39,7 @@ struct Plan {
     int group_first[kMaxGroups];     // pairs of group w are [group_first[w], group_first[w]+group_len[w])
     int group_len[kMaxGroups];
     bool saturate;
+    int force_pair;                  // 0 auto, 1 single-CTA kernel, 2 CTA-pair kernel
 };
 
 // planner.cpp

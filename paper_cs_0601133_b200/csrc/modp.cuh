@@ -37,6 +37,20 @@ __device__ __forceinline__ int32_t centre(uint32_t r, const ModP& M) {
     return r > M.half ? static_cast<int32_t>(r) - static_cast<int32_t>(M.p) : static_cast<int32_t>(r);
 }
 
+// Intermediate write-back value: a centred-ish representative of (a * w) mod p
+// for the s32 accumulator a and w in {1, 256} (Horner scaling), with the
+// quotient estimated through the fp32 reciprocal w/p (PAPER.md l.125-127:
+// "precompute the inverse of the characteristic p within a floating point
+// number ... rounding may induce a +-1 error").  No correction is applied:
+// v = a*w - q*p is exact in wrapping 32-bit arithmetic and
+// |v| <= p/2 + 385*w, a carry the planner's k-block bound
+// includes.  Used only between steps; the final output uses residue_i32.
+__device__ __forceinline__ int32_t reduce_approx(int32_t a, int32_t w, float w_over_p, int32_t p) {
+    const int32_t q = __float2int_rn(__int2float_rn(a) * w_over_p);
+    return static_cast<int32_t>(static_cast<uint32_t>(a) * static_cast<uint32_t>(w) -
+                                static_cast<uint32_t>(q) * static_cast<uint32_t>(p));
+}
+
 __device__ __forceinline__ uint32_t addmod(uint32_t a, uint32_t b, uint32_t p) {
     const uint32_t s = a + b;  // < 2p < 2^32
     return s >= p ? s - p : s;

@@ -66,6 +66,7 @@ int make_plan(uint32_t p, int64_t k, const ff_opts* opts, Plan* out) {
     if (o.scheme < FF_SCHEME_AUTO || o.scheme > FF_SCHEME_T) return FF_ERR_OPTS;
     if (o.winograd < -1 || o.winograd > 1) return FF_ERR_OPTS;
     if (o.kb_override < 0) return FF_ERR_OPTS;
+    if (o.cta_group < 0 || o.cta_group > 2) return FF_ERR_OPTS;
 
     Plan pl;
     std::memset(&pl, 0, sizeof(pl));
@@ -109,7 +110,11 @@ int make_plan(uint32_t p, int64_t k, const ff_opts* opts, Plan* out) {
         if (b > bmax) bmax = b;
     }
     I.group_bound_max = bmax;
-    I.kb_max = bmax > 0 ? (((int64_t)1 << 31) - 1 - cmax) / bmax : ((int64_t)1 << 40);
+    // Carry written back between steps: |v| <= p/2 + 385 w with w = 256 for the
+    // Horner scaling (L >= 2) and w = 1 otherwise (modp.cuh, reduce_approx).
+    const int64_t carry = cmax + (L >= 2 ? 385 * 256 : 385);
+    I.carry_max = carry;
+    I.kb_max = bmax > 0 ? (((int64_t)1 << 31) - 1 - carry) / bmax : ((int64_t)1 << 40);
     int64_t kb = I.kb_max;
     if (o.kb_override > 0) {
         if (o.kb_override > I.kb_max || o.kb_override < kBK) return FF_ERR_OPTS;
@@ -137,6 +142,7 @@ int make_plan(uint32_t p, int64_t k, const ff_opts* opts, Plan* out) {
     }
     pl.npairs = np;
     pl.saturate = o.debug_saturate != 0;
+    pl.force_pair = o.cta_group;
 
     ModP& M = pl.mp;
     M.p = p;
@@ -145,6 +151,8 @@ int make_plan(uint32_t p, int64_t k, const ff_opts* opts, Plan* out) {
     M.off31 = (uint32_t)((((uint64_t)1) << 31) % p);
     M.w256 = 256u % p;
     M.w256_sh = shoup(M.w256, p);
+    M.inv_p = (float)(1.0 / (double)p);
+    M.w256_over_p = (float)(256.0 / (double)p);
     *out = pl;
     set_scalars(out, 1, 0);
     return 0;

@@ -135,11 +135,13 @@ SHAPES = [(1, 1, 1), (3, 5, 7), (128, 256, 128), (129, 257, 129), (200, 300, 100
           (256, 512, 640), (77, 600, 33)]
 
 
+@pytest.mark.parametrize("cta_group", [1, 2])
 @pytest.mark.parametrize("p", CONFIG_PRIMES)
 @pytest.mark.parametrize("tA,tB", [("N", "N"), ("T", "N"), ("N", "T"), ("T", "T")])
-def test_gemm_vs_oracle_shapes(env, p, tA, tB):
+def test_gemm_vs_oracle_shapes(env, p, tA, tB, cta_group):
+    """Both kernels: 128x256 single-CTA and 256x256 CTA-pair (cta_group::2)."""
     torch, ff = env
-    rng = np.random.default_rng(p % 1009 + ord(tA) * 3 + ord(tB))
+    rng = np.random.default_rng(p % 1009 + ord(tA) * 3 + ord(tB) + cta_group)
     for si, (m, n, k) in enumerate(SHAPES):
         ldx = si % 3
         Abuf = _stored(rng, *((m, k) if tA == "N" else (k, m)), p, ldx)
@@ -147,7 +149,8 @@ def test_gemm_vs_oracle_shapes(env, p, tA, tB):
         Cbuf = _stored(rng, m, n, p, ldx + 1)
         alpha = [1, p - 1, 3, int(rng.integers(0, p))][si % 4]
         beta = [0, 1, p - 1, int(rng.integers(0, p))][(si + 1) % 4]
-        got = _run_gpu(torch, ff, p, tA, tB, m, n, k, alpha, Abuf, Bbuf, beta, Cbuf)
+        got = _run_gpu(torch, ff, p, tA, tB, m, n, k, alpha, Abuf, Bbuf, beta, Cbuf,
+                       {"cta_group": cta_group})
         _check(p, tA, tB, m, n, k, alpha, Abuf, Bbuf, beta, Cbuf, got)
 
 
@@ -164,16 +167,17 @@ def test_gemm_other_primes_and_noncanonical_inputs(env, p):
         _check(p, "N", "N", m, n, k, alpha, Abuf, Bbuf, beta, Cbuf, got)
 
 
+@pytest.mark.parametrize("cta_group", [1, 2])
 @pytest.mark.parametrize("p,scheme", [(65521, 2), (65521, 1), (8388593, 1), (67108859, 1),
                                       (251, 1), (8388593, 2)])
-def test_kb_override_forces_mid_k_reductions(env, p, scheme):
+def test_kb_override_forces_mid_k_reductions(env, p, scheme, cta_group):
     """Shrunk k-block ("overflow safety under shrunk gamma" analogue):
     several mid-k reductions per weight group must not change the result."""
     torch, ff = env
     rng = np.random.default_rng(11)
     m, n, k = 130, 260, 1000
     Abuf, Bbuf, Cbuf = _stored(rng, m, k, p), _stored(rng, k, n, p), _stored(rng, m, n, p)
-    opts = {"kb_override": 128, "scheme": scheme}
+    opts = {"kb_override": 128, "scheme": scheme, "cta_group": cta_group}
     assert ff.ff_plan_query(p, k, opts)["num_kblocks"] == 8
     got = _run_gpu(torch, ff, p, "N", "N", m, n, k, 5, Abuf, Bbuf, 7, Cbuf, opts)
     _check(p, "N", "N", m, n, k, 5, Abuf, Bbuf, 7, Cbuf, got)
@@ -205,14 +209,16 @@ def test_accumulator_at_the_bound_closed_form(env, p):
     if p == 65521:
         assert v == 33008
     for k in (info["kb"], 2 * info["kb"] + 45):
-        m, n = 128, 256
+        m, n = 256, 512
         A = torch.full((m, k), v, dtype=torch.int32, device="cuda")
         B = torch.full((k, n), v, dtype=torch.int32, device="cuda")
         C = torch.empty((m, n), dtype=torch.int32, device="cuda")
-        for sat in (0, 1):
-            ff.ff_gemm_ex(p, "N", "N", m, n, k, 1, A, k, B, n, 0, C, n, {"debug_saturate": sat})
+        for sat, grp in ((0, 1), (1, 1), (0, 2), (1, 2)):
+            C.fill_(-1)
+            ff.ff_gemm_ex(p, "N", "N", m, n, k, 1, A, k, B, n, 0, C, n,
+                          {"debug_saturate": sat, "cta_group": grp})
             torch.cuda.synchronize()
-            assert (C == (k * v * v) % p).all().item(), (p, k, sat)
+            assert (C == (k * v * v) % p).all().item(), (p, k, sat, grp)
 
 
 def test_quick_returns_and_degenerate(env):

@@ -125,9 +125,17 @@ def test_planner_matches_paper_bound(ff, p, L, scheme, D, kb_max):
     B = [sum(D[i] * D[w - i] for i in range(L) if 0 <= w - i < L) for w in range(2 * L - 1)]
     assert info["group_bound"] == B
     half = (p - 1) // 2
-    assert info["kb_max"] == kb_max == (2 ** 31 - 1 - half) // max(B)
-    assert kb_max * max(B) + half <= 2 ** 31 - 1 < (kb_max + 1) * max(B) + half
-    assert info["kb"] % 128 == 0 and info["kb"] <= kb_max
+    # with an exactly centred carry the bound is SURVEY §8(a)'s kb_max ...
+    assert kb_max == (2 ** 31 - 1 - half) // max(B)
+    # ... the kernel writes back a float-reciprocal residue (modp.cuh reduce_approx),
+    # |carry| <= (p-1)/2 + 385 w, w = 256 when a Horner x256 step exists (L >= 2)
+    carry = half + 385 * (256 if L >= 2 else 1)
+    assert info["carry_max"] == carry
+    kbm = info["kb_max"]
+    assert kbm == (2 ** 31 - 1 - carry) // max(B)
+    assert kbm * max(B) + carry <= 2 ** 31 - 1 < (kbm + 1) * max(B) + carry
+    assert kb_max - 4 <= kbm <= kb_max
+    assert info["kb"] % 128 == 0 and info["kb"] <= kbm
     # every config fits one k-block ("none of the 5 needs it")
     for k in (512, 4096, 8192, 16384):
         assert ff.ff_plan_query(p, k)["num_kblocks"] == 1
