@@ -10,6 +10,8 @@
 // an exact 8x8-bit integer product on the tensor cores.
 //
 // HBM-bound: each element is read once (4 B) and written once per limb (L B).
+// Both kernels are templated on (L, scheme) so the digits live in registers,
+// and both write whole 128-byte lines of every limb plane per warp.
 #include <cuda_runtime.h>
 
 #include "internal.h"
@@ -19,109 +21,107 @@ namespace ff {
 
 namespace {
 
-constexpr int kVec = 16;  // K elements per thread-chunk (one 16-byte store per limb plane)
-
-// Digits of one centred residue.  S: balanced bytes (reinterpret the low byte
-// as s8, subtract, shift); T: two's-complement bytes (top byte signed).  Both
-// subtract-then-shift steps are exact divisions by 256.
-__device__ __forceinline__ void digits(int32_t c, int L, int scheme, uint8_t* d) {
+// Digits of one centred residue, packed into byte `pos` of w[i] (limb i).
+// S: balanced bytes (low byte reinterpreted as s8, subtract, shift);
+// T: two's-complement bytes (low limbs u8, top limb s8).  Subtract-then-shift
+// is an exact division by 256.
+template <int L, int SCHEME>
+__device__ __forceinline__ void put_digits(int32_t c, int pos, uint32_t (&w)[L]) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        if (i < L) {
-            const int32_t lo = (scheme == FF_SCHEME_S) ? static_cast<int32_t>(static_cast<int8_t>(c & 0xFF))
-                                                       : (c & 0xFF);
-            d[i] = static_cast<uint8_t>(lo & 0xFF);
-            c = (c - lo) >> 8;
-        }
+    for (int i = 0; i < L; ++i) {
+        const int32_t lo = (SCHEME == FF_SCHEME_S) ? static_cast<int32_t>(static_cast<int8_t>(c & 0xFF)) : (c & 0xFF);
+        w[i] |= static_cast<uint32_t>(lo & 0xFF) << (8 * pos);
+        c = (c - lo) >> 8;
     }
 }
 
-// 16 residues -> L packed 16-byte limb vectors.
-__device__ __forceinline__ void encode16(const int32_t (&x)[kVec], const ModP& M, int L, int scheme,
-                                         uint4 (&out)[4]) {
-    uint8_t b[4][kVec];
-#pragma unroll
-    for (int t = 0; t < kVec; ++t) {
-        uint8_t d[4] = {0, 0, 0, 0};
-        digits(centre(residue_i32(x[t], M), M), L, scheme, d);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) b[i][t] = d[i];
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        uint32_t w[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-            w[q] = static_cast<uint32_t>(b[i][4 * q]) | (static_cast<uint32_t>(b[i][4 * q + 1]) << 8) |
-                   (static_cast<uint32_t>(b[i][4 * q + 2]) << 16) | (static_cast<uint32_t>(b[i][4 * q + 3]) << 24);
-        out[i] = make_uint4(w[0], w[1], w[2], w[3]);
-    }
-}
-
-// Source already K-major: limb row r = X[r*ldx + 0..k).
-__global__ void __launch_bounds__(256) encode_direct_kernel(ModP M, int L, int scheme, int64_t rows,
-                                                            int64_t k, int64_t k_pad,
+// Source already K-major: limb row r = X[r*ldx + 0..k).  One thread encodes 4
+// consecutive elements of a row into one 32-bit word per limb plane, so a warp
+// reads 512 contiguous bytes and writes 128 contiguous bytes per plane.
+template <int L, int SCHEME>
+__global__ void __launch_bounds__(256) encode_direct_kernel(ModP M, int64_t rows, int64_t k, int64_t k_pad,
                                                             const int32_t* __restrict__ X, int64_t ldx,
-                                                            int8_t* __restrict__ limbs) {
-    const int64_t cpr = k_pad / kVec;
-    const int64_t total = rows * cpr;
+                                                            int8_t* __restrict__ limbs, int vec_ok) {
+    const int64_t groups = k_pad / 4;
     const int64_t plane = rows * k_pad;
-    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-         idx += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = idx / cpr;
-        const int64_t kk0 = (idx - r * cpr) * kVec;
-        const int32_t* src = X + r * ldx + kk0;
-        int32_t x[kVec];
-        if (kk0 + kVec <= k && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+    for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
+        const int32_t* src = X + r * ldx;
+        uint32_t* dst = reinterpret_cast<uint32_t*>(limbs + r * k_pad);
+        for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < groups;
+             g += (int64_t)gridDim.x * blockDim.x) {
+            const int64_t kk = 4 * g;
+            int32_t x[4];
+            if (vec_ok && kk + 4 <= k) {
+                const int4 v = __ldg(reinterpret_cast<const int4*>(src + kk));
+                x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
+            } else {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int4 v = __ldg(reinterpret_cast<const int4*>(src) + q);
-                x[4 * q] = v.x; x[4 * q + 1] = v.y; x[4 * q + 2] = v.z; x[4 * q + 3] = v.w;
+                for (int t = 0; t < 4; ++t) x[t] = (kk + t < k) ? __ldg(src + kk + t) : 0;
             }
-        } else {
+            uint32_t w[L];
 #pragma unroll
-            for (int t = 0; t < kVec; ++t) x[t] = (kk0 + t < k) ? __ldg(src + t) : 0;
+            for (int i = 0; i < L; ++i) w[i] = 0;
+#pragma unroll
+            for (int t = 0; t < 4; ++t) put_digits<L, SCHEME>(centre(residue_i32(x[t], M), M), t, w);
+#pragma unroll
+            for (int i = 0; i < L; ++i) dst[g + i * (plane / 4)] = w[i];
         }
-        uint4 out[4];
-        encode16(x, M, L, scheme, out);
-        int8_t* dst = limbs + r * k_pad + kk0;
-        for (int i = 0; i < L; ++i) *reinterpret_cast<uint4*>(dst + i * plane) = out[i];
     }
 }
 
-// Source transposed: limb row r, column kk = X[kk*ldx + r].  64x64 tile through SMEM.
-constexpr int kT = 64;
-__global__ void __launch_bounds__(256) encode_trans_kernel(ModP M, int L, int scheme, int64_t rows,
-                                                           int64_t k, int64_t k_pad,
+// Source transposed: limb row r, column kk = X[kk*ldx + r].  Tiles of 32 rows
+// (r) x 128 columns (kk): the load phase reads 128-byte rows of X, encodes
+// each value and scatters its L digit bytes into SMEM byte tiles [L][32][132]
+// (row pitch 33 words: both the byte stores and the word reads below are
+// bank-conflict free); the write phase then emits whole 128-byte limb rows,
+// four rows per warp per plane.
+constexpr int kTR = 32, kTK = 128, kPitch = kTK + 4;
+template <int L, int SCHEME>
+__global__ void __launch_bounds__(256) encode_trans_kernel(ModP M, int64_t rows, int64_t k, int64_t k_pad,
                                                            const int32_t* __restrict__ X, int64_t ldx,
                                                            int8_t* __restrict__ limbs) {
-    __shared__ int32_t tile[kT][kT + 1];
+    __shared__ __align__(16) uint8_t tile[L][kTR][kPitch];
     const int64_t plane = rows * k_pad;
-    const int c = threadIdx.x % kT;   // r offset within the tile
-    const int rr = threadIdx.x / kT;  // 0..3
-    const int64_t tiles_r = (rows + kT - 1) / kT;
-    const int64_t tiles_k = (k_pad + kT - 1) / kT;
+    const int64_t tiles_r = (rows + kTR - 1) / kTR;
+    const int64_t tiles_k = (k_pad + kTK - 1) / kTK;
+    const int lr = threadIdx.x % kTR;       // load: r offset
+    const int lk = threadIdx.x / kTR;       // load: kk offset 0..7 (+8 i)
+    const int wr = (threadIdx.x / 32) * 4 + (threadIdx.x % 32) / 8;   // write: row 0..31
+    const int wc = (threadIdx.x % 8) * 16;                            // write: column 0..112
     for (int64_t t = blockIdx.x; t < tiles_r * tiles_k; t += gridDim.x) {
-        const int64_t r0 = (t % tiles_r) * kT;
-        const int64_t kk0 = (t / tiles_r) * kT;
+        const int64_t r0 = (t % tiles_r) * kTR;
+        const int64_t kk0 = (t / tiles_r) * kTK;
         __syncthreads();
-#pragma unroll 4
-        for (int i = 0; i < 16; ++i) {
-            const int kl = rr * 16 + i;
-            const int64_t kk = kk0 + kl, r = r0 + c;
-            tile[kl][c] = (kk < k && r < rows) ? __ldg(X + kk * ldx + r) : 0;
+        int32_t xv[kTK / 8];
+        const bool rin = (r0 + lr) < rows;
+        const int32_t* col = X + (r0 + lr);
+#pragma unroll
+        for (int i = 0; i < kTK / 8; ++i) {        // all 16 loads in flight first
+            const int64_t kk = kk0 + lk + 8 * i;
+            xv[i] = (kk < k && rin) ? __ldg(col + kk * ldx) : 0;
+        }
+#pragma unroll
+        for (int i = 0; i < kTK / 8; ++i) {
+            const int kl = lk + 8 * i;
+            int32_t c = centre(residue_i32(xv[i], M), M);
+#pragma unroll
+            for (int l = 0; l < L; ++l) {
+                const int32_t lo = (SCHEME == FF_SCHEME_S) ? static_cast<int32_t>(static_cast<int8_t>(c & 0xFF))
+                                                           : (c & 0xFF);
+                tile[l][lr][kl] = static_cast<uint8_t>(lo & 0xFF);
+                c = (c - lo) >> 8;
+            }
         }
         __syncthreads();
-        const int64_t r = r0 + c;
-        const int64_t kc = kk0 + rr * 16;
+        const int64_t r = r0 + wr;
+        const int64_t kc = kk0 + wc;
         if (r < rows && kc < k_pad) {
-            int32_t x[kVec];
-#pragma unroll
-            for (int i = 0; i < kVec; ++i) x[i] = tile[rr * 16 + i][c];
-            uint4 out[4];
-            encode16(x, M, L, scheme, out);
             int8_t* dst = limbs + r * k_pad + kc;
-            for (int i = 0; i < L; ++i) *reinterpret_cast<uint4*>(dst + i * plane) = out[i];
+#pragma unroll
+            for (int l = 0; l < L; ++l) {
+                const uint32_t* src = reinterpret_cast<const uint32_t*>(&tile[l][wr][wc]);
+                *reinterpret_cast<uint4*>(dst + l * plane) = make_uint4(src[0], src[1], src[2], src[3]);
+            }
         }
     }
 }
@@ -145,20 +145,45 @@ int grid_for(int64_t work, int threads) {
     return static_cast<int>(g < 1 ? 1 : g);
 }
 
+template <int L, int SCHEME>
+void launch_encode_t(const Plan& pl, int kmajor_src, int64_t rows, int64_t k, int64_t k_pad, const int32_t* X,
+                     int64_t ldx, int8_t* limbs, cudaStream_t st) {
+    if (kmajor_src) {
+        const int64_t groups = k_pad / 4;
+        int gx = static_cast<int>((groups + 255) / 256);
+        if (gx > 64) gx = 64;
+        int64_t gy = (int64_t)num_sms() * 8 / gx;
+        if (gy > rows) gy = rows;
+        if (gy > 65535) gy = 65535;
+        if (gy < 1) gy = 1;
+        const int vec_ok = ((ldx % 4) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0) ? 1 : 0;
+        encode_direct_kernel<L, SCHEME><<<dim3(gx, static_cast<unsigned>(gy)), 256, 0, st>>>(
+            pl.mp, rows, k, k_pad, X, ldx, limbs, vec_ok);
+    } else {
+        const int64_t tiles = ((rows + kTR - 1) / kTR) * ((k_pad + kTK - 1) / kTK);
+        const int64_t cap = (int64_t)num_sms() * 8;
+        encode_trans_kernel<L, SCHEME><<<static_cast<int>(tiles < cap ? tiles : cap), 256, 0, st>>>(
+            pl.mp, rows, k, k_pad, X, ldx, limbs);
+    }
+}
+
 }  // namespace
 
-cudaError_t launch_encode(const Plan& pl, int kmajor_src, int64_t rows, int64_t k, const int32_t* X,
-                          int64_t ldx, int8_t* limbs, cudaStream_t st) {
-    const int64_t k_pad = (k + 15) / 16 * 16;
+cudaError_t launch_encode(const Plan& pl, int kmajor_src, int64_t rows, int64_t k, const int32_t* X, int64_t ldx,
+                          int8_t* limbs, cudaStream_t st) {
+    const int64_t k_pad = pl.info.k_pad;
     if (rows == 0 || k_pad == 0) return cudaSuccess;
-    if (kmajor_src) {
-        encode_direct_kernel<<<grid_for(rows * (k_pad / kVec), 256), 256, 0, st>>>(
-            pl.mp, pl.info.L, pl.info.scheme, rows, k, k_pad, X, ldx, limbs);
-    } else {
-        const int64_t tiles = ((rows + kT - 1) / kT) * ((k_pad + kT - 1) / kT);
-        int64_t g = tiles < (int64_t)num_sms() * 8 ? tiles : (int64_t)num_sms() * 8;
-        encode_trans_kernel<<<static_cast<int>(g), 256, 0, st>>>(pl.mp, pl.info.L, pl.info.scheme, rows, k,
-                                                                k_pad, X, ldx, limbs);
+    const bool S = pl.info.scheme == FF_SCHEME_S;
+    switch (pl.info.L) {
+        case 1: S ? launch_encode_t<1, FF_SCHEME_S>(pl, kmajor_src, rows, k, k_pad, X, ldx, limbs, st)
+                  : launch_encode_t<1, FF_SCHEME_T>(pl, kmajor_src, rows, k, k_pad, X, ldx, limbs, st); break;
+        case 2: S ? launch_encode_t<2, FF_SCHEME_S>(pl, kmajor_src, rows, k, k_pad, X, ldx, limbs, st)
+                  : launch_encode_t<2, FF_SCHEME_T>(pl, kmajor_src, rows, k, k_pad, X, ldx, limbs, st); break;
+        case 3: S ? launch_encode_t<3, FF_SCHEME_S>(pl, kmajor_src, rows, k, k_pad, X, ldx, limbs, st)
+                  : launch_encode_t<3, FF_SCHEME_T>(pl, kmajor_src, rows, k, k_pad, X, ldx, limbs, st); break;
+        case 4: S ? launch_encode_t<4, FF_SCHEME_S>(pl, kmajor_src, rows, k, k_pad, X, ldx, limbs, st)
+                  : launch_encode_t<4, FF_SCHEME_T>(pl, kmajor_src, rows, k, k_pad, X, ldx, limbs, st); break;
+        default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
 }

@@ -43,7 +43,7 @@ namespace {
 constexpr int kNumEpiWarps = 16;  // 4 per TMEM lane quadrant, 64 columns each
 constexpr int kThreads = 32 * (2 + kNumEpiWarps);
 constexpr int kTmemCols = 512;  // two 256-column s32 accumulators
-constexpr int kRasterDefault = 8; // tile-rows per raster band (L2 reuse)
+constexpr int kRasterDefault = 16;  // tile-rows per raster band (L2 reuse; swept on c4)
 
 template <int kPair>
 struct Cfg {
@@ -388,7 +388,7 @@ int launch_impl(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A
     }
     a.vec_store = ((ldc % 4) == 0 && (reinterpret_cast<uintptr_t>(C) & 15) == 0) ? 1 : 0;
     a.raster = kRasterDefault;
-    a.hints = 0;
+    a.hints = 3;  // TMA loads evict_last, C stores streaming (swept on c4)
     if (const char* e = getenv("FF_RASTER")) a.raster = atoi(e) > 0 ? atoi(e) : kRasterDefault;
     if (const char* e = getenv("FF_HINTS")) a.hints = atoi(e);
 

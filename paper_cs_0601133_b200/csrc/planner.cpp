@@ -13,6 +13,7 @@
 // giving kb_max = floor((2^31 - 1 - (p-1)/2) / max_w B_w)  (
 // the "one extra carried term" form matches the paper's own t_update values,
 // l.524-527, which satisfy (t+1)(p-1)^2 < 2^53 exactly).
+#include <cstdlib>
 #include <cstring>
 
 #include "internal.h"
@@ -124,6 +125,7 @@ int make_plan(uint32_t p, int64_t k, const ff_opts* opts, Plan* out) {
     if (kb < kBK) return FF_ERR_INTERNAL;
     I.kb = kb;
     I.k_pad = (k + 15) / 16 * 16;
+    if (const char* e = getenv("FF_KPAD_EXTRA")) I.k_pad += (atoi(e) / 16) * 16;  // experiment only
     I.num_kblocks = k > 0 ? (k + kb - 1) / kb : 0;
 
     // Pairs (i,j) ordered by weight group, highest w first (Horner order).
