@@ -75,7 +75,9 @@ typedef struct ff_opts {
                                then shows as a mismatch instead of a silent wrap) */
     int32_t cta_group;      /* 0 auto; 1 force the 128x256 single-CTA kernel; 2 force the
                                256x256 CTA-pair (tcgen05 cta_group::2) kernel */
-    int32_t reserved[6];
+    int32_t host_block;     /* ff_gemm_host only: rows/columns of C per pipelined block
+                               (rounded up to 256); 0 = auto (~4096) */
+    int32_t reserved[5];
 } ff_opts;
 
 /* The plan the library derives from (p, k, opts): host-only, no GPU needed. */
@@ -135,7 +137,10 @@ int ff_gemm_ex(uint32_t p, char transA, char transB, int64_t m, int64_t n, int64
 /* As ff_gemm, but A, B and C are HOST pointers (pinned for full PCIe speed;
  * pageable works).  Copies in, computes on the current device, copies C back
  * and synchronises before returning.  Device buffers are library-owned and
- * cached.  This is the end-to-end entry point the bench's "e2e" number uses. */
+ * cached.  The work is pipelined over blocks of C on three library streams
+ * (host->device copies, compute, device->host copies), so the PCIe transfers
+ * of one block overlap the encode/GEMM of others.  This is
+ * the end-to-end entry point the bench's "e2e" number uses. */
 int ff_gemm_host(uint32_t p, char transA, char transB, int64_t m, int64_t n, int64_t k,
                  uint32_t alpha, const int32_t *A, int64_t lda, const int32_t *B, int64_t ldb,
                  uint32_t beta, int32_t *C, int64_t ldc, const ff_opts *opts);

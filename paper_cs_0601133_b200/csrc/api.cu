@@ -4,7 +4,9 @@
 
 #include <cstdint>
 #include <cstring>
+#include <algorithm>
 #include <mutex>
+#include <vector>
 
 #include "internal.h"
 
@@ -22,8 +24,26 @@ struct Buf {
     size_t bytes = 0;
 };
 Buf g_ws[kMaxDev];
-Buf g_host_a[kMaxDev], g_host_b[kMaxDev], g_host_c[kMaxDev];
+Buf g_host_a[kMaxDev], g_host_b[kMaxDev], g_host_c[kMaxDev], g_host_ws[kMaxDev];
 std::mutex g_mu;
+
+// Library-owned streams for the pipelined host entry point.
+struct HostStreams {
+    bool init = false, ok = false;
+    cudaStream_t in = nullptr, comp = nullptr, out = nullptr;
+};
+HostStreams g_hs[kMaxDev];
+
+HostStreams& host_streams(int dev) {
+    HostStreams& h = g_hs[dev];
+    if (!h.init) {
+        h.init = true;
+        h.ok = cudaStreamCreateWithFlags(&h.in, cudaStreamNonBlocking) == cudaSuccess &&
+               cudaStreamCreateWithFlags(&h.comp, cudaStreamNonBlocking) == cudaSuccess &&
+               cudaStreamCreateWithFlags(&h.out, cudaStreamNonBlocking) == cudaSuccess;
+    }
+    return h;
+}
 
 int cur_dev() {
     int d = 0;
@@ -229,34 +249,139 @@ int ff_gemm_host(uint32_t p, char transA, char transB, int64_t m, int64_t n, int
     Plan pl;
     e = make_plan(p, k, opts, &pl);
     if (e) return e;
+    if (opts && opts->host_block < 0) return FF_ERR_OPTS;
+    set_scalars(&pl, alpha, beta);
     const int dev = cur_dev();
     e = arch_check(dev);
     if (e) return e;
-    // Dense device copies of the stored operands (rows x cols as stored).
-    const int64_t ar = is_n(transA) ? m : k, ac = is_n(transA) ? k : m;
-    const int64_t br = is_n(transB) ? k : n, bc = is_n(transB) ? n : k;
     std::lock_guard<std::mutex> lk(g_mu);
-    if ((e = ensure(g_host_a[dev], sizeof(int32_t) * (size_t)(ar * ac > 0 ? ar * ac : 1)))) return e;
-    if ((e = ensure(g_host_b[dev], sizeof(int32_t) * (size_t)(br * bc > 0 ? br * bc : 1)))) return e;
+    HostStreams& hs = host_streams(dev);
+    if (!hs.ok) return FF_ERR_CUDA;
+    const bool tA = is_t(transA), tB = is_t(transB);
+    const bool beta_nz = pl.mp.beta != 0;
+    const int64_t ar = tA ? k : m, ac = tA ? m : k;   // stored A (dense copy on device)
+    const int64_t br = tB ? n : k, bc = tB ? k : n;   // stored B
     if ((e = ensure(g_host_c[dev], sizeof(int32_t) * (size_t)(m * n)))) return e;
-    Plan tmp = pl;
-    if ((e = ensure(g_ws[dev], ws_bytes(tmp, m, n)))) return e;
+    int32_t* dC = static_cast<int32_t*>(g_host_c[dev].ptr);
+    if (k == 0 || pl.mp.alpha == 0) {             // C <- beta C
+        if (beta_nz && cudaMemcpy2DAsync(dC, n * 4, C, ldc * 4, n * 4, m, cudaMemcpyHostToDevice, hs.comp))
+            return FF_ERR_CUDA;
+        if ((e = cuda_rc(launch_scale_c(pl.mp, m, n, dC, n, hs.comp)))) return e;
+        if (cudaMemcpy2DAsync(C, ldc * 4, dC, n * 4, n * 4, m, cudaMemcpyDeviceToHost, hs.comp)) return FF_ERR_CUDA;
+        return cudaStreamSynchronize(hs.comp) == cudaSuccess ? 0 : FF_ERR_CUDA;
+    }
+    // Blocks of C: P row panels x Q column chunks, multiples of 256.
+    int64_t hb = (opts && opts->host_block > 0) ? opts->host_block : 4096;
+    hb = (hb + 255) / 256 * 256;
+    const int64_t P = (m + hb - 1) / hb, Q = (n + hb - 1) / hb;
+    const int64_t mb = std::min<int64_t>(hb, m), nb = std::min<int64_t>(hb, n);
+    const size_t L = static_cast<size_t>(pl.info.L), kp = static_cast<size_t>(pl.info.k_pad);
+    const size_t a_panel = align256(L * mb * kp), b_chunk = align256(L * nb * kp);
+    if ((e = ensure(g_host_a[dev], sizeof(int32_t) * (size_t)(ar * ac)))) return e;
+    if ((e = ensure(g_host_b[dev], sizeof(int32_t) * (size_t)(br * bc)))) return e;
+    if ((e = ensure(g_host_ws[dev], a_panel * P + b_chunk * Q))) return e;
     int32_t* dA = static_cast<int32_t*>(g_host_a[dev].ptr);
     int32_t* dB = static_cast<int32_t*>(g_host_b[dev].ptr);
-    int32_t* dC = static_cast<int32_t*>(g_host_c[dev].ptr);
-    cudaStream_t st = 0;
-    if (ar * ac > 0 && cudaMemcpy2DAsync(dA, ac * 4, A, lda * 4, ac * 4, ar, cudaMemcpyHostToDevice, st))
-        return FF_ERR_CUDA;
-    if (br * bc > 0 && cudaMemcpy2DAsync(dB, bc * 4, B, ldb * 4, bc * 4, br, cudaMemcpyHostToDevice, st))
-        return FF_ERR_CUDA;
-    set_scalars(&pl, alpha, beta);
-    if (pl.mp.beta != 0 &&
-        cudaMemcpy2DAsync(dC, n * 4, C, ldc * 4, n * 4, m, cudaMemcpyHostToDevice, st))
-        return FF_ERR_CUDA;
-    e = run(pl, transA, transB, m, n, k, dA, ac > 1 ? ac : 1, dB, bc > 1 ? bc : 1, dC, n, g_ws[dev].ptr, st);
-    if (e) return e;
-    if (cudaMemcpy2DAsync(C, ldc * 4, dC, n * 4, n * 4, m, cudaMemcpyDeviceToHost, st)) return FF_ERR_CUDA;
-    return cudaStreamSynchronize(st) == cudaSuccess ? 0 : FF_ERR_CUDA;
+    int8_t* wsA = static_cast<int8_t*>(g_host_ws[dev].ptr);
+    int8_t* wsB = wsA + a_panel * P;
+    std::vector<cudaEvent_t> evs;
+    auto mkev = [&]() {
+        cudaEvent_t ev = nullptr;
+        cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+        evs.push_back(ev);
+        return ev;
+    };
+    std::vector<cudaEvent_t> evA(P), evB(Q), evCin(P * Q), evG(P * Q);
+    for (auto& x : evA) x = mkev();
+    for (auto& x : evB) x = mkev();
+    for (auto& x : evG) x = mkev();
+    if (beta_nz)
+        for (auto& x : evCin) x = mkev();
+    auto rows_of = [&](int64_t i, int64_t& r0, int64_t& r1) { r0 = i * hb; r1 = std::min(m, r0 + hb); };
+    auto cols_of = [&](int64_t j, int64_t& c0, int64_t& c1) { c0 = j * hb; c1 = std::min(n, c0 + hb); };
+    bool fail = false;
+    auto chk = [&](cudaError_t x) { if (x != cudaSuccess) fail = true; };
+    // Block order: "growing squares" s = 0, 1, ...: after row panel s of A and
+    // column chunk s of B have arrived, the new blocks (s, 0..s) and (0..s-1, s)
+    // are computable.  Copies in, GEMMs and copies out all follow this order, so
+    // the device->host stream (the PCIe floor: all of C) starts after the first
+    // panel + chunk and is never starved afterwards.
+    std::vector<std::pair<int64_t, int64_t>> order;
+    const int64_t S = std::max(P, Q);
+    for (int64_t sq = 0; sq < S; ++sq) {
+        if (sq < P)
+            for (int64_t j = 0; j <= std::min(sq, Q - 1); ++j) order.push_back({sq, j});
+        if (sq < Q)
+            for (int64_t i = 0; i < std::min(sq, P); ++i) order.push_back({i, sq});
+    }
+    // ---- host -> device (stream hs.in)
+    for (int64_t sq = 0; sq < S && !fail; ++sq) {
+        if (sq < P) {
+            int64_t r0, r1;
+            rows_of(sq, r0, r1);
+            const int64_t rows = r1 - r0;
+            if (!tA) chk(cudaMemcpy2DAsync(dA + r0 * k, k * 4, A + r0 * lda, lda * 4, k * 4, rows, cudaMemcpyHostToDevice, hs.in));
+            else chk(cudaMemcpy2DAsync(dA + r0, m * 4, A + r0, lda * 4, rows * 4, k, cudaMemcpyHostToDevice, hs.in));
+            chk(cudaEventRecord(evA[sq], hs.in));
+        }
+        if (sq < Q) {
+            int64_t c0, c1;
+            cols_of(sq, c0, c1);
+            const int64_t cols = c1 - c0;
+            if (!tB) chk(cudaMemcpy2DAsync(dB + c0, n * 4, B + c0, ldb * 4, cols * 4, k, cudaMemcpyHostToDevice, hs.in));
+            else chk(cudaMemcpy2DAsync(dB + c0 * k, k * 4, B + c0 * ldb, ldb * 4, k * 4, cols, cudaMemcpyHostToDevice, hs.in));
+            chk(cudaEventRecord(evB[sq], hs.in));
+        }
+        if (beta_nz)
+            for (const auto& blk : order) {
+                if (std::max(blk.first, blk.second) != sq) continue;
+                int64_t r0, r1, c0, c1;
+                rows_of(blk.first, r0, r1);
+                cols_of(blk.second, c0, c1);
+                chk(cudaMemcpy2DAsync(dC + r0 * n + c0, n * 4, C + r0 * ldc + c0, ldc * 4, (c1 - c0) * 4, r1 - r0,
+                                      cudaMemcpyHostToDevice, hs.in));
+                chk(cudaEventRecord(evCin[blk.first * Q + blk.second], hs.in));
+            }
+    }
+    // ---- compute (stream hs.comp): encode each operand block once, GEMM each C block
+    std::vector<char> encA(P, 0), encB(Q, 0);
+    for (const auto& blk : order) {
+        if (fail) break;
+        const int64_t i = blk.first, j = blk.second;
+        int64_t r0, r1, c0, c1;
+        rows_of(i, r0, r1);
+        cols_of(j, c0, c1);
+        int8_t* Al = wsA + a_panel * i;
+        int8_t* Bl = wsB + b_chunk * j;
+        if (!encA[i]) {
+            chk(cudaStreamWaitEvent(hs.comp, evA[i], 0));
+            chk(launch_encode(pl, tA ? 0 : 1, r1 - r0, k, tA ? dA + r0 : dA + r0 * k, tA ? m : k, Al, hs.comp));
+            encA[i] = 1;
+        }
+        if (!encB[j]) {
+            chk(cudaStreamWaitEvent(hs.comp, evB[j], 0));
+            chk(launch_encode(pl, tB ? 1 : 0, c1 - c0, k, tB ? dB + c0 * k : dB + c0, tB ? k : n, Bl, hs.comp));
+            encB[j] = 1;
+        }
+        if (beta_nz) chk(cudaStreamWaitEvent(hs.comp, evCin[i * Q + j], 0));
+        if (launch_gemm_tc(pl, r1 - r0, c1 - c0, k, Al, Bl, dC + r0 * n + c0, n, hs.comp)) fail = true;
+        chk(cudaEventRecord(evG[i * Q + j], hs.comp));
+    }
+    // ---- device -> host (stream hs.out): each C block as soon as its GEMM is done
+    for (const auto& blk : order) {
+        if (fail) break;
+        int64_t r0, r1, c0, c1;
+        rows_of(blk.first, r0, r1);
+        cols_of(blk.second, c0, c1);
+        chk(cudaStreamWaitEvent(hs.out, evG[blk.first * Q + blk.second], 0));
+        chk(cudaMemcpy2DAsync(C + r0 * ldc + c0, ldc * 4, dC + r0 * n + c0, n * 4, (c1 - c0) * 4, r1 - r0,
+                              cudaMemcpyDeviceToHost, hs.out));
+    }
+    const cudaError_t s1 = cudaStreamSynchronize(hs.in);
+    const cudaError_t s2 = cudaStreamSynchronize(hs.comp);
+    const cudaError_t s3 = cudaStreamSynchronize(hs.out);
+    for (auto ev : evs) cudaEventDestroy(ev);
+    return (fail || s1 || s2 || s3) ? FF_ERR_CUDA : 0;
 }
 
 int ff_encode(uint32_t p, int64_t k, const ff_opts* opts, int kmajor_src, int64_t rows, const int32_t* X,

@@ -64,15 +64,18 @@ class RowPanelGemm:
     """One rank's share of a row-panel-sharded fgemm (see module docstring)."""
 
     def __init__(self, prob: Problem, group=None, chunks: int = 4, opts=None, device=None,
-                 backend=None):
+                 backend=None, world: int | None = None, rank: int | None = None):
+        """`world`/`rank` override the process group's ("virtual ranks" on one GPU
+        for testing: no broadcast is issued, the caller fills non-zero ranks' B limbs)."""
         import torch
         import torch.distributed as dist
 
         self.torch, self.dist = torch, dist
         self.prob = prob
         self.group = group
-        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
-        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.virtual = world is not None
+        self.world = world if world is not None else (dist.get_world_size(group) if dist.is_initialized() else 1)
+        self.rank = rank if rank is not None else (dist.get_rank(group) if dist.is_initialized() else 0)
         self.row0, self.row1 = panel_bounds(prob.m, self.world, self.rank)
         self.mr = self.row1 - self.row0
         self.chunks = chunk_bounds(prob.n, chunks if self.world > 1 else 1)
@@ -121,7 +124,7 @@ class RowPanelGemm:
                     self.be.ff_encode(pr.p, pr.k, self.opts, kmaj, n1 - n0, src, ldx, bl,
                                       stream=self.comm_stream)
                     launches += 1
-                if self.world > 1:
+                if self.world > 1 and not self.virtual:
                     works.append(self.dist.broadcast(bl, src=0, group=self.group, async_op=True))
                 else:
                     works.append(None)

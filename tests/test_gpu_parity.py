@@ -259,15 +259,22 @@ def test_identity_permutation_on_gpu(env):
     np.testing.assert_array_equal(got, B[sigma])
 
 
-def test_host_entry_point(env):
+@pytest.mark.parametrize("tA,tB,beta,block", [("T", "N", 1, 0), ("N", "N", 0, 256), ("T", "T", 5, 256),
+                                               ("N", "T", 0, 512)])
+def test_host_entry_point(env, tA, tB, beta, block):
+    """ff_gemm_host: host buffers, pipelined over blocks of C (block=256 forces
+    several row panels and column chunks, with ragged last blocks)."""
     torch, ff = env
     p = 8388593
-    rng = np.random.default_rng(5)
-    m, n, k = 333, 444, 555
-    A, B, C = _stored(rng, k, m, p, 1), _stored(rng, k, n, p, 2), _stored(rng, m, n, p, 3)
+    rng = np.random.default_rng(5 + block)
+    m, n, k = 700, 900, 555
+    A = _stored(rng, *((m, k) if tA == "N" else (k, m)), p, 1)
+    B = _stored(rng, *((k, n) if tB == "N" else (n, k)), p, 2)
+    C = _stored(rng, m, n, p, 3)
     out = C.copy()
-    ff.ff_gemm_host(p, "T", "N", m, n, k, 3, A, A.shape[1], B, B.shape[1], 1, out, out.shape[1])
-    _check(p, "T", "N", m, n, k, 3, A, B, 1, C, out)
+    ff.ff_gemm_host(p, tA, tB, m, n, k, 3, A, A.shape[1], B, B.shape[1], beta, out, out.shape[1],
+                    {"host_block": block})
+    _check(p, tA, tB, m, n, k, 3, A, B, beta, C, out)
 
 
 def test_split_entry_points_chunked_B(env):
@@ -345,3 +352,37 @@ def test_baseline_config_sampled_rows_and_freivalds(env, name):
             rhs = (rhs + (beta % p) * oracle.matvec(p, "N", Cin, x).astype(np.int64)) % p
         np.testing.assert_array_equal(lhs, rhs)
     assert out.min() >= 0 and out.max() < p
+
+
+@pytest.mark.parametrize("world,name", [(2, "c1"), (4, "c1"), (3, "mixed")])
+def test_row_panel_virtual_ranks_match_single_gpu(env, world, name):
+    """The multi-GPU row-panel path run as `world` virtual ranks on one GPU (B limbs
+    encoded by rank 0 and copied to the others, standing in for the broadcast):
+    the concatenated panels must equal the single-GPU result bit for bit."""
+    torch, ff = env
+    from paper_cs_0601133_b200.sharded import Problem, RowPanelGemm
+    if name == "c1":
+        p, m, n, k, tA, tB, alpha, beta = 65521, 512, 512, 512, "N", "N", 1, 0
+    else:
+        p, m, n, k, tA, tB, alpha, beta = 67108859, 700, 1100, 300, "T", "N", 67108858, 1
+    rng = np.random.default_rng(world)
+    A = _stored(rng, *((m, k) if tA == "N" else (k, m)), p)
+    B = _stored(rng, *((k, n) if tB == "N" else (n, k)), p)
+    C = _stored(rng, m, n, p)
+    dA, dB = _dev(torch, A), _dev(torch, B)
+    want = _dev(torch, C)
+    ff.fgemm(p, dA, dB, want, alpha, beta, tA, tB)
+    prob = Problem(p, m, n, k, tA, tB, alpha, beta)
+    engs = [RowPanelGemm(prob, chunks=3, world=world, rank=r) for r in range(world)]
+    out = _dev(torch, C)
+    eng0 = engs[0]
+    eng0.step(eng0.a_panel_view(dA), dB, out[eng0.row0:eng0.row1])
+    torch.cuda.synchronize()
+    for e in engs[1:]:
+        for dst, src in zip(e.Bl, eng0.Bl):
+            dst.copy_(src)                       # stands in for the NCCL broadcast
+        e.step(e.a_panel_view(dA), None, out[e.row0:e.row1])
+    torch.cuda.synchronize()
+    assert torch.equal(out, want)
+    got = out.cpu().numpy()
+    np.testing.assert_array_equal(got, oracle.fgemm(p, tA, tB, alpha, A, B, beta, C))
