@@ -66,7 +66,8 @@ extern "C" {
 /* Options for the _ex / split entry points.  Zero-initialise and set fields;
  * a NULL pointer means all defaults. */
 typedef struct ff_opts {
-    int32_t winograd;       /* -1 auto, 0 never, 1 one Winograd level (Table 2) */
+    int32_t winograd;       /* 0 auto, 1 one Winograd level (Table 2; needs even
+                               m, n, k, else FF_ERR_OPTS), -1 never */
     int32_t scheme;         /* FF_SCHEME_*; AUTO picks the fewest limbs, S on ties */
     int64_t kb_override;    /* 0: planner k-block; else k-block length in elements,
                                rounded down to a multiple of 128; must not exceed the
@@ -77,7 +78,10 @@ typedef struct ff_opts {
                                256x256 CTA-pair (tcgen05 cta_group::2) kernel */
     int32_t host_block;     /* ff_gemm_host only: rows/columns of C per pipelined block
                                (rounded up to 256); 0 = auto (~4096) */
-    int32_t reserved[5];
+    int32_t korder;         /* step order of the kernel: 0 auto, 1 group-outer (each weight
+                               group over all of k), 2 k-outer (each k-block through all
+                               groups: L2 locality) */
+    int32_t reserved[4];
 } ff_opts;
 
 /* The plan the library derives from (p, k, opts): host-only, no GPU needed. */
@@ -97,8 +101,9 @@ typedef struct ff_plan_info {
     int32_t centre_max;      /* (p-1)/2 (p/2 for p = 2) */
     int32_t reserved0;
     int64_t carry_max;       /* bound on |value| written back into the accumulator
-                                between steps: centre_max + 385 w (w = 256 if L >= 2) */
-    int32_t reserved[2];
+                                between steps */
+    int32_t korder;          /* 1 group-outer, 2 k-outer */
+    int32_t reserved[1];
 } ff_plan_info;
 
 /* Library version (major*10000 + minor*100 + patch). Host only. */

@@ -105,12 +105,32 @@ int validate(uint32_t p, char transA, char transB, int64_t m, int64_t n, int64_t
     return 0;
 }
 
+// Measured: one level wins on c5 (L = 4, 16384^3: 18% faster),
+// loses on c4 (L = 2, ~2% slower) and on c2 (4096^3, 7 short launches: 65% slower).
+// So: several limbs (the MMA share of the time grows with L^2) and enough
+// half-size tiles to fill the GPU a few times over.
+bool winograd_auto_wins(const Plan& pl, int64_t m, int64_t n, int64_t k) {
+    const int64_t half_tiles = ((m / 2 + 255) / 256) * ((n / 2 + 255) / 256);
+    return pl.info.L >= 3 && half_tiles >= 4 * (num_sms() / 2) && k >= 4096;
+}
+
 size_t ws_bytes(const Plan& pl, int64_t m, int64_t n) {
     const size_t L = static_cast<size_t>(pl.info.L), kp = static_cast<size_t>(pl.info.k_pad);
     return align256(L * static_cast<size_t>(m) * kp) + align256(L * static_cast<size_t>(n) * kp);
 }
 
 int cuda_rc(cudaError_t e) { return e == cudaSuccess ? 0 : FF_ERR_CUDA; }
+
+// One Winograd level: forced by opts->winograd == 1; auto (0)
+// uses it only where it was measured to win.  Returns 1 (use), 0 (classical)
+// or FF_ERR_OPTS (forced but the shape is not even).
+int use_winograd(const Plan& pl, const ff_opts* opts, int64_t m, int64_t n, int64_t k) {
+    const int w = opts ? opts->winograd : 0;
+    const bool even = (m % 2 == 0) && (n % 2 == 0) && (k % 2 == 0) && m >= 512 && n >= 512 && k >= 256;
+    if (w == 1) return even ? 1 : -FF_ERR_OPTS;
+    if (w < 0) return 0;
+    return even && winograd_auto_wins(pl, m, n, k) ? 1 : 0;
+}
 
 // The whole path on device pointers.
 int run(const Plan& pl, char transA, char transB, int64_t m, int64_t n, int64_t k, const int32_t* A,
@@ -205,7 +225,13 @@ size_t ff_gemm_workspace_size(uint32_t p, char transA, char transB, int64_t m, i
     if (m < 0 || n < 0 || k < 0) return 0;
     Plan pl;
     if (make_plan(p, k, opts, &pl)) return 0;
-    return ws_bytes(pl, m, n);
+    size_t need = ws_bytes(pl, m, n);
+    if (use_winograd(pl, opts, m, n, k) == 1) {
+        Plan half;
+        if (make_plan(p, k / 2, opts, &half)) return 0;
+        need = std::max(need, winograd_ws_bytes(half, m, n, k));
+    }
+    return need;
 }
 
 int ff_gemm_ex(uint32_t p, char transA, char transB, int64_t m, int64_t n, int64_t k, uint32_t alpha,
@@ -217,21 +243,31 @@ int ff_gemm_ex(uint32_t p, char transA, char transB, int64_t m, int64_t n, int64
     Plan pl;
     e = make_plan(p, k, opts, &pl);
     if (e) return e;
-    if (opts && opts->winograd == 1) return FF_ERR_OPTS;  // one-level Winograd: see DESIGN.md §7
     set_scalars(&pl, alpha, beta);
+    const int wino = (k == 0 || pl.mp.alpha == 0) ? 0 : use_winograd(pl, opts, m, n, k);
+    if (wino < 0) return -wino;
+    Plan half;
+    if (wino) {
+        if ((e = make_plan(p, k / 2, opts, &half))) return e;
+        set_scalars(&half, alpha, beta);
+    }
     const int dev = cur_dev();
     e = arch_check(dev);
     if (e) return e;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const size_t need = ws_bytes(pl, m, n);
+    const size_t need = wino ? winograd_ws_bytes(half, m, n, k) : ws_bytes(pl, m, n);
+    auto go = [&](void* w) {
+        return wino ? run_winograd(half, is_t(transA), is_t(transB), m, n, k, A, lda, B, ldb, C, ldc, w, st)
+                    : run(pl, transA, transB, m, n, k, A, lda, B, ldb, C, ldc, w, st);
+    };
     if (workspace) {
         if (workspace_bytes < need || (reinterpret_cast<uintptr_t>(workspace) & 255)) return -16;
-        return run(pl, transA, transB, m, n, k, A, lda, B, ldb, C, ldc, workspace, st);
+        return go(workspace);
     }
     std::lock_guard<std::mutex> lk(g_mu);
     e = ensure(g_ws[dev], need);
     if (e) return e;
-    return run(pl, transA, transB, m, n, k, A, lda, B, ldb, C, ldc, g_ws[dev].ptr, st);
+    return go(g_ws[dev].ptr);
 }
 
 int ff_gemm(uint32_t p, char transA, char transB, int64_t m, int64_t n, int64_t k, uint32_t alpha,

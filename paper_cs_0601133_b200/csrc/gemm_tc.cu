@@ -52,13 +52,23 @@ struct Cfg {
     static constexpr int A_BYTES = 128 * kBK;      // per CTA: 128 rows of A
     static constexpr int B_BYTES = (BN / kPair) * kBK;  // per CTA: BN/kPair rows of B
     static constexpr int STAGE = A_BYTES + B_BYTES;
-    static constexpr int STAGES = kPair == 2 ? 6 : 4;
+    static constexpr int STAGES = kPair == 2 ? 7 : 4;
     static constexpr int SMEM = STAGES * STAGE + 256 + 1024;
+};
+
+// One output of the fused epilogue: C_q <- (a * R + b * C_q) mod p.  A plain
+// fgemm has one output (a = alpha, b = beta); a Winograd product adds +-alpha*P
+// into up to four quadrants of C.
+struct GemmOut {
+    int32_t* C;
+    uint32_t a, a_sh, b, b_sh;
+    int32_t vec;       // 1 if rows of C are 16-byte aligned
 };
 
 struct GemmArgs {
     ModP mp;
-    int32_t* C;
+    GemmOut out[4];
+    int32_t nout;
     int64_t ldc;
     int32_t m, n;
     int32_t tiles_m, tiles_n, num_tiles;
@@ -69,10 +79,22 @@ struct GemmArgs {
     int8_t pair_i[16], pair_j[16];
     int8_t group_first[8], group_len[8];
     uint32_t idesc[16];
-    int32_t vec_store;  // 1 if C rows are 16-byte aligned
     int32_t raster;     // tile-rows per raster band
     int32_t hints;      // bit0: TMA loads evict_last; bit1: C stores evict_first
+    int32_t last_use;   // 1 if no later launch reads these outputs (streaming stores allowed)
+    unsigned long long* trace;  // optional per-CTA cycle counters (FF_TRACE=1), else null
+    int32_t debug_same_tile;    // experiment only: tm, tn taken mod this (wrong results)
+    int32_t korder;             // 1 group-outer, 2 k-outer
+    uint32_t kinv, kinv_sh;     // k-outer: 256^-(G-1) mod p
+    const uint8_t* die_map;     // die-aware schedule (dies.cu): die of each %smid, or null
+    int* sched;                 // per-launch counters: [0],[1] clusters per die, [2] arrivals
 };
+
+__device__ __forceinline__ unsigned long long clk() {
+    unsigned long long c;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+    return c;
+}
 
 struct Smem {
     uint64_t full[8];
@@ -80,6 +102,7 @@ struct Smem {
     uint64_t accfull[2];
     uint64_t accempty[2];
     uint32_t tmem_base;
+    int32_t sched[4];   // unit, nunits, first tile, tile count of this cluster's die
 };
 
 __device__ __forceinline__ void tile_coords(const GemmArgs& a, int t, int& tm, int& tn) {
@@ -89,22 +112,32 @@ __device__ __forceinline__ void tile_coords(const GemmArgs& a, int t, int& tm, i
     const int rows_in_band = min(a.raster, a.tiles_m - band * a.raster);
     tm = band * a.raster + idx % rows_in_band;
     tn = idx / rows_in_band;
+    if (a.debug_same_tile) { tm %= a.debug_same_tile; tn %= a.debug_same_tile; }   // experiment only
 }
 
-// The common schedule every role walks: tiles in pairs (one per TMEM slot),
-// groups from the highest weight down, k-blocks in order, then the slots.
+// The common schedule every role walks: tiles in pairs (one per TMEM slot);
+// per tile pair either groups (highest weight first) outer and k-blocks inner
+// (group-outer), or k-blocks outer and all groups inner (k-outer, so a k-slice
+// of every limb is reused from L2 by all groups); the two slots innermost.
+// Tiles of this cluster: base + unit + j * nunits for j = 0, 1, ... < count.
 template <class F>
-__device__ __forceinline__ void for_each_step(const GemmArgs& a, int unit, int nunits, F&& f) {
-    for (int t0 = unit; t0 < a.num_tiles; t0 += 2 * nunits) {
+__device__ __forceinline__ void for_each_step(const GemmArgs& a, int unit, int nunits, int base, int count, F&& f) {
+    for (int t0 = unit; t0 < count; t0 += 2 * nunits) {
         const int t1 = t0 + nunits;
-        const int nslots = t1 < a.num_tiles ? 2 : 1;
-        for (int g = a.G - 1; g >= 0; --g)
+        const int nslots = t1 < count ? 2 : 1;
+        if (a.korder == 2) {
             for (int kb = 0; kb < a.nkb; ++kb)
-                for (int s = 0; s < nslots; ++s) f(s == 0 ? t0 : t1, s, g, kb);
+                for (int g = a.G - 1; g >= 0; --g)
+                    for (int s = 0; s < nslots; ++s) f(base + (s == 0 ? t0 : t1), s, g, kb);
+        } else {
+            for (int g = a.G - 1; g >= 0; --g)
+                for (int kb = 0; kb < a.nkb; ++kb)
+                    for (int s = 0; s < nslots; ++s) f(base + (s == 0 ? t0 : t1), s, g, kb);
+        }
     }
 }
 
-template <int kPair>
+template <int kPair, bool kTrace>
 __global__ void __launch_bounds__(kThreads, 1)
     ffgemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ GemmArgs a) {
@@ -116,7 +149,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane = ptx::lane_id();
     const uint32_t rank = kPair == 2 ? ptx::cluster_ctarank() : 0;
     const bool leader = (rank == 0);
-    const int unit = blockIdx.x / kPair, nunits = gridDim.x / kPair;
 
     if (threadIdx.x == 0) {
         ptx::tma_prefetch(&tmA);
@@ -135,10 +167,47 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (kPair == 2) ptx::tmem_alloc_pair(&sh->tmem_base, kTmemCols);
         else ptx::tmem_alloc(&sh->tmem_base, kTmemCols);
     }
+    // Work assignment.  Plain: cluster c takes tiles c, c + C, ...  Die-aware: each
+    // cluster registers on its die's counter, waits until every cluster of the
+    // launch has registered (co-residency is guaranteed by the cooperative launch),
+    // and the tile raster is split between the dies in proportion to their cluster
+    // counts, so each die's L2 holds only its own operands.
+    if (threadIdx.x == 0 && leader) {
+        const int nclusters = gridDim.x / kPair;
+        int unit = blockIdx.x / kPair, nunits = nclusters, base = 0, count = a.num_tiles;
+        if (a.die_map) {
+            uint32_t smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            const int d = a.die_map[smid] ? 1 : 0;
+            unit = atomicAdd(&a.sched[d], 1);
+            __threadfence();
+            atomicAdd(&a.sched[2], 1);
+            while (atomicAdd(&a.sched[2], 0) < nclusters) __nanosleep(64);
+            const int n0 = atomicAdd(&a.sched[0], 0), n1 = nclusters - n0;
+            const int T0 = n1 == 0 ? a.num_tiles
+                                   : (n0 == 0 ? 0 : static_cast<int>(static_cast<long long>(a.num_tiles) * n0 / nclusters));
+            nunits = d ? n1 : n0;
+            base = d ? T0 : 0;
+            count = d ? a.num_tiles - T0 : T0;
+        }
+        sh->sched[0] = unit; sh->sched[1] = nunits; sh->sched[2] = base; sh->sched[3] = count;
+    }
     ptx::tc_fence_before();
     if (kPair == 2) ptx::cluster_sync();
     else __syncthreads();
     ptx::tc_fence_after();
+    if (kPair == 2) {   // the peer CTA takes the leader's assignment (DSMEM read)
+        if (threadIdx.x == 0 && !leader) {
+            for (int i = 0; i < 4; ++i) {
+                const uint32_t ra = ptx::mapa(ptx::smem_u32(&sh->sched[i]), 0);
+                int v;
+                asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(ra) : "memory");
+                sh->sched[i] = v;
+            }
+        }
+        ptx::cluster_sync();
+    }
+    const int unit = sh->sched[0], nunits = sh->sched[1], tbase = sh->sched[2], tcount = sh->sched[3];
     const uint32_t tmem_base = sh->tmem_base;
 
     if (warp == 0) {
@@ -146,7 +215,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             uint32_t stage = 0, phase = 0;
             const uint64_t pol = (a.hints & 1) ? ptx::policy_evict_last() : ptx::policy_evict_normal();
-            for_each_step(a, unit, nunits, [&](int tile, int, int g, int kb) {
+            for_each_step(a, unit, nunits, tbase, tcount, [&](int tile, int, int g, int kb) {
                 int tm, tn;
                 tile_coords(a, tile, tm, tn);
                 const int arow = tm * K::BM + static_cast<int>(rank) * 128;
@@ -179,9 +248,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0 && leader) {
             uint32_t stage = 0, phase = 0;
             uint32_t acc_par[2] = {0, 0};
-            for_each_step(a, unit, nunits, [&](int, int slot, int g, int kb) {
+            unsigned long long t_start = clk(), w_acc = 0, w_full = 0, nsteps = 0;
+            for_each_step(a, unit, nunits, tbase, tcount, [&](int, int slot, int g, int kb) {
+                const unsigned long long t0 = kTrace ? clk() : 0;
                 if (kPair == 2) ptx::mbar_wait_cluster(&sh->accempty[slot], acc_par[slot] ^ 1);
                 else ptx::mbar_wait(&sh->accempty[slot], acc_par[slot] ^ 1);
+                if (kTrace) { w_acc += clk() - t0; ++nsteps; }
                 acc_par[slot] ^= 1;
                 ptx::tc_fence_after();
                 const uint32_t d = tmem_base + slot * kTileN;
@@ -191,7 +263,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int pi = a.group_first[g]; pi < a.group_first[g] + a.group_len[g]; ++pi) {
                     const uint32_t idesc = a.idesc[pi];
                     for (int ks = ks0; ks < ks1; ++ks) {
+                        const unsigned long long t1 = kTrace ? clk() : 0;
                         ptx::mbar_wait(&sh->full[stage], phase);
+                        if (kTrace) w_full += clk() - t1;
                         ptx::tc_fence_after();
                         const uint32_t sa = ptx::smem_u32(smem + stage * K::STAGE);
                         const uint64_t da = ptx::smem_desc_sw128(sa);
@@ -212,6 +286,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (kPair == 2) ptx::tc_commit_pair(&sh->accfull[slot]);
                 else ptx::tc_commit(&sh->accfull[slot]);
             });
+            if (kTrace) {
+                unsigned long long* tr = a.trace + blockIdx.x * 8;
+                tr[0] = clk() - t_start;  // MMA thread lifetime (cycles)
+                tr[1] = w_acc;            // waiting for the epilogue to free a TMEM slot
+                tr[2] = w_full;           // waiting for TMA data
+                tr[3] = nsteps;
+            }
         }
     } else {
         // ------------------------------------------------ epilogue warps (both CTAs)
@@ -221,24 +302,49 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t accempty_leader0 = kPair == 2 ? ptx::mapa(ptx::smem_u32(&sh->accempty[0]), 0) : 0;
         const uint32_t accempty_leader1 = kPair == 2 ? ptx::mapa(ptx::smem_u32(&sh->accempty[1]), 0) : 0;
         uint32_t acc_par[2] = {0, 0};
-        for_each_step(a, unit, nunits, [&](int tile, int slot, int g, int kb) {
+        unsigned long long e_wait = 0, e_busy = 0, e_final = 0;
+        for_each_step(a, unit, nunits, tbase, tcount, [&](int tile, int slot, int g, int kb) {
+            const unsigned long long t0 = kTrace ? clk() : 0;
             ptx::mbar_wait(&sh->accfull[slot], acc_par[slot]);
+            const unsigned long long t1 = kTrace ? clk() : 0;
             acc_par[slot] ^= 1;
             ptx::tc_fence_after();
             const bool last_kb = (kb == a.nkb - 1);
             const bool final_step = last_kb && g == 0;
+            // Write-back factor: x256 (Horner) when the next step is the next-lower group;
+            // k-outer order: 256^-(G-1) (exact) when the next step restarts the groups
+            // on the next k-block; group-outer order: x1 between k-blocks of a group.
+            const bool horner = (a.korder == 2) ? (g > 0) : last_kb;
+            const bool rescale = (a.korder == 2) && g == 0 && !last_kb;
             const uint32_t tcol = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + slot * kTileN + h * 64;
-            if (!final_step) {
-                // delayed reduction between steps (+ Horner x256 after the last k-block of a group)
+            if (rescale) {
                 uint32_t v[64];
                 ptx::tmem_ld64(tcol, v);
                 ptx::tmem_wait_ld();
-                const int32_t w = last_kb ? 256 : 1;
-                const float f = last_kb ? M.w256_over_p : M.inv_p;
 #pragma unroll
                 for (int t = 0; t < 64; ++t)
-                    v[t] = static_cast<uint32_t>(reduce_approx(static_cast<int32_t>(v[t]), w, f,
-                                                               static_cast<int32_t>(M.p)));
+                    v[t] = static_cast<uint32_t>(centre(mulmod_shoup(residue_i32(static_cast<int32_t>(v[t]), M),
+                                                                     a.kinv, a.kinv_sh, M.p), M));
+                ptx::tmem_st64(tcol, v);
+                ptx::tmem_wait_st();
+            } else if (!final_step) {
+                // delayed reduction between steps (+ Horner x256 before the next-lower group)
+                uint32_t v[64];
+                ptx::tmem_ld64(tcol, v);
+                ptx::tmem_wait_ld();
+                const int32_t w = horner ? 256 : 1;
+                if (M.int_wb) {
+                    const int32_t mm = horner ? M.m256 : M.m1;
+#pragma unroll
+                    for (int t = 0; t < 64; ++t)
+                        v[t] = static_cast<uint32_t>(reduce_mulhi(static_cast<int32_t>(v[t]), w, mm, M.p));
+                } else {
+                    const float f = horner ? M.w256_over_p : M.inv_p;
+#pragma unroll
+                    for (int t = 0; t < 64; ++t)
+                        v[t] = static_cast<uint32_t>(reduce_approx(static_cast<int32_t>(v[t]), w, f,
+                                                                   static_cast<int32_t>(M.p)));
+                }
                 ptx::tmem_st64(tcol, v);
                 ptx::tmem_wait_st();
             } else {
@@ -252,42 +358,46 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::tmem_wait_ld();
                     if (row >= a.m) continue;
                     const int col0 = tn * K::BN + h * 64 + half * 32;
-                    int32_t* crow = a.C + static_cast<int64_t>(row) * a.ldc + col0;
-                    const bool full = a.vec_store && (col0 + 32 <= a.n);
-                    uint32_t o[32];
-                    if (M.beta != 0) {
-                        if (full) {
 #pragma unroll
-                            for (int t = 0; t < 8; ++t) {
-                                const int4 x = *reinterpret_cast<const int4*>(crow + 4 * t);
-                                o[4 * t] = x.x; o[4 * t + 1] = x.y; o[4 * t + 2] = x.z; o[4 * t + 3] = x.w;
+                    for (int t = 0; t < 32; ++t) v[t] = residue_i32(static_cast<int32_t>(v[t]), M);  // exact R
+#pragma unroll 1
+                    for (int qo = 0; qo < a.nout; ++qo) {
+                        const GemmOut O = a.out[qo];
+                        int32_t* crow = O.C + static_cast<int64_t>(row) * a.ldc + col0;
+                        const bool full = O.vec && (col0 + 32 <= a.n);
+                        uint32_t o[32];
+                        if (O.b != 0) {
+                            if (full) {
+#pragma unroll
+                                for (int t = 0; t < 8; ++t) {
+                                    const int4 x = *reinterpret_cast<const int4*>(crow + 4 * t);
+                                    o[4 * t] = x.x; o[4 * t + 1] = x.y; o[4 * t + 2] = x.z; o[4 * t + 3] = x.w;
+                                }
+                            } else {
+#pragma unroll
+                                for (int t = 0; t < 32; ++t) o[t] = (col0 + t < a.n) ? crow[t] : 0;
                             }
+                        }
+#pragma unroll
+                        for (int t = 0; t < 32; ++t) {
+                            uint32_t r = mulmod_shoup(v[t], O.a, O.a_sh, M.p);
+                            if (O.b != 0)
+                                r = addmod(r, mulmod_shoup(residue_i32(static_cast<int32_t>(o[t]), M), O.b, O.b_sh, M.p), M.p);
+                            o[t] = r;
+                        }
+                        if (full && (a.hints & 2) && qo == a.nout - 1 && a.last_use) {
+#pragma unroll
+                            for (int t = 0; t < 8; ++t)
+                                ptx::st_global_v4_stream(crow + 4 * t, o[4 * t], o[4 * t + 1], o[4 * t + 2], o[4 * t + 3]);
+                        } else if (full) {
+#pragma unroll
+                            for (int t = 0; t < 8; ++t)
+                                *reinterpret_cast<int4*>(crow + 4 * t) = make_int4(o[4 * t], o[4 * t + 1], o[4 * t + 2], o[4 * t + 3]);
                         } else {
 #pragma unroll
-                            for (int t = 0; t < 32; ++t) o[t] = (col0 + t < a.n) ? crow[t] : 0;
+                            for (int t = 0; t < 32; ++t)
+                                if (col0 + t < a.n) crow[t] = static_cast<int32_t>(o[t]);
                         }
-                    }
-#pragma unroll
-                    for (int t = 0; t < 32; ++t) {
-                        uint32_t r = mulmod_shoup(residue_i32(static_cast<int32_t>(v[t]), M), M.alpha, M.alpha_sh, M.p);
-                        if (M.beta != 0) {
-                            const uint32_t cr = residue_i32(static_cast<int32_t>(o[t]), M);
-                            r = addmod(r, mulmod_shoup(cr, M.beta, M.beta_sh, M.p), M.p);
-                        }
-                        o[t] = r;
-                    }
-                    if (full && (a.hints & 2)) {
-#pragma unroll
-                        for (int t = 0; t < 8; ++t)
-                            ptx::st_global_v4_stream(crow + 4 * t, o[4 * t], o[4 * t + 1], o[4 * t + 2], o[4 * t + 3]);
-                    } else if (full) {
-#pragma unroll
-                        for (int t = 0; t < 8; ++t)
-                            *reinterpret_cast<int4*>(crow + 4 * t) = make_int4(o[4 * t], o[4 * t + 1], o[4 * t + 2], o[4 * t + 3]);
-                    } else {
-#pragma unroll
-                        for (int t = 0; t < 32; ++t)
-                            if (col0 + t < a.n) crow[t] = static_cast<int32_t>(o[t]);
                     }
                 }
             }
@@ -297,7 +407,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (kPair == 2) ptx::mbar_arrive_cluster(slot ? accempty_leader1 : accempty_leader0);
                 else ptx::mbar_arrive(&sh->accempty[slot]);
             }
+            if (kTrace) {
+                const unsigned long long t2 = clk();
+                e_wait += t1 - t0;
+                if (final_step) e_final += t2 - t1; else e_busy += t2 - t1;
+            }
         });
+        if (kTrace && warp == 2 && lane == 0) {
+            unsigned long long* tr = a.trace + blockIdx.x * 8;
+            tr[4] = e_wait;   // epilogue waiting for an accumulator
+            tr[5] = e_busy;   // epilogue work on intermediate steps
+            tr[6] = e_final;  // epilogue work on final steps (stores)
+        }
     }
 
     ptx::tc_fence_before();
@@ -354,16 +475,29 @@ uint32_t make_idesc(bool a_signed, bool b_signed, bool saturate, int M, int N) {
     return d;
 }
 
+uint32_t shoup_host(uint32_t w, uint32_t p) { return static_cast<uint32_t>((static_cast<uint64_t>(w) << 32) / p); }
+
 template <int kPair>
 int launch_impl(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A_limbs, const int8_t* B_limbs,
-                int32_t* C, int64_t ldc, cudaStream_t st) {
+                const OutSpec* outs, int nout, int64_t ldc, int last_use, cudaStream_t st) {
     using K = Cfg<kPair>;
     const ff_plan_info& I = pl.info;
     if (m > INT32_MAX - K::BM || n > INT32_MAX - K::BN) return -2;
     GemmArgs a;
     std::memset(&a, 0, sizeof(a));
     a.mp = pl.mp;
-    a.C = C;
+    if (nout < 1 || nout > 4) return -10;
+    a.nout = nout;
+    for (int q = 0; q < nout; ++q) {
+        const uint32_t p = pl.mp.p;
+        a.out[q].C = outs[q].C;
+        a.out[q].a = outs[q].a % p;
+        a.out[q].a_sh = shoup_host(a.out[q].a, p);
+        a.out[q].b = outs[q].b % p;
+        a.out[q].b_sh = shoup_host(a.out[q].b, p);
+        a.out[q].vec = ((ldc % 4) == 0 && (reinterpret_cast<uintptr_t>(outs[q].C) & 15) == 0) ? 1 : 0;
+    }
+    a.last_use = last_use;
     a.ldc = ldc;
     a.m = static_cast<int32_t>(m);
     a.n = static_cast<int32_t>(n);
@@ -386,7 +520,34 @@ int launch_impl(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A
         a.group_first[w] = static_cast<int8_t>(pl.group_first[w]);
         a.group_len[w] = static_cast<int8_t>(pl.group_len[w]);
     }
-    a.vec_store = ((ldc % 4) == 0 && (reinterpret_cast<uintptr_t>(C) & 15) == 0) ? 1 : 0;
+    a.trace = nullptr;
+    static unsigned long long* trace_buf = nullptr;
+    const bool tracing = getenv("FF_TRACE") != nullptr;
+    if (tracing) {
+        if (!trace_buf) cudaMalloc(&trace_buf, 8 * 1024 * sizeof(unsigned long long));
+        cudaMemsetAsync(trace_buf, 0, 8 * 1024 * sizeof(unsigned long long), st);
+        a.trace = trace_buf;
+    }
+    a.die_map = nullptr;
+    a.sched = nullptr;
+    {
+        const uint8_t* dm = nullptr;
+        int* ring = nullptr;
+        const int64_t units_total = (nt < num_sms() / kPair) ? nt : num_sms() / kPair;
+        if (kPair == 2 && units_total >= 8 && die_schedule(&dm, &ring)) {
+            static unsigned slot = 0;                 // fresh counters per launch (ring of 4096)
+            int* c = ring + 4 * (slot++ % 4096);
+            if (cudaMemsetAsync(c, 0, 4 * sizeof(int), st) == cudaSuccess) {
+                a.die_map = dm;
+                a.sched = c;
+            }
+        }
+    }
+    a.debug_same_tile = 0;
+    if (const char* e = getenv("FF_DEBUG_SAMETILE")) a.debug_same_tile = atoi(e) > 0 ? atoi(e) : 1;
+    a.korder = pl.korder;
+    a.kinv = pl.kinv;
+    a.kinv_sh = pl.kinv_sh;
     a.raster = kRasterDefault;
     a.hints = 3;  // TMA loads evict_last, C stores streaming (swept on c4)
     if (const char* e = getenv("FF_RASTER")) a.raster = atoi(e) > 0 ? atoi(e) : kRasterDefault;
@@ -398,8 +559,10 @@ int launch_impl(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A
 
     static bool attr_set = false;
     if (!attr_set) {
-        if (cudaFuncSetAttribute(ffgemm_tc_kernel<kPair>, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM) !=
-            cudaSuccess)
+        if (cudaFuncSetAttribute(ffgemm_tc_kernel<kPair, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM) !=
+                cudaSuccess ||
+            cudaFuncSetAttribute(ffgemm_tc_kernel<kPair, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM) !=
+                cudaSuccess)
             return FF_ERR_CUDA;
         attr_set = true;
     }
@@ -410,27 +573,55 @@ int launch_impl(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = K::SMEM;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = kPair;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeCooperative;   // all CTAs co-resident (die-aware registration)
+    attr[1].val.cooperative = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    if (cudaLaunchKernelEx(&cfg, ffgemm_tc_kernel<kPair>, mapA, mapB, a) != cudaSuccess) return FF_ERR_CUDA;
+    cfg.numAttrs = a.die_map ? 2 : 1;
+    const cudaError_t lerr = tracing ? cudaLaunchKernelEx(&cfg, ffgemm_tc_kernel<kPair, true>, mapA, mapB, a)
+                                     : cudaLaunchKernelEx(&cfg, ffgemm_tc_kernel<kPair, false>, mapA, mapB, a);
+    if (lerr != cudaSuccess) return FF_ERR_CUDA;
+    if (tracing) {  // development aid: per-CTA cycle counters, averaged over MMA-issuing CTAs
+        unsigned long long h[8 * 1024];
+        cudaStreamSynchronize(st);
+        cudaMemcpy(h, trace_buf, sizeof(unsigned long long) * 8 * grid, cudaMemcpyDeviceToHost);
+        double s[8] = {0};
+        int nl = 0, ne = 0;
+        for (int b = 0; b < grid; ++b) {
+            if (h[8 * b] > 0) { ++nl; for (int i = 0; i < 4; ++i) s[i] += h[8 * b + i]; }
+            if (h[8 * b + 4] + h[8 * b + 5] > 0) { ++ne; for (int i = 4; i < 7; ++i) s[i] += h[8 * b + i]; }
+        }
+        for (int i = 0; i < 4; ++i) s[i] /= nl > 0 ? nl : 1;
+        for (int i = 4; i < 7; ++i) s[i] /= ne > 0 ? ne : 1;
+        fprintf(stderr, "[ff trace] kPair=%d m=%lld n=%lld k=%lld steps/CTA=%.0f  MMA thread: life %.3g cyc, "
+                "wait slot %.1f%%, wait data %.1f%% | epilogue: wait %.1f%%, step work %.1f%% (%.0f cyc/step), "
+                "final %.1f%%\n", kPair, (long long)m, (long long)n, (long long)k, s[3], s[0], 100 * s[1] / s[0],
+                100 * s[2] / s[0], 100 * s[4] / s[0], 100 * s[5] / s[0], s[5] / (s[3] > 0 ? s[3] : 1), 100 * s[6] / s[0]);
+    }
     return cudaGetLastError() == cudaSuccess ? 0 : FF_ERR_CUDA;
 }
 
 }  // namespace
 
-int launch_gemm_tc(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A_limbs, const int8_t* B_limbs,
-                   int32_t* C, int64_t ldc, cudaStream_t st) {
+int launch_gemm_tc_multi(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A_limbs,
+                         const int8_t* B_limbs, const OutSpec* outs, int nout, int64_t ldc, int last_use,
+                         cudaStream_t st) {
     // The CTA-pair kernel unless the problem has too few 256 x 256 tiles to
     // occupy the GPU (then the 128 x 256 single-CTA kernel gives more CTAs).
     const int64_t pair_tiles = ((m + 255) / 256) * ((n + 255) / 256);
     if (pl.force_pair == 1 || (pl.force_pair == 0 && pair_tiles * 2 < num_sms()))
-        return launch_impl<1>(pl, m, n, k, A_limbs, B_limbs, C, ldc, st);
-    return launch_impl<2>(pl, m, n, k, A_limbs, B_limbs, C, ldc, st);
+        return launch_impl<1>(pl, m, n, k, A_limbs, B_limbs, outs, nout, ldc, last_use, st);
+    return launch_impl<2>(pl, m, n, k, A_limbs, B_limbs, outs, nout, ldc, last_use, st);
+}
+
+int launch_gemm_tc(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A_limbs, const int8_t* B_limbs,
+                   int32_t* C, int64_t ldc, cudaStream_t st) {
+    const OutSpec o = {C, pl.mp.alpha, pl.mp.beta};
+    return launch_gemm_tc_multi(pl, m, n, k, A_limbs, B_limbs, &o, 1, ldc, 1, st);
 }
 
 }  // namespace ff

@@ -28,6 +28,8 @@ struct ModP {
     uint32_t beta, beta_sh;
     float inv_p;          // fl(1/p)
     float w256_over_p;    // fl(256/p)
+    int32_t m1, m256;     // round(w 2^32 / p) for w = 1, 256 (clamped to 2^31-1), integer write-back
+    int32_t int_wb;       // 1: integer write-back (p < 2^29), 0: fp32-reciprocal write-back
 };
 
 struct Plan {
@@ -40,7 +42,11 @@ struct Plan {
     int group_len[kMaxGroups];
     bool saturate;
     int force_pair;                  // 0 auto, 1 single-CTA kernel, 2 CTA-pair kernel
+    int korder;                      // 1 group-outer, 2 k-outer step order
+    uint32_t kinv, kinv_sh;          // 256^-(G-1) mod p and its Shoup constant (k-outer carry)
 };
+
+constexpr int64_t kKbLocalityBytes = 8192;  // L * kb per row-slice in k-outer order (swept on c4, c5)
 
 // planner.cpp
 int make_plan(uint32_t p, int64_t k, const ff_opts* opts, Plan* out);
@@ -53,8 +59,20 @@ cudaError_t launch_scale_c(const ModP& mp, int64_t m, int64_t n, int32_t* C, int
                            cudaStream_t st);
 
 // gemm_tc.cu
+struct OutSpec {          // C <- (a * A B + b * C) mod p for one output block
+    int32_t* C;
+    uint32_t a, b;
+};
+int launch_gemm_tc_multi(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A_limbs,
+                         const int8_t* B_limbs, const OutSpec* outs, int nout, int64_t ldc, int last_use,
+                         cudaStream_t st);
 int launch_gemm_tc(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A_limbs,
                    const int8_t* B_limbs, int32_t* C, int64_t ldc, cudaStream_t st);
+
+// winograd.cu
+size_t winograd_ws_bytes(const Plan& half, int64_t m, int64_t n, int64_t k);
+int run_winograd(const Plan& half, bool transA, bool transB, int64_t m, int64_t n, int64_t k, const int32_t* A,
+                 int64_t lda, const int32_t* B, int64_t ldb, int32_t* C, int64_t ldc, void* ws, cudaStream_t st);
 
 // gen.cu
 cudaError_t launch_fill_uniform(int32_t* X, int64_t rows, int64_t cols, int64_t ld, uint32_t p,
@@ -62,5 +80,8 @@ cudaError_t launch_fill_uniform(int32_t* X, int64_t rows, int64_t cols, int64_t 
                                 cudaStream_t st);
 
 int num_sms();
+
+// dies.cu: SM -> die map and per-launch counter ring for the die-aware schedule
+bool die_schedule(const uint8_t** die_map, int** sched);
 
 }  // namespace ff

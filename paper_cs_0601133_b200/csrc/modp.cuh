@@ -51,6 +51,16 @@ __device__ __forceinline__ int32_t reduce_approx(int32_t a, int32_t w, float w_o
                                 static_cast<uint32_t>(q) * static_cast<uint32_t>(p));
 }
 
+// Same purpose with integer instructions only (no int<->float conversions,
+// which issue at quarter rate): q = floor(a * m / 2^32) with
+// m = round(w 2^32 / p) (clamped to 2^31-1) estimates a*w/p within [-1.5, +0.5],
+// so v = a*w - q*p (wrapping 32-bit) lies in [-p/2, 3p/2].  Valid while
+// 2p < 2^31 (the planner uses it for p < 2^29); DESIGN.md §4.4.
+__device__ __forceinline__ int32_t reduce_mulhi(int32_t a, uint32_t w, int32_t m, uint32_t p) {
+    const int32_t q = __mulhi(a, m);
+    return static_cast<int32_t>(static_cast<uint32_t>(a) * w - static_cast<uint32_t>(q) * p);
+}
+
 __device__ __forceinline__ uint32_t addmod(uint32_t a, uint32_t b, uint32_t p) {
     const uint32_t s = a + b;  // < 2p < 2^32
     return s >= p ? s - p : s;

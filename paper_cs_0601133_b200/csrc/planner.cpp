@@ -68,6 +68,7 @@ int make_plan(uint32_t p, int64_t k, const ff_opts* opts, Plan* out) {
     if (o.winograd < -1 || o.winograd > 1) return FF_ERR_OPTS;
     if (o.kb_override < 0) return FF_ERR_OPTS;
     if (o.cta_group < 0 || o.cta_group > 2) return FF_ERR_OPTS;
+    if (o.korder < 0 || o.korder > 2) return FF_ERR_OPTS;
 
     Plan pl;
     std::memset(&pl, 0, sizeof(pl));
@@ -111,15 +112,29 @@ int make_plan(uint32_t p, int64_t k, const ff_opts* opts, Plan* out) {
         if (b > bmax) bmax = b;
     }
     I.group_bound_max = bmax;
-    // Carry written back between steps: |v| <= p/2 + 385 w with w = 256 for the
-    // Horner scaling (L >= 2) and w = 1 otherwise (modp.cuh, reduce_approx).
-    const int64_t carry = cmax + (L >= 2 ? 385 * 256 : 385);
+    // Carry written back between steps (modp.cuh): integer write-back
+    // (p < 2^29) leaves |v| <= 3p/2; the fp32-reciprocal one |v| <= p/2 + 385 w
+    // with w = 256 for the Horner scaling (L >= 2) and w = 1 otherwise.
+    // (m = round(w 2^32/p) must fit in int32 for every w used: p >= 512 when the
+    // Horner factor w = 256 occurs, i.e. L >= 2.)
+    const bool int_wb = p < (1u << 29) && (L == 1 || p >= 512);
+    const int64_t carry = int_wb ? (3 * (int64_t)p + 1) / 2 : cmax + (L >= 2 ? 385 * 256 : 385);
     I.carry_max = carry;
     I.kb_max = bmax > 0 ? (((int64_t)1 << 31) - 1 - carry) / bmax : ((int64_t)1 << 40);
+    // Step order: k-outer needs 256 invertible mod p when there are several groups.
+    int korder = o.korder == 0 ? 2 : o.korder;
+    if (const char* e = getenv("FF_KORDER")) korder = atoi(e) == 1 ? 1 : 2;  // experiment only
+    if (korder == 2 && L > 1 && (p % 2) == 0) korder = 1;
+    pl.korder = korder;
+    I.korder = korder;
     int64_t kb = I.kb_max;
     if (o.kb_override > 0) {
         if (o.kb_override > I.kb_max || o.kb_override < kBK) return FF_ERR_OPTS;
         kb = o.kb_override;
+    } else if (korder == 2) {
+        int64_t loc = (kKbLocalityBytes / L + kBK - 1) / kBK * kBK;   // L=1: 8192, 2: 4096, 3: 2816, 4: 2048
+        if (const char* e = getenv("FF_KBLOC")) loc = atoll(e) > 0 ? atoll(e) : loc;  // experiment only
+        kb = loc < kb ? loc : kb;
     }
     kb = (kb / kBK) * kBK;
     if (kb < kBK) return FF_ERR_INTERNAL;
@@ -155,6 +170,27 @@ int make_plan(uint32_t p, int64_t k, const ff_opts* opts, Plan* out) {
     M.w256_sh = shoup(M.w256, p);
     M.inv_p = (float)(1.0 / (double)p);
     M.w256_over_p = (float)(256.0 / (double)p);
+    auto mround = [&](double w) {
+        const double v = w * 4294967296.0 / (double)p + 0.5;
+        return (int32_t)(v >= 2147483647.0 ? 2147483647.0 : v);
+    };
+    M.m1 = mround(1.0);
+    M.m256 = mround(256.0);
+    M.int_wb = int_wb ? 1 : 0;
+    // 256^-(G-1) mod p (k-outer carry between k-blocks); 1 when G = 1.
+    pl.kinv = 1 % p;
+    if (korder == 2 && I.groups > 1) {
+        int64_t r0 = p, r1 = 256 % p, s0 = 0, s1 = 1;     // extended Euclid: s1 * 256 = r1 (mod p)
+        while (r1 != 0) {
+            const int64_t qq = r0 / r1, t = r0 - qq * r1, u = s0 - qq * s1;
+            r0 = r1; r1 = t; s0 = s1; s1 = u;
+        }
+        int64_t inv = ((s0 % (int64_t)p) + p) % p;          // r0 == 1 since p is odd
+        uint64_t acc = 1;
+        for (int g = 0; g < I.groups - 1; ++g) acc = acc * (uint64_t)inv % p;
+        pl.kinv = (uint32_t)acc;
+    }
+    pl.kinv_sh = shoup(pl.kinv, p);
     *out = pl;
     set_scalars(out, 1, 0);
     return 0;

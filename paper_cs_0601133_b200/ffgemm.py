@@ -31,7 +31,7 @@ _p, _ch, _sz = ctypes.c_void_p, ctypes.c_char, ctypes.c_size_t
 class ff_opts(ctypes.Structure):
     _fields_ = [("winograd", _i32), ("scheme", _i32), ("kb_override", _i64),
                 ("debug_saturate", _i32), ("cta_group", _i32), ("host_block", _i32),
-                ("reserved", _i32 * 5)]
+                ("korder", _i32), ("reserved", _i32 * 4)]
 
 
 class ff_plan_info(ctypes.Structure):
@@ -39,7 +39,7 @@ class ff_plan_info(ctypes.Structure):
                 ("limb_signed", _i32 * 4), ("digit_max", _i32 * 4), ("group_bound", _i64 * 7),
                 ("group_bound_max", _i64), ("kb_max", _i64), ("kb", _i64), ("k_pad", _i64),
                 ("num_kblocks", _i64), ("centre_max", _i32), ("reserved0", _i32),
-                ("carry_max", _i64), ("reserved", _i32 * 2)]
+                ("carry_max", _i64), ("korder", _i32), ("reserved", _i32 * 1)]
 
 
 _OPTS_P = ctypes.POINTER(ff_opts)
@@ -115,7 +115,7 @@ def ff_plan_query(p: int, k: int, opts=None) -> dict:
             "group_bound": list(info.group_bound[:G]), "group_bound_max": info.group_bound_max,
             "kb_max": info.kb_max, "kb": info.kb, "k_pad": info.k_pad,
             "num_kblocks": info.num_kblocks, "centre_max": info.centre_max,
-            "carry_max": info.carry_max}
+            "carry_max": info.carry_max, "korder": info.korder}
 
 
 def ff_gemm(p, transA, transB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc) -> None:

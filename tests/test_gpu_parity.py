@@ -167,17 +167,18 @@ def test_gemm_other_primes_and_noncanonical_inputs(env, p):
         _check(p, "N", "N", m, n, k, alpha, Abuf, Bbuf, beta, Cbuf, got)
 
 
+@pytest.mark.parametrize("korder", [1, 2])
 @pytest.mark.parametrize("cta_group", [1, 2])
 @pytest.mark.parametrize("p,scheme", [(65521, 2), (65521, 1), (8388593, 1), (67108859, 1),
-                                      (251, 1), (8388593, 2)])
-def test_kb_override_forces_mid_k_reductions(env, p, scheme, cta_group):
+                                      (251, 1), (8388593, 2), (3, 1), (65537, 1)])
+def test_kb_override_forces_mid_k_reductions(env, p, scheme, cta_group, korder):
     """Shrunk k-block ("overflow safety under shrunk gamma" analogue):
     several mid-k reductions per weight group must not change the result."""
     torch, ff = env
     rng = np.random.default_rng(11)
     m, n, k = 130, 260, 1000
     Abuf, Bbuf, Cbuf = _stored(rng, m, k, p), _stored(rng, k, n, p), _stored(rng, m, n, p)
-    opts = {"kb_override": 128, "scheme": scheme, "cta_group": cta_group}
+    opts = {"kb_override": 128, "scheme": scheme, "cta_group": cta_group, "korder": korder}
     assert ff.ff_plan_query(p, k, opts)["num_kblocks"] == 8
     got = _run_gpu(torch, ff, p, "N", "N", m, n, k, 5, Abuf, Bbuf, 7, Cbuf, opts)
     _check(p, "N", "N", m, n, k, 5, Abuf, Bbuf, 7, Cbuf, got)
@@ -204,7 +205,7 @@ def test_accumulator_at_the_bound_closed_form(env, p):
     """All entries = a digit-extreme residue v, k = the planner's largest k-block
     (and 2 k-blocks + a ragged tail): every entry must be k v^2 mod p."""
     torch, ff = env
-    info = ff.ff_plan_query(p, 1)
+    info = ff.ff_plan_query(p, 1, {"korder": 1})   # the safety k-block
     v = _adversarial_residue(p, info)
     if p == 65521:
         assert v == 33008
@@ -213,12 +214,13 @@ def test_accumulator_at_the_bound_closed_form(env, p):
         A = torch.full((m, k), v, dtype=torch.int32, device="cuda")
         B = torch.full((k, n), v, dtype=torch.int32, device="cuda")
         C = torch.empty((m, n), dtype=torch.int32, device="cuda")
-        for sat, grp in ((0, 1), (1, 1), (0, 2), (1, 2)):
+        for sat, grp, ko in ((0, 1, 1), (1, 1, 1), (0, 2, 1), (1, 2, 1), (0, 2, 2), (1, 1, 2)):
             C.fill_(-1)
+            kbo = info["kb"] if ko == 1 else 0      # k-outer: the locality k-block, several per k
             ff.ff_gemm_ex(p, "N", "N", m, n, k, 1, A, k, B, n, 0, C, n,
-                          {"debug_saturate": sat, "cta_group": grp})
+                          {"debug_saturate": sat, "cta_group": grp, "korder": ko, "kb_override": kbo})
             torch.cuda.synchronize()
-            assert (C == (k * v * v) % p).all().item(), (p, k, sat, grp)
+            assert (C == (k * v * v) % p).all().item(), (p, k, sat, grp, ko)
 
 
 def test_quick_returns_and_degenerate(env):
@@ -386,3 +388,50 @@ def test_row_panel_virtual_ranks_match_single_gpu(env, world, name):
     assert torch.equal(out, want)
     got = out.cpu().numpy()
     np.testing.assert_array_equal(got, oracle.fgemm(p, tA, tB, alpha, A, B, beta, C))
+
+
+# ---------------------------------------------------------------- one Winograd level (row a7)
+
+@pytest.mark.parametrize("p", CONFIG_PRIMES + [2, 3, 2 ** 31 - 1])
+@pytest.mark.parametrize("tA,tB", [("N", "N"), ("T", "N"), ("N", "T"), ("T", "T")])
+def test_winograd_level_vs_oracle(env, p, tA, tB):
+    """One Winograd level (Table 2, A22 fix) fused into the GEMM
+    epilogues: bit-exact against the oracle, and bit-identical to the classical
+    path ("level invariance")."""
+    torch, ff = env
+    rng = np.random.default_rng(p % 991 + ord(tA) + 2 * ord(tB))
+    for (m, n, k) in [(512, 512, 256), (768, 1024, 640), (1030, 514, 258)]:
+        Abuf = _stored(rng, *((m, k) if tA == "N" else (k, m)), p, 3)
+        Bbuf = _stored(rng, *((k, n) if tB == "N" else (n, k)), p, 1)
+        Cbuf = _stored(rng, m, n, p, 2)
+        for alpha, beta in [(1, 0), (p - 1, 1), (int(rng.integers(0, p)), int(rng.integers(0, p)))]:
+            got = _run_gpu(torch, ff, p, tA, tB, m, n, k, alpha, Abuf, Bbuf, beta, Cbuf, {"winograd": 1})
+            _check(p, tA, tB, m, n, k, alpha, Abuf, Bbuf, beta, Cbuf, got)
+            classic = _run_gpu(torch, ff, p, tA, tB, m, n, k, alpha, Abuf, Bbuf, beta, Cbuf, {"winograd": -1})
+            np.testing.assert_array_equal(got, classic)
+
+
+def test_winograd_rejects_odd_shapes(env):
+    torch, ff = env
+    A = torch.zeros((513, 256), dtype=torch.int32, device="cuda")
+    B = torch.zeros((256, 512), dtype=torch.int32, device="cuda")
+    C = torch.zeros((513, 512), dtype=torch.int32, device="cuda")
+    with pytest.raises(ff.FFError):
+        ff.fgemm(65521, A, B, C, opts={"winograd": 1})
+
+
+@pytest.mark.parametrize("name", ["c2", "c5"])
+def test_baseline_config_winograd_sampled_rows(env, name):
+    torch, ff = env
+    p, m, n, k, tA, tB, alpha, beta, seed = CONFIGS[name]
+    A, B, C = _make_config(torch, ff, name)
+    Cin = C.clone()
+    ff.fgemm(p, A, B, C, alpha, beta, tA, tB, opts={"winograd": 1})
+    ref = Cin.clone()
+    ff.fgemm(p, A, B, ref, alpha, beta, tA, tB, opts={"winograd": -1})
+    torch.cuda.synchronize()
+    assert torch.equal(C, ref)                 # level invariance at full size
+    out, Ah, Bh, Cinh = C.cpu().numpy(), A.cpu().numpy(), B.cpu().numpy(), Cin.cpu().numpy()
+    rows = [0, 1, m // 2 - 1, m // 2, m - 1]
+    want = oracle.fgemm_rows(p, tA, tB, alpha, Ah, Bh, beta, Cinh[rows], rows, m, n, k)
+    np.testing.assert_array_equal(out[rows], want)

@@ -127,18 +127,22 @@ def test_planner_matches_paper_bound(ff, p, L, scheme, D, kb_max):
     half = (p - 1) // 2
     # with an exactly centred carry the bound is SURVEY §8(a)'s kb_max ...
     assert kb_max == (2 ** 31 - 1 - half) // max(B)
-    # ... the kernel writes back a float-reciprocal residue (modp.cuh reduce_approx),
-    # |carry| <= (p-1)/2 + 385 w, w = 256 when a Horner x256 step exists (L >= 2)
-    carry = half + 385 * (256 if L >= 2 else 1)
+    # ... the kernel writes back an integer-Barrett estimate (modp.cuh reduce_mulhi)
+    # with |carry| <= 3p/2 for p < 2^29 (else a float-reciprocal one: (p-1)/2 + 385 w)
+    carry = (3 * p + 1) // 2 if p < 2 ** 29 and (L == 1 or p >= 512) else half + 385 * (256 if L >= 2 else 1)
     assert info["carry_max"] == carry
     kbm = info["kb_max"]
     assert kbm == (2 ** 31 - 1 - carry) // max(B)
     assert kbm * max(B) + carry <= 2 ** 31 - 1 < (kbm + 1) * max(B) + carry
-    assert kb_max - 4 <= kbm <= kb_max
+    assert 0.95 * kb_max <= kbm <= kb_max
     assert info["kb"] % 128 == 0 and info["kb"] <= kbm
-    # every config fits one k-block ("none of the 5 needs it")
+    # every config fits one safe k-block ("none of the 5 needs it") in
+    # group-outer order; the default k-outer order blocks k by 8192/L for L2 locality
     for k in (512, 4096, 8192, 16384):
-        assert ff.ff_plan_query(p, k)["num_kblocks"] == 1
+        assert ff.ff_plan_query(p, k, {"korder": 1})["num_kblocks"] == 1
+        d = ff.ff_plan_query(p, k)
+        loc = -(-(8192 // L) // 128) * 128
+        assert d["korder"] == 2 and d["kb"] == min(loc, info["kb"]) and d["num_kblocks"] == -(-k // d["kb"])
 
 
 @pytest.mark.parametrize("p", [2, 3, 5, 251, 257, 65279, 65521, 65537])
