@@ -80,7 +80,7 @@ typedef struct ff_opts {
                                (rounded up to 256); 0 = auto (~4096) */
     int32_t korder;         /* step order of the kernel: 0 auto, 1 group-outer (each weight
                                group over all of k), 2 k-outer (each k-block through all
-                               groups: L2 locality, DESIGN.md §4.6) */
+                               groups: L2 locality, DESIGN.md §4.7) */
     int32_t reserved[4];
 } ff_opts;
 

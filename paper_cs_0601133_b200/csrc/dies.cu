@@ -4,7 +4,7 @@
 // Why: a line touched by SMs of both dies ends up cached in both L2 halves,
 // so the usable L2 for operands shared by the whole GPU is ~half of 126 MB
 // (measured: DRAM traffic appears at a ~48-64 MiB shared working set;
-// DESIGN.md §4.7).  The GEMM therefore gives each die its own contiguous part
+// DESIGN.md §4.8).  The GEMM therefore gives each die its own contiguous part
 // of the tile raster, so each die's L2 holds only its own operands.
 //
 // How: one CTA per SM (forced by a large SMEM request) times dependent L2 hits
@@ -66,7 +66,7 @@ DieInfo g_die[64];
 void calibrate(int dev, DieInfo& D) {
     D.done = true;
     // Off unless requested: measured 4-6% slower than the plain raster on c4/c5
-    // (DESIGN.md §4.7), kept as an experiment.
+    // (DESIGN.md §4.8), kept as an experiment.
     if (!getenv("FF_DIE_AWARE") || getenv("FF_NO_DIE_AWARE")) return;
     const int nsm = num_sms();
     std::vector<int> h(512 * 64 * kGran);

@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // cluster registers on its die's counter, waits until every cluster of the
     // launch has registered (co-residency is guaranteed by the cooperative launch),
     // and the tile raster is split between the dies in proportion to their cluster
-    // counts, so each die's L2 holds only its own operands (DESIGN.md §4.7).
+    // counts, so each die's L2 holds only its own operands (DESIGN.md §4.8).
     if (threadIdx.x == 0 && leader) {
         const int nclusters = gridDim.x / kPair;
         int unit = blockIdx.x / kPair, nunits = nclusters, base = 0, count = a.num_tiles;

@@ -10,7 +10,7 @@
 //
 //      kb * B_w + (p-1)/2 <= 2^31 - 1,      B_w = sum_{i+j=w} D_i D_j,
 //
-// giving kb_max = floor((2^31 - 1 - (p-1)/2) / max_w B_w)  (
+// giving kb_max = floor((2^31 - 1 - carry_max) / max_w B_w)  (
 // the "one extra carried term" form matches the paper's own t_update values,
 // l.524-527, which satisfy (t+1)(p-1)^2 < 2^53 exactly).
 #include <cstdlib>
