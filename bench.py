@@ -224,9 +224,17 @@ def main():
     world = _env_int("WORLD_SIZE", 1)
     rank = _env_int("RANK", 0)
     local = _env_int("LOCAL_RANK", 0)
+    # FF_BENCH_SHARE_GPU=1 (testing only): every rank on cuda:0 over gloo, to run
+    # this multi-rank code path on a 1-GPU box; the real path is NCCL, one GPU per rank.
+    share = os.environ.get("FF_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import ffgen
     import paper_cs_0601133_b200 as ff
     from paper_cs_0601133_b200.sharded import Problem, RowPanelGemm
@@ -261,7 +269,10 @@ def main():
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            if share:
+                dist.barrier()
+            else:
+                dist.barrier(device_ids=[local])
 
     # ---- warm-up
     for _ in range(args.warmup):
@@ -408,7 +419,10 @@ def run_e2e(args, cfg, eng, A_panel, B, C_panel, world, rank, local, dev):
     for _ in range(max(1, min(args.warmup, 2))):
         one_step()
     if world > 1:
-        dist.barrier(device_ids=[local])
+        if os.environ.get("FF_BENCH_SHARE_GPU") == "1":
+            dist.barrier()
+        else:
+            dist.barrier(device_ids=[local])
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()

@@ -140,7 +140,6 @@ int make_plan(uint32_t p, int64_t k, const ff_opts* opts, Plan* out) {
     if (kb < kBK) return FF_ERR_INTERNAL;
     I.kb = kb;
     I.k_pad = (k + 15) / 16 * 16;
-    if (const char* e = getenv("FF_KPAD_EXTRA")) I.k_pad += (atoi(e) / 16) * 16;  // experiment only
     I.num_kblocks = k > 0 ? (k + kb - 1) / kb : 0;
 
     // Pairs (i,j) ordered by weight group, highest w first (Horner order).
