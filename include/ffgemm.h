@@ -58,17 +58,26 @@ extern "C" {
 #define FF_ERR_INTERNAL 5 /* planner could not represent p (should not happen for p < 2^31) */
 
 /* Limb schemes.  S: balanced signed digits in [-128,127];
- * T: two's-complement bytes (low limbs u8 in [0,255], top limb s8). */
+ * T: two's-complement bytes (low limbs u8 in [0,255], top limb s8).
+ * CRT: multi-modular (the paper's "Chinese remainder
+ * algorithm" for large fields): the centred residue c is
+ * replaced by its centred residues modulo pairwise-coprime q_i <= 256, one
+ * exact int8 product per modulus, and the exact integer dot product is
+ * reconstructed from them before the final reduction mod p.  AUTO uses it
+ * when it needs fewer int8 products than the limb schemes (large p). */
 #define FF_SCHEME_AUTO 0
 #define FF_SCHEME_S 1
 #define FF_SCHEME_T 2
+#define FF_SCHEME_CRT 3
+#define FF_MAX_MODULI 16
 
 /* Options for the _ex / split entry points.  Zero-initialise and set fields;
  * a NULL pointer means all defaults. */
 typedef struct ff_opts {
     int32_t winograd;       /* 0 auto, 1 one Winograd level (Table 2; needs even
                                m, n, k, else FF_ERR_OPTS), -1 never */
-    int32_t scheme;         /* FF_SCHEME_*; AUTO picks the fewest limbs, S on ties */
+    int32_t scheme;         /* FF_SCHEME_*; AUTO picks the fewest int8 products: limbs
+                               (S on ties) unless CRT needs clearly fewer */
     int64_t kb_override;    /* 0: planner k-block; else k-block length in elements,
                                rounded down to a multiple of 128; must not exceed the
                                safe bound (else FF_ERR_OPTS).  Forces mid-k reductions. */
@@ -87,12 +96,15 @@ typedef struct ff_opts {
 /* The plan the library derives from (p, k, opts): host-only, no GPU needed. */
 typedef struct ff_plan_info {
     uint32_t p;
-    int32_t L;               /* limbs per residue, 1..4 */
-    int32_t scheme;          /* FF_SCHEME_S or FF_SCHEME_T */
-    int32_t groups;          /* 2L-1 weight groups w = i+j */
-    int32_t limb_signed[4];  /* 1 if limb i is s8, 0 if u8 */
-    int32_t digit_max[4];    /* D_i = max |limb i| over all centred residues */
-    int64_t group_bound[7];  /* B_w = sum_{i+j=w} D_i D_j  (per unit of k) */
+    int32_t L;               /* int8 planes per operand: limbs (1..4) or, for
+                                FF_SCHEME_CRT, moduli (2..FF_MAX_MODULI) */
+    int32_t scheme;          /* FF_SCHEME_S, FF_SCHEME_T or FF_SCHEME_CRT */
+    int32_t groups;          /* accumulation groups: 2L-1 weight groups w = i+j
+                                (limbs) or L moduli (CRT) */
+    int32_t limb_signed[4];  /* 1 if limb i is s8, 0 if u8 (limb schemes) */
+    int32_t digit_max[4];    /* D_i = max |limb i| over all centred residues
+                                (limb schemes; CRT: max |residue| of plane i, i < 4) */
+    int64_t group_bound[7];  /* B_w = sum_{i+j=w} D_i D_j  (per unit of k; CRT: D_w^2) */
     int64_t group_bound_max; /* max_w B_w */
     int64_t kb_max;          /* floor((2^31-1-carry_max) / max_w B_w): Eq. (2) analogue */
     int64_t kb;              /* k-block actually used (multiple of 128, <= kb_max) */
@@ -102,8 +114,12 @@ typedef struct ff_plan_info {
     int32_t reserved0;
     int64_t carry_max;       /* bound on |value| written back into the accumulator
                                 between steps */
-    int32_t korder;          /* 1 group-outer, 2 k-outer */
-    int32_t reserved[1];
+    int32_t korder;          /* 1 group-outer, 2 k-outer (CRT: always 1) */
+    int32_t nmod;            /* FF_SCHEME_CRT: number of moduli (= L); else 0 */
+    uint32_t moduli[FF_MAX_MODULI]; /* CRT moduli q_0 > q_1 > ..., pairwise coprime,
+                                q_i <= 256, with prod q_i >= 4 k centre_max^2 */
+    int32_t log2_M_floor;    /* CRT: floor(log2(prod q_i)) */
+    int32_t log2_bound_ceil; /* CRT: ceil(log2(4 k centre_max^2)) (<= log2_M_floor) */
 } ff_plan_info;
 
 /* Library version (major*10000 + minor*100 + patch). Host only. */
@@ -155,7 +171,8 @@ int ff_gemm_host(uint32_t p, char transA, char transB, int64_t m, int64_t n, int
  * byte l*rows*k_pad + r*k_pad + kk), where L and k_pad come from
  * ff_plan_query(p, k, opts) and rows is the operand's row count in K-major
  * form (m for op(A), n for op(B)^T).  Size: L*rows*k_pad bytes, dev,
- * 16-byte aligned. */
+ * 16-byte aligned.  Under FF_SCHEME_CRT plane l holds the centred residues
+ * modulo moduli[l] (s8) instead of a limb. */
 
 /* Encode `rows` K-major rows of an operand into limb planes: row r, column
  * kk of the K-major view is X[r*ldx + kk] if kmajor_src = 1 (op(A) with
@@ -167,8 +184,10 @@ int ff_encode(uint32_t p, int64_t k, const ff_opts *opts, int kmajor_src, int64_
 
 /* C (m x n, ldc) <- (alpha * op(A) * op(B) + beta * C) mod p from limb planes
  * produced by ff_encode with the same (p, k, opts): A_limbs has m rows,
- * B_limbs has n rows.  Codes: -1 p, -2 m, -3 n, -4 k, -7 A_limbs, -8 B_limbs,
- * -10 C, -11 ldc. */
+ * B_limbs has n rows.  Under FF_SCHEME_CRT the kernel's per-CTA residue
+ * scratch comes from a library-owned per-device buffer (so concurrent calls
+ * on different streams of one device are not reentrant for CRT plans).
+ * Codes: -1 p, -2 m, -3 n, -4 k, -7 A_limbs, -8 B_limbs, -10 C, -11 ldc. */
 int ff_gemm_limbs(uint32_t p, int64_t m, int64_t n, int64_t k, const ff_opts *opts,
                   uint32_t alpha, const int8_t *A_limbs, const int8_t *B_limbs,
                   uint32_t beta, int32_t *C, int64_t ldc, void *stream);

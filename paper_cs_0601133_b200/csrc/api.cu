@@ -25,6 +25,7 @@ struct Buf {
 };
 Buf g_ws[kMaxDev];
 Buf g_host_a[kMaxDev], g_host_b[kMaxDev], g_host_c[kMaxDev], g_host_ws[kMaxDev];
+Buf g_scratch[kMaxDev];   // CRT residue scratch of ff_gemm_limbs
 std::mutex g_mu;
 
 // Library-owned streams for the pipelined host entry point.
@@ -116,7 +117,8 @@ bool winograd_auto_wins(const Plan& pl, int64_t m, int64_t n, int64_t k) {
 
 size_t ws_bytes(const Plan& pl, int64_t m, int64_t n) {
     const size_t L = static_cast<size_t>(pl.info.L), kp = static_cast<size_t>(pl.info.k_pad);
-    return align256(L * static_cast<size_t>(m) * kp) + align256(L * static_cast<size_t>(n) * kp);
+    return align256(L * static_cast<size_t>(m) * kp) + align256(L * static_cast<size_t>(n) * kp) +
+           align256(crt_scratch_bytes(pl));
 }
 
 int cuda_rc(cudaError_t e) { return e == cudaSuccess ? 0 : FF_ERR_CUDA; }
@@ -138,11 +140,12 @@ int run(const Plan& pl, char transA, char transB, int64_t m, int64_t n, int64_t 
     if (k == 0 || pl.mp.alpha == 0) return cuda_rc(launch_scale_c(pl.mp, m, n, C, ldc, st));
     int8_t* al = static_cast<int8_t*>(ws);
     int8_t* bl = al + align256(static_cast<size_t>(pl.info.L) * m * pl.info.k_pad);
+    int8_t* scratch = bl + align256(static_cast<size_t>(pl.info.L) * n * pl.info.k_pad);
     int e = cuda_rc(launch_encode(pl, is_n(transA) ? 1 : 0, m, k, A, lda, al, st));
     if (e) return e;
     e = cuda_rc(launch_encode(pl, is_t(transB) ? 1 : 0, n, k, B, ldb, bl, st));
     if (e) return e;
-    return launch_gemm_tc(pl, m, n, k, al, bl, C, ldc, st);
+    return launch_gemm_tc(pl, m, n, k, al, bl, C, ldc, scratch, st);
 }
 
 }  // namespace
@@ -315,11 +318,13 @@ int ff_gemm_host(uint32_t p, char transA, char transB, int64_t m, int64_t n, int
     const size_t a_panel = align256(L * mb * kp), b_chunk = align256(L * nb * kp);
     if ((e = ensure(g_host_a[dev], sizeof(int32_t) * (size_t)(ar * ac)))) return e;
     if ((e = ensure(g_host_b[dev], sizeof(int32_t) * (size_t)(br * bc)))) return e;
-    if ((e = ensure(g_host_ws[dev], a_panel * P + b_chunk * Q))) return e;
+    const size_t scr = align256(crt_scratch_bytes(pl));
+    if ((e = ensure(g_host_ws[dev], a_panel * P + b_chunk * Q + scr))) return e;
     int32_t* dA = static_cast<int32_t*>(g_host_a[dev].ptr);
     int32_t* dB = static_cast<int32_t*>(g_host_b[dev].ptr);
     int8_t* wsA = static_cast<int8_t*>(g_host_ws[dev].ptr);
     int8_t* wsB = wsA + a_panel * P;
+    int8_t* scratch = wsB + b_chunk * Q;    // GEMMs of the blocks run in order on hs.comp
     std::vector<cudaEvent_t> evs;
     auto mkev = [&]() {
         cudaEvent_t ev = nullptr;
@@ -400,7 +405,7 @@ int ff_gemm_host(uint32_t p, char transA, char transB, int64_t m, int64_t n, int
             encB[j] = 1;
         }
         if (beta_nz) chk(cudaStreamWaitEvent(hs.comp, evCin[i * Q + j], 0));
-        if (launch_gemm_tc(pl, r1 - r0, c1 - c0, k, Al, Bl, dC + r0 * n + c0, n, hs.comp)) fail = true;
+        if (launch_gemm_tc(pl, r1 - r0, c1 - c0, k, Al, Bl, dC + r0 * n + c0, n, scratch, hs.comp)) fail = true;
         chk(cudaEventRecord(evG[i * Q + j], hs.comp));
     }
     // ---- device -> host (stream hs.out): each C block as soon as its GEMM is done
@@ -456,7 +461,14 @@ int ff_gemm_limbs(uint32_t p, int64_t m, int64_t n, int64_t k, const ff_opts* op
     if (e) return e;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (k == 0 || pl.mp.alpha == 0) return cuda_rc(launch_scale_c(pl.mp, m, n, C, ldc, st));
-    return launch_gemm_tc(pl, m, n, k, A_limbs, B_limbs, C, ldc, st);
+    void* scratch = nullptr;
+    if (const size_t sb = crt_scratch_bytes(pl)) {
+        std::lock_guard<std::mutex> lk(g_mu);
+        const int dev = cur_dev();
+        if ((e = ensure(g_scratch[dev], sb))) return e;
+        scratch = g_scratch[dev].ptr;
+    }
+    return launch_gemm_tc(pl, m, n, k, A_limbs, B_limbs, C, ldc, scratch, st);
 }
 
 int ff_fill_uniform(int32_t* X, int64_t rows, int64_t cols, int64_t ld, uint32_t p, uint64_t seed,

@@ -126,6 +126,102 @@ __global__ void __launch_bounds__(256) encode_trans_kernel(ModP M, int64_t rows,
     }
 }
 
+// ---- multi-modular (CRT) planes: plane i holds the centred
+// residue of c (the centred residue of x mod p) modulo q_i, as s8.  The same
+// two access patterns as the limb encoders; the moduli are runtime constants.
+
+__device__ __forceinline__ uint32_t crt_digit(int32_t c, const CrtConsts& C, int i) {
+    const uint32_t r = residue_small(c, C.q[i], C.mu[i], C.off31[i]);
+    return static_cast<uint32_t>(centre_small(r, C.q[i], C.half[i])) & 0xFFu;
+}
+
+__global__ void __launch_bounds__(256) encode_crt_direct_kernel(ModP M, CrtConsts C, int64_t rows, int64_t k,
+                                                                int64_t k_pad, const int32_t* __restrict__ X,
+                                                                int64_t ldx, int8_t* __restrict__ planes,
+                                                                int vec_ok) {
+    const int64_t groups = k_pad / 4;
+    const int64_t plane = rows * k_pad;
+    for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
+        const int32_t* src = X + r * ldx;
+        uint32_t* dst = reinterpret_cast<uint32_t*>(planes + r * k_pad);
+        for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < groups;
+             g += (int64_t)gridDim.x * blockDim.x) {
+            const int64_t kk = 4 * g;
+            int32_t c[4];
+            if (vec_ok && kk + 4 <= k) {
+                const int4 v = __ldg(reinterpret_cast<const int4*>(src + kk));
+                c[0] = v.x; c[1] = v.y; c[2] = v.z; c[3] = v.w;
+            } else {
+#pragma unroll
+                for (int t = 0; t < 4; ++t) c[t] = (kk + t < k) ? __ldg(src + kk + t) : 0;
+            }
+#pragma unroll
+            for (int t = 0; t < 4; ++t) c[t] = centre(residue_i32(c[t], M), M);
+#pragma unroll
+            for (int i = 0; i < kMaxMod; ++i) {
+                if (i < C.nq) {
+                    uint32_t w = 0;
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) w |= crt_digit(c[t], C, i) << (8 * t);
+                    dst[g + i * (plane / 4)] = w;
+                }
+            }
+        }
+    }
+}
+
+// Transposed source: as encode_trans_kernel, the moduli in batches of 4 planes
+// through the SMEM byte tile (the centred values stay in registers).
+__global__ void __launch_bounds__(256) encode_crt_trans_kernel(ModP M, CrtConsts C, int64_t rows, int64_t k,
+                                                               int64_t k_pad, const int32_t* __restrict__ X,
+                                                               int64_t ldx, int8_t* __restrict__ planes) {
+    __shared__ __align__(16) uint8_t tile[4][kTR][kPitch];
+    const int64_t plane = rows * k_pad;
+    const int64_t tiles_r = (rows + kTR - 1) / kTR;
+    const int64_t tiles_k = (k_pad + kTK - 1) / kTK;
+    const int lr = threadIdx.x % kTR;
+    const int lk = threadIdx.x / kTR;
+    const int wr = (threadIdx.x / 32) * 4 + (threadIdx.x % 32) / 8;
+    const int wc = (threadIdx.x % 8) * 16;
+    for (int64_t t = blockIdx.x; t < tiles_r * tiles_k; t += gridDim.x) {
+        const int64_t r0 = (t % tiles_r) * kTR;
+        const int64_t kk0 = (t / tiles_r) * kTK;
+        int32_t cv[kTK / 8];
+        const bool rin = (r0 + lr) < rows;
+        const int32_t* col = X + (r0 + lr);
+#pragma unroll
+        for (int i = 0; i < kTK / 8; ++i) {
+            const int64_t kk = kk0 + lk + 8 * i;
+            cv[i] = (kk < k && rin) ? __ldg(col + kk * ldx) : 0;
+        }
+#pragma unroll
+        for (int i = 0; i < kTK / 8; ++i) cv[i] = centre(residue_i32(cv[i], M), M);
+        const int64_t r = r0 + wr;
+        const int64_t kc = kk0 + wc;
+        for (int b0 = 0; b0 < C.nq; b0 += 4) {
+            __syncthreads();
+#pragma unroll
+            for (int i = 0; i < kTK / 8; ++i) {
+                const int kl = lk + 8 * i;
+#pragma unroll
+                for (int l = 0; l < 4; ++l)
+                    if (b0 + l < C.nq) tile[l][lr][kl] = static_cast<uint8_t>(crt_digit(cv[i], C, b0 + l));
+            }
+            __syncthreads();
+            if (r < rows && kc < k_pad) {
+                int8_t* dst = planes + r * k_pad + kc;
+#pragma unroll
+                for (int l = 0; l < 4; ++l) {
+                    if (b0 + l < C.nq) {
+                        const uint32_t* src = reinterpret_cast<const uint32_t*>(&tile[l][wr][wc]);
+                        *reinterpret_cast<uint4*>(dst + (b0 + l) * plane) = make_uint4(src[0], src[1], src[2], src[3]);
+                    }
+                }
+            }
+        }
+    }
+}
+
 // C <- beta * C mod p (k = 0 or alpha = 0); C <- 0 when beta = 0 (C not read).
 __global__ void scale_c_kernel(ModP M, int64_t m, int64_t n, int32_t* __restrict__ C, int64_t ldc) {
     const int64_t total = m * n;
@@ -173,6 +269,26 @@ cudaError_t launch_encode(const Plan& pl, int kmajor_src, int64_t rows, int64_t 
                           int8_t* limbs, cudaStream_t st) {
     const int64_t k_pad = pl.info.k_pad;
     if (rows == 0 || k_pad == 0) return cudaSuccess;
+    if (pl.crt) {
+        if (kmajor_src) {
+            const int64_t groups = k_pad / 4;
+            int gx = static_cast<int>((groups + 255) / 256);
+            if (gx > 64) gx = 64;
+            int64_t gy = (int64_t)num_sms() * 8 / gx;
+            if (gy > rows) gy = rows;
+            if (gy > 65535) gy = 65535;
+            if (gy < 1) gy = 1;
+            const int vec_ok = ((ldx % 4) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0) ? 1 : 0;
+            encode_crt_direct_kernel<<<dim3(gx, static_cast<unsigned>(gy)), 256, 0, st>>>(
+                pl.mp, pl.cc, rows, k, k_pad, X, ldx, limbs, vec_ok);
+        } else {
+            const int64_t tiles = ((rows + kTR - 1) / kTR) * ((k_pad + kTK - 1) / kTK);
+            const int64_t cap = (int64_t)num_sms() * 8;
+            encode_crt_trans_kernel<<<static_cast<int>(tiles < cap ? tiles : cap), 256, 0, st>>>(
+                pl.mp, pl.cc, rows, k, k_pad, X, ldx, limbs);
+        }
+        return cudaGetLastError();
+    }
     const bool S = pl.info.scheme == FF_SCHEME_S;
     switch (pl.info.L) {
         case 1: S ? launch_encode_t<1, FF_SCHEME_S>(pl, kmajor_src, rows, k, k_pad, X, ldx, limbs, st)

@@ -76,9 +76,9 @@ struct GemmArgs {
     int32_t kb_iters;  // k-block length / 128
     int32_t nkb;       // number of k-blocks
     int32_t G;         // weight groups
-    int8_t pair_i[16], pair_j[16];
-    int8_t group_first[8], group_len[8];
-    uint32_t idesc[16];
+    int8_t pair_i[kMaxPairs], pair_j[kMaxPairs];
+    int8_t group_first[kMaxGroups], group_len[kMaxGroups];
+    uint32_t idesc[kMaxPairs];
     int32_t raster;     // tile-rows per raster band
     int32_t hints;      // bit0: TMA loads evict_last; bit1: C stores evict_first
     int32_t last_use;   // 1 if no later launch reads these outputs (streaming stores allowed)
@@ -88,7 +88,19 @@ struct GemmArgs {
     uint32_t kinv, kinv_sh;     // k-outer: 256^-(G-1) mod p
     const uint8_t* die_map;     // die-aware schedule (dies.cu): die of each %smid, or null
     int* sched;                 // per-launch counters: [0],[1] clusters per die, [2] arrivals
+    int32_t crt;                // 1: groups are CRT moduli
+    CrtConsts cc;
+    uint8_t* scratch;           // CRT: per CTA and slot, G-1 byte planes of kCrtPlane bytes
 };
+
+// CRT residue scratch: one 128 x 256 byte plane per (CTA, slot, modulus 1..G-1),
+// laid out [h: 64-column quarter][c: 16-column chunk][row 0..127][16 bytes] so
+// that a warp's 32 rows store / load 512 contiguous bytes per instruction.
+constexpr int kCrtPlane = 128 * kTileN;
+
+__device__ __forceinline__ uint8_t* crt_plane(const GemmArgs& a, int slot, int g) {
+    return a.scratch + (static_cast<size_t>(blockIdx.x * 2 + slot) * (a.G - 1) + (g - 1)) * kCrtPlane;
+}
 
 __device__ __forceinline__ unsigned long long clk() {
     unsigned long long c;
@@ -257,7 +269,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 acc_par[slot] ^= 1;
                 ptx::tc_fence_after();
                 const uint32_t d = tmem_base + slot * kTileN;
-                uint32_t acc = (g == a.G - 1 && kb == 0) ? 0u : 1u;  // first MMA of a tile overwrites
+                // The first MMA of a tile (limbs: Horner continues in the accumulator)
+                // or of each modulus (CRT: independent products) overwrites.
+                uint32_t acc = (a.crt ? kb == 0 : (g == a.G - 1 && kb == 0)) ? 0u : 1u;
                 const int ks0 = kb * a.kb_iters;
                 const int ks1 = min(ks0 + a.kb_iters, a.k_iters);
                 for (int pi = a.group_first[g]; pi < a.group_first[g] + a.group_len[g]; ++pi) {
@@ -317,7 +331,41 @@ __global__ void __launch_bounds__(kThreads, 1)
             const bool horner = (a.korder == 2) ? (g > 0) : last_kb;
             const bool rescale = (a.korder == 2) && g == 0 && !last_kb;
             const uint32_t tcol = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + slot * kTileN + h * 64;
-            if (rescale) {
+            const int crow = q * 32 + static_cast<int>(lane);   // row of this thread within the CTA tile
+            if (a.crt && !final_step) {
+                // CRT: between k-blocks keep the centred residue
+                // mod q_g; after the last one store u_g = (S_g mod q_g) v_g mod q_g
+                // to this CTA's scratch (read back by the final step of the tile).
+                uint32_t v[64];
+                ptx::tmem_ld64(tcol, v);
+                ptx::tmem_wait_ld();
+                const uint32_t qg = a.cc.q[g], mu = a.cc.mu[g], off = a.cc.off31[g];
+                if (!last_kb) {
+                    const uint32_t hf = a.cc.half[g];
+#pragma unroll
+                    for (int t = 0; t < 64; ++t)
+                        v[t] = static_cast<uint32_t>(centre_small(residue_small(static_cast<int32_t>(v[t]), qg, mu, off), qg, hf));
+                    ptx::tmem_st64(tcol, v);
+                    ptx::tmem_wait_st();
+                } else {
+                    const uint32_t vg = a.cc.v[g];
+                    uint8_t* dst = crt_plane(a, slot, g) + (h * 4 * 128 + crow) * 16;
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        uint32_t w[4];
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            w[j] = 0;
+#pragma unroll
+                            for (int b = 0; b < 4; ++b) {
+                                const uint32_t r = residue_small(static_cast<int32_t>(v[c * 16 + j * 4 + b]), qg, mu, off);
+                                w[j] |= mulmod_small(r, vg, qg, mu) << (8 * b);
+                            }
+                        }
+                        *reinterpret_cast<uint4*>(dst + c * 128 * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+                    }
+                }
+            } else if (rescale) {
                 uint32_t v[64];
                 ptx::tmem_ld64(tcol, v);
                 ptx::tmem_wait_ld();
@@ -358,8 +406,45 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::tmem_wait_ld();
                     if (row >= a.m) continue;
                     const int col0 = tn * K::BN + h * 64 + half * 32;
+                    if (a.crt) {
+                        // X = sum_i u_i M_i - t M exactly, t = round(sum_i u_i / q_i)
+                        // (|X| <= M/4); X mod p = sum_i u_i (M_i mod p) + t (p - M mod p).
+                        const uint32_t q0 = a.cc.q[0], mu0 = a.cc.mu[0], off0 = a.cc.off31[0], v0 = a.cc.v[0];
 #pragma unroll
-                    for (int t = 0; t < 32; ++t) v[t] = residue_i32(static_cast<int32_t>(v[t]), M);  // exact R
+                        for (int cc = 0; cc < 4; ++cc) {      // 8 columns at a time (register budget)
+                            unsigned long long S[8];
+                            uint32_t F[8];
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) {
+                                const uint32_t u = mulmod_small(
+                                    residue_small(static_cast<int32_t>(v[cc * 8 + j]), q0, mu0, off0), v0, q0, mu0);
+                                S[j] = static_cast<unsigned long long>(u) * a.cc.W[0];
+                                F[j] = u * a.cc.R[0];
+                            }
+                            const uint8_t* src = crt_plane(a, slot, 1) +
+                                                 ((h * 4 + half * 2 + (cc >> 1)) * 128 + crow) * 16 + (cc & 1) * 8;
+#pragma unroll 1
+                            for (int g2 = 1; g2 < a.G; ++g2) {
+                                const uint2 x = *reinterpret_cast<const uint2*>(src + static_cast<size_t>(g2 - 1) * kCrtPlane);
+                                const uint32_t W = a.cc.W[g2], R = a.cc.R[g2];
+#pragma unroll
+                                for (int j = 0; j < 8; ++j) {
+                                    const uint32_t u = ((j < 4 ? x.x : x.y) >> (8 * (j & 3))) & 0xFFu;
+                                    S[j] += static_cast<unsigned long long>(u) * W;
+                                    F[j] += u * R;
+                                }
+                            }
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) {
+                                const uint32_t t = (F[j] + (1u << 23)) >> 24;
+                                v[cc * 8 + j] = residue_u64(S[j] + static_cast<unsigned long long>(t) * a.cc.Mneg,
+                                                            a.cc.mu64, M.p);
+                            }
+                        }
+                    } else {
+#pragma unroll
+                        for (int t = 0; t < 32; ++t) v[t] = residue_i32(static_cast<int32_t>(v[t]), M);  // exact R
+                    }
 #pragma unroll 1
                     for (int qo = 0; qo < a.nout; ++qo) {
                         const GemmOut O = a.out[qo];
@@ -479,7 +564,7 @@ uint32_t shoup_host(uint32_t w, uint32_t p) { return static_cast<uint32_t>((stat
 
 template <int kPair>
 int launch_impl(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A_limbs, const int8_t* B_limbs,
-                const OutSpec* outs, int nout, int64_t ldc, int last_use, cudaStream_t st) {
+                const OutSpec* outs, int nout, int64_t ldc, int last_use, void* scratch, cudaStream_t st) {
     using K = Cfg<kPair>;
     const ff_plan_info& I = pl.info;
     if (m > INT32_MAX - K::BM || n > INT32_MAX - K::BN) return -2;
@@ -513,13 +598,18 @@ int launch_impl(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A
     for (int pi = 0; pi < pl.npairs; ++pi) {
         a.pair_i[pi] = static_cast<int8_t>(pl.pair_i[pi]);
         a.pair_j[pi] = static_cast<int8_t>(pl.pair_j[pi]);
-        a.idesc[pi] = make_idesc(I.limb_signed[pl.pair_i[pi]] != 0, I.limb_signed[pl.pair_j[pi]] != 0,
-                                 pl.saturate, K::BM, K::BN);
+        const bool sa = pl.crt || I.limb_signed[pl.pair_i[pi]] != 0;   // CRT residues are s8
+        const bool sb = pl.crt || I.limb_signed[pl.pair_j[pi]] != 0;
+        a.idesc[pi] = make_idesc(sa, sb, pl.saturate, K::BM, K::BN);
     }
     for (int w = 0; w < I.groups; ++w) {
         a.group_first[w] = static_cast<int8_t>(pl.group_first[w]);
         a.group_len[w] = static_cast<int8_t>(pl.group_len[w]);
     }
+    a.crt = pl.crt ? 1 : 0;
+    a.cc = pl.cc;
+    a.scratch = static_cast<uint8_t*>(scratch);
+    if (pl.crt && pl.cc.nq > 1 && !scratch) return FF_ERR_INTERNAL;
     a.trace = nullptr;
     static unsigned long long* trace_buf = nullptr;
     const bool tracing = getenv("FF_TRACE") != nullptr;
@@ -607,21 +697,27 @@ int launch_impl(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A
 
 }  // namespace
 
+size_t crt_scratch_bytes(const Plan& pl) {
+    if (!pl.crt || pl.cc.nq <= 1) return 0;
+    // grid <= num_sms() CTAs (both kernels), 2 TMEM slots each
+    return static_cast<size_t>(num_sms()) * 2 * static_cast<size_t>(pl.cc.nq - 1) * kCrtPlane;
+}
+
 int launch_gemm_tc_multi(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A_limbs,
                          const int8_t* B_limbs, const OutSpec* outs, int nout, int64_t ldc, int last_use,
-                         cudaStream_t st) {
+                         void* scratch, cudaStream_t st) {
     // The CTA-pair kernel unless the problem has too few 256 x 256 tiles to
     // occupy the GPU (then the 128 x 256 single-CTA kernel gives more CTAs).
     const int64_t pair_tiles = ((m + 255) / 256) * ((n + 255) / 256);
     if (pl.force_pair == 1 || (pl.force_pair == 0 && pair_tiles * 2 < num_sms()))
-        return launch_impl<1>(pl, m, n, k, A_limbs, B_limbs, outs, nout, ldc, last_use, st);
-    return launch_impl<2>(pl, m, n, k, A_limbs, B_limbs, outs, nout, ldc, last_use, st);
+        return launch_impl<1>(pl, m, n, k, A_limbs, B_limbs, outs, nout, ldc, last_use, scratch, st);
+    return launch_impl<2>(pl, m, n, k, A_limbs, B_limbs, outs, nout, ldc, last_use, scratch, st);
 }
 
 int launch_gemm_tc(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A_limbs, const int8_t* B_limbs,
-                   int32_t* C, int64_t ldc, cudaStream_t st) {
+                   int32_t* C, int64_t ldc, void* scratch, cudaStream_t st) {
     const OutSpec o = {C, pl.mp.alpha, pl.mp.beta};
-    return launch_gemm_tc_multi(pl, m, n, k, A_limbs, B_limbs, &o, 1, ldc, 1, st);
+    return launch_gemm_tc_multi(pl, m, n, k, A_limbs, B_limbs, &o, 1, ldc, 1, scratch, st);
 }
 
 }  // namespace ff

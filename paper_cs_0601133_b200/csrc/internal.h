@@ -9,7 +9,9 @@
 namespace ff {
 
 constexpr int kMaxLimbs = 4;
-constexpr int kMaxGroups = 2 * kMaxLimbs - 1;
+constexpr int kMaxMod = FF_MAX_MODULI;       // CRT moduli
+constexpr int kMaxGroups = kMaxMod;          // >= 2 kMaxLimbs - 1 weight groups
+constexpr int kMaxPairs = 16;                // >= kMaxLimbs^2 limb pairs, >= kMaxMod moduli
 constexpr int kBK = 128;        // bytes (= int8 elements) of K per pipeline stage (one 128B swizzle row)
 constexpr int kMmaK = 32;       // K per tcgen05.mma.kind::i8 instruction
 constexpr int kTileM = 128;     // rows of op(A) per CTA tile (= TMEM lanes)
@@ -32,12 +34,29 @@ struct ModP {
     int32_t int_wb;       // 1: integer write-back (p < 2^29), 0: fp32-reciprocal write-back
 };
 
+// Multi-modular (CRT) constants.  M = prod q_i, M_i = M / q_i.
+// Small-modulus residues use the same Barrett form as residue_i32 (modp.cuh).
+struct CrtConsts {
+    int32_t nq;
+    uint32_t q[kMaxMod];       // moduli, pairwise coprime, <= 256
+    uint32_t mu[kMaxMod];      // floor(2^32 / q)
+    uint32_t off31[kMaxMod];   // 2^31 mod q
+    uint32_t half[kMaxMod];    // (q-1)/2: residues r > half are centred to r - q
+    uint32_t v[kMaxMod];       // (M_i mod q_i)^-1 mod q_i
+    uint32_t W[kMaxMod];       // M_i mod p
+    uint32_t R[kMaxMod];       // round(2^24 / q_i): fixed-point 1/q_i for the quotient t
+    uint32_t Mneg;             // (p - M mod p) mod p
+    unsigned long long mu64;   // floor(2^64 / p) (Barrett for the 64-bit sum)
+};
+
 struct Plan {
     ff_plan_info info;
     ModP mp;
-    int npairs;                      // L*L
-    int pair_i[kMaxLimbs * kMaxLimbs];
-    int pair_j[kMaxLimbs * kMaxLimbs];
+    bool crt;                        // FF_SCHEME_CRT: groups are moduli, one pair (i, i) each
+    CrtConsts cc;
+    int npairs;                      // L*L (limbs) or L (CRT)
+    int pair_i[kMaxPairs];
+    int pair_j[kMaxPairs];
     int group_first[kMaxGroups];     // pairs of group w are [group_first[w], group_first[w]+group_len[w])
     int group_len[kMaxGroups];
     bool saturate;
@@ -55,6 +74,9 @@ void set_scalars(Plan* pl, uint32_t alpha, uint32_t beta);
 // encode.cu
 cudaError_t launch_encode(const Plan& pl, int kmajor_src, int64_t rows, int64_t k,
                           const int32_t* X, int64_t ldx, int8_t* limbs, cudaStream_t st);
+// CRT scratch of the GEMM kernel: per CTA and TMEM slot, the (nq-1) byte planes
+// of u_i = r_i v_i mod q_i for a 128 x 256 tile (0 for limb plans).
+size_t crt_scratch_bytes(const Plan& pl);
 cudaError_t launch_scale_c(const ModP& mp, int64_t m, int64_t n, int32_t* C, int64_t ldc,
                            cudaStream_t st);
 
@@ -63,11 +85,12 @@ struct OutSpec {          // C <- (a * A B + b * C) mod p for one output block
     int32_t* C;
     uint32_t a, b;
 };
+// `scratch`: crt_scratch_bytes(pl) bytes of device memory (ignored for limb plans).
 int launch_gemm_tc_multi(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A_limbs,
                          const int8_t* B_limbs, const OutSpec* outs, int nout, int64_t ldc, int last_use,
-                         cudaStream_t st);
+                         void* scratch, cudaStream_t st);
 int launch_gemm_tc(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A_limbs,
-                   const int8_t* B_limbs, int32_t* C, int64_t ldc, cudaStream_t st);
+                   const int8_t* B_limbs, int32_t* C, int64_t ldc, void* scratch, cudaStream_t st);
 
 // winograd.cu
 size_t winograd_ws_bytes(const Plan& half, int64_t m, int64_t n, int64_t k);

@@ -61,6 +61,37 @@ __device__ __forceinline__ int32_t reduce_mulhi(int32_t a, uint32_t w, int32_t m
     return static_cast<int32_t>(static_cast<uint32_t>(a) * w - static_cast<uint32_t>(q) * p);
 }
 
+// ---- small moduli q <= 256 of the multi-modular scheme
+
+// Any int32 -> its residue in [0, q), the same Barrett form as residue_i32
+// (mu = floor(2^32/q), off31 = 2^31 mod q).
+__device__ __forceinline__ uint32_t residue_small(int32_t a, uint32_t q, uint32_t mu, uint32_t off31) {
+    const uint32_t x = static_cast<uint32_t>(a) ^ 0x80000000u;
+    uint32_t r = x - __umulhi(x, mu) * q;
+    if (r >= q) r -= q;
+    return r >= off31 ? r - off31 : r + (q - off31);
+}
+
+// r in [0, q) -> centred representative: r - q if r > (q-1)/2 (q = 256: [-128, 127]).
+__device__ __forceinline__ int32_t centre_small(uint32_t r, uint32_t q, uint32_t half) {
+    return r > half ? static_cast<int32_t>(r) - static_cast<int32_t>(q) : static_cast<int32_t>(r);
+}
+
+// (r v) mod q for r, v in [0, q): r v < 2^16, one Barrett step + one correction.
+__device__ __forceinline__ uint32_t mulmod_small(uint32_t r, uint32_t v, uint32_t q, uint32_t mu) {
+    const uint32_t y = r * v;
+    uint32_t u = y - __umulhi(y, mu) * q;
+    return u >= q ? u - q : u;
+}
+
+// x mod p for x < 2^64 (Barrett with mu64 = floor(2^64/p): the quotient
+// estimate is floor(x/p) or one less, so one correction).
+__device__ __forceinline__ uint32_t residue_u64(unsigned long long x, unsigned long long mu64, uint32_t p) {
+    const unsigned long long q = __umul64hi(x, mu64);
+    unsigned long long r = x - q * p;
+    return static_cast<uint32_t>(r >= p ? r - p : r);
+}
+
 __device__ __forceinline__ uint32_t addmod(uint32_t a, uint32_t b, uint32_t p) {
     const uint32_t s = a + b;  // < 2p < 2^32
     return s >= p ? s - p : s;

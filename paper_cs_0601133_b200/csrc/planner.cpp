@@ -56,34 +56,132 @@ uint32_t shoup(uint32_t w, uint32_t p) {
     return (uint32_t)(((uint64_t)w << 32) / p);
 }
 
-}  // namespace
+typedef unsigned __int128 u128;
 
-int make_plan(uint32_t p, int64_t k, const ff_opts* opts, Plan* out) {
-    if (p < 2 || p >= (1u << 31)) return -1;
-    if (k < 0) return -6;
-    ff_opts o;
-    std::memset(&o, 0, sizeof(o));
-    if (opts) o = *opts;
-    if (o.scheme < FF_SCHEME_AUTO || o.scheme > FF_SCHEME_T) return FF_ERR_OPTS;
-    if (o.winograd < -1 || o.winograd > 1) return FF_ERR_OPTS;
-    if (o.kb_override < 0) return FF_ERR_OPTS;
-    if (o.cta_group < 0 || o.cta_group > 2) return FF_ERR_OPTS;
-    if (o.korder < 0 || o.korder > 2) return FF_ERR_OPTS;
+uint32_t gcd32(uint32_t a, uint32_t b) {
+    while (b) { const uint32_t t = a % b; a = b; b = t; }
+    return a;
+}
 
-    Plan pl;
-    std::memset(&pl, 0, sizeof(pl));
+// x^-1 mod q for gcd(x, q) = 1 (extended Euclid).
+uint32_t inv_mod(uint32_t x, uint32_t q) {
+    int64_t r0 = q, r1 = x % q, s0 = 0, s1 = 1;
+    while (r1 != 0) {
+        const int64_t qq = r0 / r1, t = r0 - qq * r1, u = s0 - qq * s1;
+        r0 = r1; r1 = t; s0 = s1; s1 = u;
+    }
+    return (uint32_t)(((s0 % (int64_t)q) + q) % q);
+}
+
+int ceil_log2_u128(u128 x) {   // smallest e with 2^e >= x (x >= 1)
+    int e = 0;
+    while (((u128)1 << e) < x) ++e;
+    return e;
+}
+
+int floor_log2_u128(u128 x) {  // largest e with 2^e <= x (x >= 1)
+    int e = 0;
+    while (e < 127 && ((u128)1 << (e + 1)) <= x) ++e;
+    return e;
+}
+
+// Multi-modular moduli.  The exact integer dot product X of
+// two centred residue vectors of length k satisfies |X| <= k cmax^2; it is
+// recovered from its residues modulo pairwise-coprime q_i <= 256 when
+// M = prod q_i >= 4 k cmax^2 (so |X| / M <= 1/4: the CRT quotient is then the
+// nearest integer to sum_i u_i / q_i with a 1/4 margin for its fixed-point
+// evaluation).  Greedy from 256 down: the fewest moduli (each one int8 GEMM).
+// Returns the count (0 if more than kMaxMod would be needed).
+int crt_select(int64_t cmax, int64_t k, uint32_t* q, u128* Mout, u128* Bout) {
+    const u128 kk = (u128)(k > 0 ? k : 1);
+    const u128 B = (u128)4 * kk * (u128)cmax * (u128)cmax;
+    u128 M = 1;
+    int n = 0;
+    for (uint32_t c = 256; c >= 2 && M < B; --c) {
+        bool ok = true;
+        for (int i = 0; i < n && ok; ++i) ok = gcd32(c, q[i]) == 1;
+        if (!ok) continue;
+        if (n == kMaxMod) return 0;
+        q[n++] = c;
+        M *= c;
+    }
+    if (M < B) return 0;
+    if (n == 0) { q[n++] = 256; M = 256; }
+    *Mout = M;
+    *Bout = B;
+    return n;
+}
+
+// Fill the CRT part of a plan (one group = one modulus = one pair (i, i)).
+int make_crt_plan(uint32_t p, int64_t k, const ff_opts& o, int64_t cmax, Plan& pl) {
     ff_plan_info& I = pl.info;
-    // Centred residues lie in [-neg, half]: neg = half for odd p, half + 1 for p = 2.
-    const int64_t half = (int64_t)(p - 1) / 2;
-    const int64_t neg = (int64_t)(p - 1) - half;
-    const int64_t cmax = neg > half ? neg : half;
-    I.p = p;
-    I.centre_max = (int32_t)cmax;
+    uint32_t q[kMaxMod];
+    u128 M = 0, B = 0;
+    const int nq = crt_select(cmax, k, q, &M, &B);
+    if (nq == 0) return FF_ERR_OPTS;
+    pl.crt = true;
+    I.scheme = FF_SCHEME_CRT;
+    I.L = nq;
+    I.groups = nq;
+    I.nmod = nq;
+    I.log2_M_floor = floor_log2_u128(M);
+    I.log2_bound_ceil = ceil_log2_u128(B);
+    int64_t bmax = 0;
+    for (int i = 0; i < nq; ++i) {
+        I.moduli[i] = q[i];
+        const int64_t D = q[i] / 2;            // |centred residue| <= q/2 (q = 256: [-128, 127])
+        if (i < 4) { I.digit_max[i] = (int32_t)D; I.limb_signed[i] = 1; }
+        if (i < 7) I.group_bound[i] = D * D;
+        if (D * D > bmax) bmax = D * D;
+    }
+    I.group_bound_max = bmax;
+    // The carry written back between k-blocks is a centred residue mod q_i.
+    I.carry_max = q[0] / 2;
+    I.kb_max = (((int64_t)1 << 31) - 1 - I.carry_max) / bmax;
+    pl.korder = 1;
+    I.korder = 1;
+    int64_t kb = I.kb_max;
+    if (o.kb_override > 0) {
+        if (o.kb_override > I.kb_max || o.kb_override < kBK) return FF_ERR_OPTS;
+        kb = o.kb_override;
+    }
+    kb = (kb / kBK) * kBK;
+    I.kb = kb;
+    I.k_pad = (k + 15) / 16 * 16;
+    I.num_kblocks = k > 0 ? (k + kb - 1) / kb : 0;
+    // Groups are processed from index G-1 down to 0 (as the limb groups): the
+    // last one (modulus 0) is the final step that reconstructs.
+    for (int i = 0; i < nq; ++i) {
+        pl.group_first[i] = i;
+        pl.group_len[i] = 1;
+        pl.pair_i[i] = i;
+        pl.pair_j[i] = i;
+    }
+    pl.npairs = nq;
+    CrtConsts& C = pl.cc;
+    C.nq = nq;
+    const u128 Mp = M % p;
+    C.Mneg = (uint32_t)((p - (uint32_t)Mp) % p);
+    C.mu64 = (unsigned long long)((((u128)1) << 64) / p);
+    for (int i = 0; i < nq; ++i) {
+        const uint32_t qi = q[i];
+        const u128 Mi = M / qi;
+        C.q[i] = qi;
+        C.mu[i] = (uint32_t)((((uint64_t)1) << 32) / qi);
+        C.off31[i] = (uint32_t)((((uint64_t)1) << 31) % qi);
+        C.half[i] = (qi - 1) / 2;
+        C.v[i] = inv_mod((uint32_t)(Mi % qi), qi);
+        C.W[i] = (uint32_t)(Mi % p);
+        C.R[i] = (uint32_t)(((((uint64_t)1) << 25) / qi + 1) / 2);   // round(2^24 / q)
+    }
+    return 0;
+}
 
-    const int LS = min_limbs(half, neg, FF_SCHEME_S), LT = min_limbs(half, neg, FF_SCHEME_T);
-    int scheme = o.scheme;
-    if (scheme == FF_SCHEME_AUTO) scheme = (LS != 0 && (LT == 0 || LS <= LT)) ? FF_SCHEME_S : FF_SCHEME_T;
-    const int L = scheme == FF_SCHEME_S ? LS : LT;
+// Limb schemes S / T: digit bounds, group bounds, the
+// Eq. (2) k-block and the (i, j) pairs of each weight group.
+int make_limb_plan(uint32_t p, int64_t k, const ff_opts& o, int64_t half, int64_t neg, int64_t cmax, int scheme,
+                   int L, Plan& pl, bool& int_wb) {
+    ff_plan_info& I = pl.info;
     if (L == 0) return FF_ERR_INTERNAL;
     I.L = L;
     I.scheme = scheme;
@@ -117,7 +215,7 @@ int make_plan(uint32_t p, int64_t k, const ff_opts* opts, Plan* out) {
     // with w = 256 for the Horner scaling (L >= 2) and w = 1 otherwise.
     // (m = round(w 2^32/p) must fit in int32 for every w used: p >= 512 when the
     // Horner factor w = 256 occurs, i.e. L >= 2.)
-    const bool int_wb = p < (1u << 29) && (L == 1 || p >= 512);
+    int_wb = p < (1u << 29) && (L == 1 || p >= 512);
     const int64_t carry = int_wb ? (3 * (int64_t)p + 1) / 2 : cmax + (L >= 2 ? 385 * 256 : 385);
     I.carry_max = carry;
     I.kb_max = bmax > 0 ? (((int64_t)1 << 31) - 1 - carry) / bmax : ((int64_t)1 << 40);
@@ -157,6 +255,57 @@ int make_plan(uint32_t p, int64_t k, const ff_opts* opts, Plan* out) {
         pl.group_len[w] = np - pl.group_first[w];
     }
     pl.npairs = np;
+    return 0;
+}
+
+}  // namespace
+
+int make_plan(uint32_t p, int64_t k, const ff_opts* opts, Plan* out) {
+    if (p < 2 || p >= (1u << 31)) return -1;
+    if (k < 0) return -6;
+    ff_opts o;
+    std::memset(&o, 0, sizeof(o));
+    if (opts) o = *opts;
+    if (o.scheme < FF_SCHEME_AUTO || o.scheme > FF_SCHEME_CRT) return FF_ERR_OPTS;
+    if (o.winograd < -1 || o.winograd > 1) return FF_ERR_OPTS;
+    if (o.kb_override < 0) return FF_ERR_OPTS;
+    if (o.cta_group < 0 || o.cta_group > 2) return FF_ERR_OPTS;
+    if (o.korder < 0 || o.korder > 2) return FF_ERR_OPTS;
+
+    Plan pl;
+    std::memset(&pl, 0, sizeof(pl));
+    ff_plan_info& I = pl.info;
+    // Centred residues lie in [-neg, half]: neg = half for odd p, half + 1 for p = 2.
+    const int64_t half = (int64_t)(p - 1) / 2;
+    const int64_t neg = (int64_t)(p - 1) - half;
+    const int64_t cmax = neg > half ? neg : half;
+    I.p = p;
+    I.centre_max = (int32_t)cmax;
+
+    const int LS = min_limbs(half, neg, FF_SCHEME_S), LT = min_limbs(half, neg, FF_SCHEME_T);
+    int scheme = o.scheme;
+    if (scheme == FF_SCHEME_AUTO) {
+        scheme = (LS != 0 && (LT == 0 || LS <= LT)) ? FF_SCHEME_S : FF_SCHEME_T;
+        // Multi-modular when it needs clearly fewer int8 products than the
+        // limbs (L^2): c5 (p ~ 2^26, k = 16384) takes 9 instead of 16.  The
+        // margin of 2 charges its extra encoder planes and residue scratch
+        // (DESIGN.md §4.9): c2 (8 vs 9) stays on limbs.
+        const int Ll = scheme == FF_SCHEME_S ? LS : LT;
+        uint32_t q[kMaxMod];
+        u128 M, B;
+        const int nq = crt_select(cmax, k, q, &M, &B);
+        if (nq > 0 && nq + 2 < Ll * Ll) scheme = FF_SCHEME_CRT;
+    }
+    if (scheme == FF_SCHEME_CRT) {
+        const int e = make_crt_plan(p, k, o, cmax, pl);
+        if (e) return e;
+    }
+    const int L = scheme == FF_SCHEME_S ? LS : scheme == FF_SCHEME_T ? LT : 0;
+    bool int_wb = false;
+    if (scheme != FF_SCHEME_CRT) {
+        const int e = make_limb_plan(p, k, o, half, neg, cmax, scheme, L, pl, int_wb);
+        if (e) return e;
+    }
     pl.saturate = o.debug_saturate != 0;
     pl.force_pair = o.cta_group;
 
@@ -178,7 +327,7 @@ int make_plan(uint32_t p, int64_t k, const ff_opts* opts, Plan* out) {
     M.int_wb = int_wb ? 1 : 0;
     // 256^-(G-1) mod p (k-outer carry between k-blocks); 1 when G = 1.
     pl.kinv = 1 % p;
-    if (korder == 2 && I.groups > 1) {
+    if (pl.korder == 2 && I.groups > 1 && !pl.crt) {
         int64_t r0 = p, r1 = 256 % p, s0 = 0, s1 = 1;     // extended Euclid: s1 * 256 = r1 (mod p)
         while (r1 != 0) {
             const int64_t qq = r0 / r1, t = r0 - qq * r1, u = s0 - qq * s1;

@@ -80,7 +80,7 @@ size_t winograd_ws_bytes(const Plan& half, int64_t m, int64_t n, int64_t k) {
     const size_t hm = m / 2, hn = n / 2, hk = k / 2;
     const size_t L = half.info.L, kp = half.info.k_pad;
     return 4 * align256(4 * hm * hk) + 4 * align256(4 * hk * hn) + 7 * align256(L * hm * kp) +
-           7 * align256(L * hn * kp);
+           7 * align256(L * hn * kp) + align256(crt_scratch_bytes(half));
 }
 
 int run_winograd(const Plan& half, bool transA, bool transB, int64_t m, int64_t n, int64_t k, const int32_t* A,
@@ -97,6 +97,7 @@ int run_winograd(const Plan& half, bool transA, bool transB, int64_t m, int64_t 
     int8_t* Bl[7];
     for (int i = 0; i < 7; ++i) Al[i] = reinterpret_cast<int8_t*>(take(L * hm * kp));
     for (int i = 0; i < 7; ++i) Bl[i] = reinterpret_cast<int8_t*>(take(L * hn * kp));
+    void* scratch = take(crt_scratch_bytes(half));   // CRT residue scratch, shared by the 7 launches
 
     // Pre-additions in stored orientation: A quadrants are stored hm x hk (or hk x hm).
     const int64_t a_rows = transA ? hk : hm, a_cols = transA ? hm : hk;
@@ -149,7 +150,8 @@ int run_winograd(const Plan& half, bool transA, bool transB, int64_t m, int64_t 
     const OutSpec* outs[7] = {o1, o2, o3, o4, o5, o6, o7};
     const int nouts[7] = {4, 1, 1, 1, 2, 3, 2};
     for (int i = 0; i < 7; ++i) {
-        const int e = launch_gemm_tc_multi(half, hm, hn, hk, Al[i], Bl[i], outs[i], nouts[i], ldc, i == 6 ? 1 : 0, st);
+        const int e = launch_gemm_tc_multi(half, hm, hn, hk, Al[i], Bl[i], outs[i], nouts[i], ldc, i == 6 ? 1 : 0,
+                                             scratch, st);
         if (e) return e;
     }
     return 0;

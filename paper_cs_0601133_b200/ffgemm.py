@@ -22,7 +22,8 @@ if not os.path.exists(LIB_PATH):
 _lib = ctypes.CDLL(LIB_PATH)
 
 FF_OK, FF_ERR_CUDA, FF_ERR_NOMEM, FF_ERR_ARCH, FF_ERR_OPTS, FF_ERR_INTERNAL = 0, 1, 2, 3, 4, 5
-FF_SCHEME_AUTO, FF_SCHEME_S, FF_SCHEME_T = 0, 1, 2
+FF_SCHEME_AUTO, FF_SCHEME_S, FF_SCHEME_T, FF_SCHEME_CRT = 0, 1, 2, 3
+FF_MAX_MODULI = 16
 
 _i32, _i64, _u32, _u64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, ctypes.c_uint64
 _p, _ch, _sz = ctypes.c_void_p, ctypes.c_char, ctypes.c_size_t
@@ -39,7 +40,8 @@ class ff_plan_info(ctypes.Structure):
                 ("limb_signed", _i32 * 4), ("digit_max", _i32 * 4), ("group_bound", _i64 * 7),
                 ("group_bound_max", _i64), ("kb_max", _i64), ("kb", _i64), ("k_pad", _i64),
                 ("num_kblocks", _i64), ("centre_max", _i32), ("reserved0", _i32),
-                ("carry_max", _i64), ("korder", _i32), ("reserved", _i32 * 1)]
+                ("carry_max", _i64), ("korder", _i32), ("nmod", _i32), ("moduli", _u32 * 16),
+                ("log2_M_floor", _i32), ("log2_bound_ceil", _i32)]
 
 
 _OPTS_P = ctypes.POINTER(ff_opts)
@@ -110,12 +112,14 @@ def ff_plan_query(p: int, k: int, opts=None) -> dict:
     info = ff_plan_info()
     _check(_lib.ff_plan_query(p, k, _opts(opts), ctypes.byref(info)), "ff_plan_query")
     L, G = info.L, info.groups
-    return {"p": info.p, "L": L, "scheme": {1: "S", 2: "T"}[info.scheme], "groups": G,
-            "limb_signed": list(info.limb_signed[:L]), "digit_max": list(info.digit_max[:L]),
-            "group_bound": list(info.group_bound[:G]), "group_bound_max": info.group_bound_max,
+    return {"p": info.p, "L": L, "scheme": {1: "S", 2: "T", 3: "CRT"}[info.scheme], "groups": G,
+            "limb_signed": list(info.limb_signed[:min(L, 4)]), "digit_max": list(info.digit_max[:min(L, 4)]),
+            "group_bound": list(info.group_bound[:min(G, 7)]), "group_bound_max": info.group_bound_max,
             "kb_max": info.kb_max, "kb": info.kb, "k_pad": info.k_pad,
             "num_kblocks": info.num_kblocks, "centre_max": info.centre_max,
-            "carry_max": info.carry_max, "korder": info.korder}
+            "carry_max": info.carry_max, "korder": info.korder, "nmod": info.nmod,
+            "moduli": list(info.moduli[:info.nmod]), "log2_M_floor": info.log2_M_floor,
+            "log2_bound_ceil": info.log2_bound_ceil}
 
 
 def ff_gemm(p, transA, transB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc) -> None:

@@ -73,6 +73,13 @@ def test_fill_uniform_matches_numpy_generator(env):
         assert (got[:, cols:] == -7).all()
 
 
+def _limb_opts(ff, p, k):
+    """The limb scheme AUTO would pick if multi-modular were off (fewest limbs, S on ties)."""
+    LS = ff.ff_plan_query(p, k, {"scheme": 1})["L"]
+    LT = ff.ff_plan_query(p, k, {"scheme": 2})["L"]
+    return {"scheme": 1 if LS <= LT else 2}
+
+
 # ---------------------------------------------------------------- encoder
 
 def _decode(limbs, info):
@@ -92,13 +99,14 @@ def test_encoder_roundtrip(env, p, kmajor):
     torch, ff = env
     rng = np.random.default_rng(p % 997 + kmajor)
     rows, k = 150, 333      # ragged: not multiples of the 64/16 encoder tiles
-    info = ff.ff_plan_query(p, k)
+    lopt = _limb_opts(ff, p, k)
+    info = ff.ff_plan_query(p, k, lopt)
     x = rng.integers(-2 ** 31, 2 ** 31, size=(rows, k), dtype=np.int64).astype(np.int32)
     x[0, :min(k, p)] = np.arange(min(k, p))                       # include 0..p-1 verbatim
     src = x if kmajor else np.ascontiguousarray(x.T)
     X = _dev(torch, src)
     limbs = torch.full((info["L"], rows, info["k_pad"]), 99, dtype=torch.int8, device="cuda")
-    ff.ff_encode(p, k, None, kmajor, rows, X, src.shape[1], limbs)
+    ff.ff_encode(p, k, lopt, kmajor, rows, X, src.shape[1], limbs)
     torch.cuda.synchronize()
     lb = limbs.cpu().numpy()
     r = np.mod(x.astype(np.int64), p)
@@ -120,9 +128,10 @@ def test_encoder_exhaustive_residues(env, p):
     rows = (p + k - 1) // k
     vals = np.arange(rows * k, dtype=np.int64) % p
     X = _dev(torch, vals.astype(np.int32).reshape(rows, k))
-    info = ff.ff_plan_query(p, k)
+    lopt = _limb_opts(ff, p, k)
+    info = ff.ff_plan_query(p, k, lopt)
     limbs = torch.empty((info["L"], rows, info["k_pad"]), dtype=torch.int8, device="cuda")
-    ff.ff_encode(p, k, None, 1, rows, X, k, limbs)
+    ff.ff_encode(p, k, lopt, 1, rows, X, k, limbs)
     torch.cuda.synchronize()
     dec = _decode(limbs.cpu().numpy(), info).reshape(-1)
     want = np.where(vals > (p - 1) // 2, vals - p, vals)
@@ -135,12 +144,15 @@ SHAPES = [(1, 1, 1), (3, 5, 7), (128, 256, 128), (129, 257, 129), (200, 300, 100
           (256, 512, 640), (77, 600, 33)]
 
 
+@pytest.mark.parametrize("scheme", ["limb", "crt"])
 @pytest.mark.parametrize("cta_group", [1, 2])
 @pytest.mark.parametrize("p", CONFIG_PRIMES)
 @pytest.mark.parametrize("tA,tB", [("N", "N"), ("T", "N"), ("N", "T"), ("T", "T")])
-def test_gemm_vs_oracle_shapes(env, p, tA, tB, cta_group):
-    """Both kernels: 128x256 single-CTA and 256x256 CTA-pair (cta_group::2)."""
+def test_gemm_vs_oracle_shapes(env, p, tA, tB, cta_group, scheme):
+    """Both kernels: 128x256 single-CTA and 256x256 CTA-pair (cta_group::2);
+    both product schemes: limbs (Horner in TMEM) and multi-modular (CRT)."""
     torch, ff = env
+    sopt = _limb_opts(ff, p, 1000) if scheme == "limb" else {"scheme": 3}
     rng = np.random.default_rng(p % 1009 + ord(tA) * 3 + ord(tB) + cta_group)
     for si, (m, n, k) in enumerate(SHAPES):
         ldx = si % 3
@@ -150,7 +162,7 @@ def test_gemm_vs_oracle_shapes(env, p, tA, tB, cta_group):
         alpha = [1, p - 1, 3, int(rng.integers(0, p))][si % 4]
         beta = [0, 1, p - 1, int(rng.integers(0, p))][(si + 1) % 4]
         got = _run_gpu(torch, ff, p, tA, tB, m, n, k, alpha, Abuf, Bbuf, beta, Cbuf,
-                       {"cta_group": cta_group})
+                       dict(sopt, cta_group=cta_group))
         _check(p, tA, tB, m, n, k, alpha, Abuf, Bbuf, beta, Cbuf, got)
 
 
@@ -170,7 +182,8 @@ def test_gemm_other_primes_and_noncanonical_inputs(env, p):
 @pytest.mark.parametrize("korder", [1, 2])
 @pytest.mark.parametrize("cta_group", [1, 2])
 @pytest.mark.parametrize("p,scheme", [(65521, 2), (65521, 1), (8388593, 1), (67108859, 1),
-                                      (251, 1), (8388593, 2), (3, 1), (65537, 1)])
+                                      (251, 1), (8388593, 2), (3, 1), (65537, 1),
+                                      (67108859, 3), (65521, 3), (2 ** 31 - 1, 3), (3, 3)])
 def test_kb_override_forces_mid_k_reductions(env, p, scheme, cta_group, korder):
     """Shrunk k-block ("overflow safety under shrunk gamma" analogue):
     several mid-k reductions per weight group must not change the result."""
@@ -179,7 +192,7 @@ def test_kb_override_forces_mid_k_reductions(env, p, scheme, cta_group, korder):
     m, n, k = 130, 260, 1000
     Abuf, Bbuf, Cbuf = _stored(rng, m, k, p), _stored(rng, k, n, p), _stored(rng, m, n, p)
     opts = {"kb_override": 128, "scheme": scheme, "cta_group": cta_group, "korder": korder}
-    assert ff.ff_plan_query(p, k, opts)["num_kblocks"] == 8
+    assert ff.ff_plan_query(p, k, opts)["num_kblocks"] == 8     # (CRT plans always run korder 1)
     got = _run_gpu(torch, ff, p, "N", "N", m, n, k, 5, Abuf, Bbuf, 7, Cbuf, opts)
     _check(p, "N", "N", m, n, k, 5, Abuf, Bbuf, 7, Cbuf, got)
 
@@ -205,7 +218,8 @@ def test_accumulator_at_the_bound_closed_form(env, p):
     """All entries = a digit-extreme residue v, k = the planner's largest k-block
     (and 2 k-blocks + a ragged tail): every entry must be k v^2 mod p."""
     torch, ff = env
-    info = ff.ff_plan_query(p, 1, {"korder": 1})   # the safety k-block
+    lopt = _limb_opts(ff, p, 1)
+    info = ff.ff_plan_query(p, 1, dict(lopt, korder=1))   # the safety k-block
     v = _adversarial_residue(p, info)
     if p == 65521:
         assert v == 33008
@@ -218,9 +232,58 @@ def test_accumulator_at_the_bound_closed_form(env, p):
             C.fill_(-1)
             kbo = info["kb"] if ko == 1 else 0      # k-outer: the locality k-block, several per k
             ff.ff_gemm_ex(p, "N", "N", m, n, k, 1, A, k, B, n, 0, C, n,
-                          {"debug_saturate": sat, "cta_group": grp, "korder": ko, "kb_override": kbo})
+                          dict(lopt, debug_saturate=sat, cta_group=grp, korder=ko, kb_override=kbo))
             torch.cuda.synchronize()
             assert (C == (k * v * v) % p).all().item(), (p, k, sat, grp, ko)
+
+
+# ---------------------------------------------------------------- multi-modular (CRT) specifics
+
+@pytest.mark.parametrize("p", CONFIG_PRIMES + [2, 3, 65537, 2 ** 31 - 1])
+@pytest.mark.parametrize("kmajor", [1, 0])
+def test_crt_encoder_residue_planes(env, p, kmajor):
+    """Plane i holds the centred residue of centre(x mod p) modulo q_i, as s8."""
+    torch, ff = env
+    rng = np.random.default_rng(p % 991 + 7 * kmajor)
+    rows, k = 150, 333
+    opts = {"scheme": 3}
+    info = ff.ff_plan_query(p, k, opts)
+    x = rng.integers(-2 ** 31, 2 ** 31, size=(rows, k), dtype=np.int64).astype(np.int32)
+    x[0, :min(k, p)] = np.arange(min(k, p))
+    src = x if kmajor else np.ascontiguousarray(x.T)
+    planes = torch.full((info["L"], rows, info["k_pad"]), 99, dtype=torch.int8, device="cuda")
+    ff.ff_encode(p, k, opts, kmajor, rows, _dev(torch, src), src.shape[1], planes)
+    torch.cuda.synchronize()
+    pl = planes.cpu().numpy().astype(np.int64)
+    r = np.mod(x.astype(np.int64), p)
+    c = np.where(r > (p - 1) // 2, r - p, r)
+    for i, q in enumerate(info["moduli"]):
+        d = pl[i, :, :k]
+        assert ((d - c) % q == 0).all(), (p, q)
+        assert d.min() >= -(q // 2) and d.max() <= (q - 1) // 2
+        assert (pl[i, :, k:] == 0).all()
+
+
+@pytest.mark.parametrize("p,k", [(67108859, 16384), (67108859, 333), (2 ** 31 - 1, 4096),
+                                 (65521, 8192), (8388593, 4096), (65537, 1000)])
+def test_crt_dot_product_at_the_bound(env, p, k):
+    """|X| = k cmax^2, the largest exact dot product the moduli must recover
+    (M >= 4 k cmax^2): all entries -cmax (X = +k cmax^2) and A = -cmax against
+    B = +cmax (X = -k cmax^2); every entry must be X mod p."""
+    torch, ff = env
+    cm = (p - 1) // 2
+    m, n = 256, 512
+    for va, vb in ((p - cm, p - cm), (p - cm, cm), (cm, cm)):
+        A = torch.full((m, k), va, dtype=torch.int32, device="cuda")
+        B = torch.full((k, n), vb, dtype=torch.int32, device="cuda")
+        C = torch.empty((m, n), dtype=torch.int32, device="cuda")
+        X = k * ((va + cm) % p - cm) * ((vb + cm) % p - cm)
+        assert abs(X) == k * cm * cm
+        for grp in (1, 2):
+            C.fill_(-1)
+            ff.ff_gemm_ex(p, "N", "N", m, n, k, 1, A, k, B, n, 0, C, n, {"scheme": 3, "cta_group": grp})
+            torch.cuda.synchronize()
+            assert (C == X % p).all().item(), (p, k, va, vb, grp)
 
 
 def test_quick_returns_and_degenerate(env):
@@ -418,6 +481,20 @@ def test_winograd_rejects_odd_shapes(env):
     C = torch.zeros((513, 512), dtype=torch.int32, device="cuda")
     with pytest.raises(ff.FFError):
         ff.fgemm(65521, A, B, C, opts={"winograd": 1})
+
+
+def test_c5_full_size_crt_equals_limbs(env):
+    """c5 at full size: the multi-modular path (the default there) and the
+    4-limb Horner path give bit-identical outputs."""
+    torch, ff = env
+    p, m, n, k, tA, tB, alpha, beta, seed = CONFIGS["c5"]
+    A, B, C = _make_config(torch, ff, "c5")
+    assert ff.ff_plan_query(p, k)["scheme"] == "CRT"
+    ref = C.clone()
+    ff.fgemm(p, A, B, C, alpha, beta, tA, tB, opts={"scheme": 3, "winograd": -1})
+    ff.fgemm(p, A, B, ref, alpha, beta, tA, tB, opts={"scheme": 1, "winograd": -1})
+    torch.cuda.synchronize()
+    assert torch.equal(C, ref)
 
 
 @pytest.mark.parametrize("name", ["c2", "c5"])

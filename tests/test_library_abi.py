@@ -117,7 +117,8 @@ def _centred_all(p):
     (67108859, 4, "S", [128, 128, 128, 2], 43008),  # c5
 ])
 def test_planner_matches_paper_bound(ff, p, L, scheme, D, kb_max):
-    info = ff.ff_plan_query(p, 1000)
+    lopt = {"scheme": {"S": 1, "T": 2}[scheme]}      # the limb scheme (AUTO may pick CRT for c5)
+    info = ff.ff_plan_query(p, 1000, lopt)
     assert info["L"] == L and info["scheme"] == scheme
     assert info["digit_max"] == D
     # Eq. (2) with gamma = 32 for the s32 accumulator, per weight group, plus one
@@ -139,8 +140,8 @@ def test_planner_matches_paper_bound(ff, p, L, scheme, D, kb_max):
     # every config fits one safe k-block ("none of the 5 needs it") in
     # group-outer order; the default k-outer order blocks k by 8192/L for L2 locality
     for k in (512, 4096, 8192, 16384):
-        assert ff.ff_plan_query(p, k, {"korder": 1})["num_kblocks"] == 1
-        d = ff.ff_plan_query(p, k)
+        assert ff.ff_plan_query(p, k, dict(lopt, korder=1))["num_kblocks"] == 1
+        d = ff.ff_plan_query(p, k, lopt)
         loc = -(-(8192 // L) // 128) * 128
         assert d["korder"] == 2 and d["kb"] == min(loc, info["kb"]) and d["num_kblocks"] == -(-k // d["kb"])
 
@@ -148,6 +149,8 @@ def test_planner_matches_paper_bound(ff, p, L, scheme, D, kb_max):
 @pytest.mark.parametrize("p", [2, 3, 5, 251, 257, 65279, 65521, 65537])
 def test_digit_bounds_exhaustive_small_primes(ff, p):
     info = ff.ff_plan_query(p, 64)
+    if info["scheme"] == "CRT":          # 65537 (+-32768 needs 3 limbs): AUTO is multi-modular
+        info = ff.ff_plan_query(p, 64, {"scheme": 1})
     L = info["L"]
     split = _balanced_digits if info["scheme"] == "S" else _twos_digits
     seen = [0] * L
@@ -170,7 +173,13 @@ def test_scheme_choice_rule(ff):
     assert ff.ff_plan_query(65279, 8)["scheme"] == "S"   # 2 balanced digits reach +-32639
     assert ff.ff_plan_query(65521, 8)["scheme"] == "T"   # centred +-32760 needs T for L=2
     assert ff.ff_plan_query(65521, 8, {"scheme": 1})["L"] == 3
-    assert ff.ff_plan_query(2 ** 31 - 1, 8)["L"] == 4
+    assert ff.ff_plan_query(2 ** 31 - 1, 8, {"scheme": 1})["L"] == 4
+    # multi-modular when it needs >= 3 fewer int8 products than L^2
+    assert ff.ff_plan_query(2 ** 31 - 1, 8)["scheme"] == "CRT"
+    assert ff.ff_plan_query(67108859, 16384)["scheme"] == "CRT"      # c5: 9 moduli vs 16
+    assert ff.ff_plan_query(67108859, 16384)["L"] == 9
+    assert ff.ff_plan_query(8388593, 4096)["scheme"] == "S"          # c2: 8 vs 9, stays on limbs
+    assert ff.ff_plan_query(65521, 8192)["scheme"] == "T"            # c4: 6 vs 4
 
 
 def test_kb_override_rules(ff):
