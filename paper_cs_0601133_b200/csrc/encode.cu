@@ -130,9 +130,32 @@ __global__ void __launch_bounds__(256) encode_trans_kernel(ModP M, int64_t rows,
 // residue of c (the centred residue of x mod p) modulo q_i, as s8.  The same
 // two access patterns as the limb encoders; the moduli are runtime constants.
 
-__device__ __forceinline__ uint32_t crt_digit(int32_t c, const CrtConsts& C, int i) {
-    const uint32_t r = residue_small(c, C.q[i], C.mu[i], C.off31[i]);
-    return static_cast<uint32_t>(centre_small(r, C.q[i], C.half[i])) & 0xFFu;
+// Centred residue of c mod q as a byte, in fp32 (full-rate FFMA instead of
+// integer Barrett).  c = h1 2^15 + h0 with h0 in [0, 2^15): s = h1 (2^15 mod q)
+// + h0 satisfies |s| < 2^23 for odd q <= 255, so s is exact in fp32 and
+// t = fl(s fl(1/q)) rounded to an integer equals round(s/q): its error is below
+// |s/q| 2^-24 < 1/(2q), while s/q is at least 1/(2q) away from any half-integer
+// (q odd).  r = s - q t is then the exact centred residue, and the low byte of
+// the float r + 1.5 2^23 is its two's-complement byte.  q = 256: the low byte of c.
+struct CrtDigitsIn {
+    float h0, h1;
+};
+
+__device__ __forceinline__ CrtDigitsIn crt_split(int32_t c) {
+    const uint32_t h0 = static_cast<uint32_t>(c) & 0x7FFFu;
+    const uint32_t h1 = static_cast<uint32_t>((c >> 15) + 32768);          // in [0, 2^16)
+    CrtDigitsIn d;
+    d.h0 = __uint_as_float(0x4B000000u | h0) - 8388608.0f;
+    d.h1 = __uint_as_float(0x4B000000u | h1) - (8388608.0f + 32768.0f);
+    return d;
+}
+
+__device__ __forceinline__ uint32_t crt_digit(int32_t c, const CrtDigitsIn& d, const CrtConsts& C, int i) {
+    if (C.q[i] == 256u) return static_cast<uint32_t>(c) & 0xFFu;
+    const float s = fmaf(d.h1, C.fw15[i], d.h0);
+    const float t = fmaf(s, C.finv[i], 12582912.0f) - 12582912.0f;
+    const float r = fmaf(-C.fq[i], t, s);
+    return __float_as_uint(r + 12582912.0f) & 0xFFu;
 }
 
 __global__ void __launch_bounds__(256) encode_crt_direct_kernel(ModP M, CrtConsts C, int64_t rows, int64_t k,
@@ -155,14 +178,18 @@ __global__ void __launch_bounds__(256) encode_crt_direct_kernel(ModP M, CrtConst
 #pragma unroll
                 for (int t = 0; t < 4; ++t) c[t] = (kk + t < k) ? __ldg(src + kk + t) : 0;
             }
+            CrtDigitsIn dg[4];
 #pragma unroll
-            for (int t = 0; t < 4; ++t) c[t] = centre(residue_i32(c[t], M), M);
+            for (int t = 0; t < 4; ++t) {
+                c[t] = centre(residue_i32(c[t], M), M);
+                dg[t] = crt_split(c[t]);
+            }
 #pragma unroll
             for (int i = 0; i < kMaxMod; ++i) {
                 if (i < C.nq) {
                     uint32_t w = 0;
 #pragma unroll
-                    for (int t = 0; t < 4; ++t) w |= crt_digit(c[t], C, i) << (8 * t);
+                    for (int t = 0; t < 4; ++t) w |= crt_digit(c[t], dg[t], C, i) << (8 * t);
                     dst[g + i * (plane / 4)] = w;
                 }
             }
@@ -205,7 +232,8 @@ __global__ void __launch_bounds__(256) encode_crt_trans_kernel(ModP M, CrtConsts
                 const int kl = lk + 8 * i;
 #pragma unroll
                 for (int l = 0; l < 4; ++l)
-                    if (b0 + l < C.nq) tile[l][lr][kl] = static_cast<uint8_t>(crt_digit(cv[i], C, b0 + l));
+                    if (b0 + l < C.nq)
+                        tile[l][lr][kl] = static_cast<uint8_t>(crt_digit(cv[i], crt_split(cv[i]), C, b0 + l));
             }
             __syncthreads();
             if (r < rows && kc < k_pad) {

@@ -226,7 +226,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ------------------------------------------------ TMA producer (both CTAs)
         if (lane == 0) {
             uint32_t stage = 0, phase = 0;
-            const uint64_t pol = (a.hints & 1) ? ptx::policy_evict_last() : ptx::policy_evict_normal();
+            // L2 policies (experiment bits, FF_HINTS): bit0 both operands evict_last;
+            // bit2 A evict_last + B evict_first; bit3 A evict_first + B evict_last.
+            uint64_t polA = (a.hints & 1) ? ptx::policy_evict_last() : ptx::policy_evict_normal();
+            uint64_t polB = polA;
+            if (a.hints & 4) { polA = ptx::policy_evict_last(); polB = ptx::policy_evict_first(); }
+            if (a.hints & 8) { polA = ptx::policy_evict_first(); polB = ptx::policy_evict_last(); }
             for_each_step(a, unit, nunits, tbase, tcount, [&](int tile, int, int g, int kb) {
                 int tm, tn;
                 tile_coords(a, tile, tm, tn);
@@ -241,14 +246,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                         uint8_t* sa = smem + stage * K::STAGE;
                         if (kPair == 1) {
                             ptx::mbar_arrive_expect_tx(&sh->full[stage], K::STAGE);
-                            ptx::tma_load_3d(sa, &tmA, &sh->full[stage], ks * kBK, arow, li, pol);
-                            ptx::tma_load_3d(sa + K::A_BYTES, &tmB, &sh->full[stage], ks * kBK, brow, lj, pol);
+                            ptx::tma_load_3d(sa, &tmA, &sh->full[stage], ks * kBK, arow, li, polA);
+                            ptx::tma_load_3d(sa + K::A_BYTES, &tmB, &sh->full[stage], ks * kBK, brow, lj, polB);
                         } else {
                             // both CTAs' bytes are counted on the leader's full barrier
                             if (leader) ptx::mbar_arrive_expect_tx(&sh->full[stage], 2 * K::STAGE);
                             const uint32_t bar = ptx::mapa(ptx::smem_u32(&sh->full[stage]), 0);
-                            ptx::tma_load_3d_pair(sa, &tmA, bar, ks * kBK, arow, li, pol);
-                            ptx::tma_load_3d_pair(sa + K::A_BYTES, &tmB, bar, ks * kBK, brow, lj, pol);
+                            ptx::tma_load_3d_pair(sa, &tmA, bar, ks * kBK, arow, li, polA);
+                            ptx::tma_load_3d_pair(sa + K::A_BYTES, &tmB, bar, ks * kBK, brow, lj, polB);
                         }
                         if (++stage == K::STAGES) { stage = 0; phase ^= 1; }
                     }

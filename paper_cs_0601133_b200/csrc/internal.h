@@ -45,6 +45,9 @@ struct CrtConsts {
     uint32_t v[kMaxMod];       // (M_i mod q_i)^-1 mod q_i
     uint32_t W[kMaxMod];       // M_i mod p
     uint32_t R[kMaxMod];       // round(2^24 / q_i): fixed-point 1/q_i for the quotient t
+    float fq[kMaxMod];         // q as float (encoder, fp32 residue path)
+    float finv[kMaxMod];       // fl(1/q)
+    float fw15[kMaxMod];       // 2^15 mod q, as float
     uint32_t Mneg;             // (p - M mod p) mod p
     unsigned long long mu64;   // floor(2^64 / p) (Barrett for the 64-bit sum)
 };

@@ -173,6 +173,9 @@ int make_crt_plan(uint32_t p, int64_t k, const ff_opts& o, int64_t cmax, Plan& p
         C.v[i] = inv_mod((uint32_t)(Mi % qi), qi);
         C.W[i] = (uint32_t)(Mi % p);
         C.R[i] = (uint32_t)(((((uint64_t)1) << 25) / qi + 1) / 2);   // round(2^24 / q)
+        C.fq[i] = (float)qi;
+        C.finv[i] = (float)(1.0 / (double)qi);
+        C.fw15[i] = (float)(32768u % qi);
     }
     return 0;
 }
