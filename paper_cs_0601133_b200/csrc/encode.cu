@@ -70,11 +70,12 @@ __global__ void __launch_bounds__(256) encode_direct_kernel(ModP M, int64_t rows
 }
 
 // Source transposed: limb row r, column kk = X[kk*ldx + r].  Tiles of 32 rows
-// (r) x 128 columns (kk): the load phase reads 128-byte rows of X, encodes
-// each value and scatters its L digit bytes into SMEM byte tiles [L][32][132]
-// (row pitch 33 words: both the byte stores and the word reads below are
-// bank-conflict free); the write phase then emits whole 128-byte limb rows,
-// four rows per warp per plane.
+// (r) x 128 columns (kk): the load phase reads 128-byte rows of X (a warp =
+// 32 consecutive r at one kk); each thread holds 4 groups of 4 consecutive kk
+// of its row, so the digits of a group pack into one 32-bit word per plane,
+// stored into SMEM tiles [L][32][132] (row pitch 33 words: the word stores
+// and the 16-byte reads below are bank-conflict free); the write phase then
+// emits whole 128-byte limb rows, four rows per warp per plane.
 constexpr int kTR = 32, kTK = 128, kPitch = kTK + 4;
 template <int L, int SCHEME>
 __global__ void __launch_bounds__(256) encode_trans_kernel(ModP M, int64_t rows, int64_t k, int64_t k_pad,
@@ -88,30 +89,37 @@ __global__ void __launch_bounds__(256) encode_trans_kernel(ModP M, int64_t rows,
     const int lk = threadIdx.x / kTR;       // load: kk offset 0..7 (+8 i)
     const int wr = (threadIdx.x / 32) * 4 + (threadIdx.x % 32) / 8;   // write: row 0..31
     const int wc = (threadIdx.x % 8) * 16;                            // write: column 0..112
-    for (int64_t t = blockIdx.x; t < tiles_r * tiles_k; t += gridDim.x) {
+    // Software-pipelined: the next tile's 16 loads are issued before this
+    // tile's write phase, so HBM reads overlap the SMEM transpose and stores.
+    int32_t xv[kTK / 8];
+    auto load_tile = [&](int64_t t) {
         const int64_t r0 = (t % tiles_r) * kTR;
         const int64_t kk0 = (t / tiles_r) * kTK;
-        __syncthreads();
-        int32_t xv[kTK / 8];
         const bool rin = (r0 + lr) < rows;
         const int32_t* col = X + (r0 + lr);
 #pragma unroll
         for (int i = 0; i < kTK / 8; ++i) {        // all 16 loads in flight first
-            const int64_t kk = kk0 + lk + 8 * i;
+            const int64_t kk = kk0 + 4 * lk + 32 * (i >> 2) + (i & 3);
             xv[i] = (kk < k && rin) ? __ldg(col + kk * ldx) : 0;
         }
+    };
+    const int64_t ntiles = tiles_r * tiles_k;
+    if (static_cast<int64_t>(blockIdx.x) < ntiles) load_tile(blockIdx.x);
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int64_t r0 = (t % tiles_r) * kTR;
+        const int64_t kk0 = (t / tiles_r) * kTK;
+        __syncthreads();
 #pragma unroll
-        for (int i = 0; i < kTK / 8; ++i) {
-            const int kl = lk + 8 * i;
-            int32_t c = centre(residue_i32(xv[i], M), M);
+        for (int g = 0; g < 4; ++g) {
+            uint32_t w[L];
 #pragma unroll
-            for (int l = 0; l < L; ++l) {
-                const int32_t lo = (SCHEME == FF_SCHEME_S) ? static_cast<int32_t>(static_cast<int8_t>(c & 0xFF))
-                                                           : (c & 0xFF);
-                tile[l][lr][kl] = static_cast<uint8_t>(lo & 0xFF);
-                c = (c - lo) >> 8;
-            }
+            for (int l = 0; l < L; ++l) w[l] = 0;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) put_digits<L, SCHEME>(centre(residue_i32(xv[4 * g + e], M), M), e, w);
+#pragma unroll
+            for (int l = 0; l < L; ++l) *reinterpret_cast<uint32_t*>(&tile[l][lr][4 * lk + 32 * g]) = w[l];
         }
+        if (t + gridDim.x < ntiles) load_tile(t + gridDim.x);
         __syncthreads();
         const int64_t r = r0 + wr;
         const int64_t kc = kk0 + wc;
@@ -210,30 +218,45 @@ __global__ void __launch_bounds__(256) encode_crt_trans_kernel(ModP M, CrtConsts
     const int lk = threadIdx.x / kTR;
     const int wr = (threadIdx.x / 32) * 4 + (threadIdx.x % 32) / 8;
     const int wc = (threadIdx.x % 8) * 16;
-    for (int64_t t = blockIdx.x; t < tiles_r * tiles_k; t += gridDim.x) {
+    int32_t xv[kTK / 8];
+    auto load_tile = [&](int64_t t) {
         const int64_t r0 = (t % tiles_r) * kTR;
         const int64_t kk0 = (t / tiles_r) * kTK;
-        int32_t cv[kTK / 8];
         const bool rin = (r0 + lr) < rows;
         const int32_t* col = X + (r0 + lr);
 #pragma unroll
         for (int i = 0; i < kTK / 8; ++i) {
-            const int64_t kk = kk0 + lk + 8 * i;
-            cv[i] = (kk < k && rin) ? __ldg(col + kk * ldx) : 0;
+            const int64_t kk = kk0 + 4 * lk + 32 * (i >> 2) + (i & 3);
+            xv[i] = (kk < k && rin) ? __ldg(col + kk * ldx) : 0;
         }
+    };
+    const int64_t ntiles = tiles_r * tiles_k;
+    if (static_cast<int64_t>(blockIdx.x) < ntiles) load_tile(blockIdx.x);
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int64_t r0 = (t % tiles_r) * kTR;
+        const int64_t kk0 = (t / tiles_r) * kTK;
+        int32_t cv[kTK / 8];
 #pragma unroll
-        for (int i = 0; i < kTK / 8; ++i) cv[i] = centre(residue_i32(cv[i], M), M);
+        for (int i = 0; i < kTK / 8; ++i) cv[i] = centre(residue_i32(xv[i], M), M);
+        if (t + gridDim.x < ntiles) load_tile(t + gridDim.x);     // next tile's loads in flight
         const int64_t r = r0 + wr;
         const int64_t kc = kk0 + wc;
         for (int b0 = 0; b0 < C.nq; b0 += 4) {
             __syncthreads();
 #pragma unroll
-            for (int i = 0; i < kTK / 8; ++i) {
-                const int kl = lk + 8 * i;
+            for (int g = 0; g < 4; ++g) {
+                uint32_t w[4] = {0, 0, 0, 0};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int32_t c = cv[4 * g + e];
+                    const CrtDigitsIn dg = crt_split(c);
+#pragma unroll
+                    for (int l = 0; l < 4; ++l)
+                        if (b0 + l < C.nq) w[l] |= crt_digit(c, dg, C, b0 + l) << (8 * e);
+                }
 #pragma unroll
                 for (int l = 0; l < 4; ++l)
-                    if (b0 + l < C.nq)
-                        tile[l][lr][kl] = static_cast<uint8_t>(crt_digit(cv[i], crt_split(cv[i]), C, b0 + l));
+                    if (b0 + l < C.nq) *reinterpret_cast<uint32_t*>(&tile[l][lr][4 * lk + 32 * g]) = w[l];
             }
             __syncthreads();
             if (r < rows && kc < k_pad) {
