@@ -4,9 +4,12 @@ Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
 ``--impl reference`` legs may import this package.  The product path
 (``paper_cs_0601133_b200``) never imports it and shares no code with it.
 
-``oracle.c`` holds the definition (see its header for the passages followed);
-this module only marshals numpy arrays into it, plus ``winograd.py`` (Table 1
-op counts and the Table 2 schedule) in exact Python ints.
+``oracle.c`` holds the definitions (fgemm, and the triangular solve ``trsm``
+of PAPER.md Sec. 4; see its header for the passages followed); this module
+only marshals numpy arrays into it, plus ``winograd.py`` (Table 1 op counts
+and the Table 2 schedule) and ``bounds.py`` (the paper's
+delayed-reduction thresholds: Eq. (1)/(2), Cor. 3.4, Thm. 4.2, Eq. (4)/(5))
+in exact Python ints.
 
 Parity status: every function here is pinned by tests/test_oracle_pins.py.
 """
@@ -54,6 +57,9 @@ def _load():
         lib.oracle_matvec.argtypes = [_u32, _char, _i64, _i64, _p, _i64, _p, _p, ctypes.c_int]
         lib.oracle_matvec.restype = ctypes.c_int
         lib.oracle_max_threads.restype = ctypes.c_int
+        lib.oracle_trsm.argtypes = [_u32, _char, _char, _char, _char, _i64, _i64, _u32, _p, _i64,
+                                    _p, _i64, ctypes.c_int]
+        lib.oracle_trsm.restype = ctypes.c_int
         _lib = lib
     return _lib
 
@@ -135,3 +141,22 @@ def matvec(p: int, trans: str, X: np.ndarray, v: np.ndarray, nthreads: int = 0) 
     if e:
         raise ValueError("oracle_matvec argument %d invalid" % -e)
     return out
+
+
+def trsm(p: int, side: str, uplo: str, transA: str, diag: str, alpha: int, A: np.ndarray,
+         B: np.ndarray, nthreads: int = 0) -> np.ndarray:
+    """X with op(A) X = alpha B (side 'L') or X op(A) = alpha B (side 'R'), mod p,
+    as a new int32 array (Sec. 4, plain substitution; see oracle.c)."""
+    lib = _load()
+    A = _c32(A)
+    X = np.array(_c32(B), copy=True)
+    m, n = X.shape
+    e = lib.oracle_trsm(p, side.encode(), uplo.encode(), transA.encode(), diag.encode(), m, n,
+                        alpha % (1 << 32), _ptr(A), _ld(A), _ptr(X), _ld(X), nthreads)
+    if e < 0:
+        raise ValueError("oracle_trsm argument %d invalid" % -e)
+    if e == 1:
+        raise ZeroDivisionError("oracle_trsm: a diagonal entry is not invertible mod p")
+    if e:
+        raise MemoryError("oracle_trsm")
+    return X

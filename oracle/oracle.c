@@ -32,6 +32,9 @@
  * is formed in unsigned __int128 and reduced.  Nothing is reordered: each
  * output is the dot product over l = 0..k-1 in order.
  *
+ * oracle_trsm (below) is the triangular solve of PAPER.md Sec. 4 written as
+ * plain substitution; see its own header.
+ *
  * Parity status: pinned (see tests/test_oracle_pins.py): SPEC worked example,
  * exhaustive GF(2)/GF(3) brute force, random shapes vs Python big integers,
  * identity/permutation matrices, closed forms, transpose identity,
@@ -39,6 +42,7 @@
  */
 #include <stdint.h>
 #include <stddef.h>
+#include <stdlib.h>
 #ifdef _OPENMP
 #include <omp.h>
 #endif
@@ -173,6 +177,114 @@ int oracle_matvec(uint32_t p, char trans, int64_t rows, int64_t cols,
         }
         out[i] = (int32_t)(uint64_t)(s % p);
     }
+    return 0;
+}
+
+/* ------------------------------------------------------------------------
+ * ftrsm: triangular solve with a matrix right-hand side (Sec. 4,
+ * l.346-356: "the operation B <- U^{-1} B, where U is m x m upper triangular
+ * and B is m x n", in the BLAS trsm convention l.348).  Written out as plain
+ * substitution over Z/pZ, one right-hand side at a time -- the definition
+ * the block-recursive Algorithm 1 (l.366-384) reaches exactly:
+ *
+ *   side = 'L':  op(A) X = alpha B   (op(A) m x m, X and B m x n)
+ *   side = 'R':  X op(A) = alpha B   (op(A) n x n)
+ *
+ * op(A) = A (transA = 'N') or A^T ('T'); uplo names the triangle of A that is
+ * read (the other one is never referenced); diag = 'U' means a unit diagonal
+ * that is not read.  Divisions by the diagonal are multiplications by its
+ * inverse mod p (extended Euclid), the field operations of l.398-400.
+ * X overwrites B.  Returns 0, -i for an invalid argument i, or 1 when a
+ * diagonal entry is not invertible mod p (B is then left partially solved).
+ * ------------------------------------------------------------------------ */
+static int64_t inv_mod(uint64_t a, int64_t p)
+{
+    int64_t r0 = p, r1 = (int64_t)(a % (uint64_t)p), s0 = 0, s1 = 1;
+    while (r1 != 0) {
+        int64_t q = r0 / r1, t = r0 - q * r1, u = s0 - q * s1;
+        r0 = r1; r1 = t; s0 = s1; s1 = u;
+    }
+    if (r0 != 1) return -1;
+    return ((s0 % p) + p) % p;
+}
+
+/* T(i, l) = op(A)[i][l], reduced mod p. */
+static uint64_t t_elem(const int32_t *A, int64_t lda, int tA, int64_t i, int64_t l, int64_t p)
+{
+    return residue(tA ? A[l * lda + i] : A[i * lda + l], p);
+}
+
+int oracle_trsm(uint32_t p, char side, char uplo, char transA, char diag, int64_t m, int64_t n,
+                uint32_t alpha, const int32_t *A, int64_t lda, int32_t *B, int64_t ldb, int nthreads)
+{
+    if (p < 2 || p >= (1u << 31)) return -1;
+    const int left = (side == 'L' || side == 'l'), right = (side == 'R' || side == 'r');
+    if (!left && !right) return -2;
+    const int up = (uplo == 'U' || uplo == 'u'), lo = (uplo == 'L' || uplo == 'l');
+    if (!up && !lo) return -3;
+    if (!is_n(transA) && !is_t(transA)) return -4;
+    const int unit = (diag == 'U' || diag == 'u');
+    if (!unit && !(diag == 'N' || diag == 'n')) return -5;
+    if (m < 0) return -6;
+    if (n < 0) return -7;
+    const int64_t dim = left ? m : n;
+    if (lda < (dim > 1 ? dim : 1)) return -10;
+    if (ldb < (n > 1 ? n : 1)) return -12;
+    const int tA = is_t(transA);
+    const int t_upper = up ^ tA;           /* op(A) is upper triangular */
+    const int64_t P = (int64_t)p;
+    const uint64_t al = alpha % p;
+    /* inverses of the diagonal of op(A) */
+    int singular = 0;
+    int64_t *inv = NULL;
+    if (dim > 0) {
+        inv = (int64_t *)malloc((size_t)dim * sizeof(int64_t));
+        if (!inv) return 2;
+        for (int64_t i = 0; i < dim; ++i) {
+            inv[i] = unit ? 1 : inv_mod(t_elem(A, lda, tA, i, i, P), P);
+            if (inv[i] < 0) singular = 1;
+        }
+    }
+    if (singular) { free(inv); return 1; }
+#ifdef _OPENMP
+    if (nthreads <= 0) nthreads = omp_get_max_threads();
+#endif
+    if (left) {
+        /* columns of B are independent right-hand sides */
+#ifdef _OPENMP
+#pragma omp parallel for schedule(dynamic, 4) num_threads(nthreads)
+#endif
+        for (int64_t j = 0; j < n; ++j) {
+            for (int64_t s = 0; s < m; ++s) {
+                const int64_t i = t_upper ? m - 1 - s : s;      /* back / forward substitution */
+                u128 acc = (u128)al * residue(B[i * ldb + j], P);
+                u128 sub = 0;
+                const int64_t l0 = t_upper ? i + 1 : 0, l1 = t_upper ? m : i;
+                for (int64_t l = l0; l < l1; ++l)
+                    sub += (u128)t_elem(A, lda, tA, i, l, P) * (uint64_t)B[l * ldb + j];
+                const uint64_t v = (uint64_t)((acc % P + (P - sub % P)) % P);
+                B[i * ldb + j] = (int32_t)(uint64_t)(((u128)v * (uint64_t)inv[i]) % P);
+            }
+        }
+    } else {
+        /* rows of B are independent: x_i op(A) = alpha b_i */
+#ifdef _OPENMP
+#pragma omp parallel for schedule(dynamic, 4) num_threads(nthreads)
+#endif
+        for (int64_t i = 0; i < m; ++i) {
+            for (int64_t s = 0; s < n; ++s) {
+                const int64_t j = t_upper ? s : n - 1 - s;
+                u128 acc = (u128)al * residue(B[i * ldb + j], P);
+                u128 sub = 0;
+                const int64_t l0 = t_upper ? 0 : j + 1, l1 = t_upper ? j : n;
+                for (int64_t l = l0; l < l1; ++l)
+                    sub += (u128)(uint64_t)B[i * ldb + l] * t_elem(A, lda, tA, l, j, P);
+                const uint64_t v = (uint64_t)((acc % P + (P - sub % P)) % P);
+                B[i * ldb + j] = (int32_t)(uint64_t)(((u128)v * (uint64_t)inv[j]) % P);
+            }
+        }
+    }
+    free(inv);
     return 0;
 }
 
