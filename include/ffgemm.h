@@ -192,6 +192,35 @@ int ff_gemm_limbs(uint32_t p, int64_t m, int64_t n, int64_t k, const ff_opts *op
                   uint32_t alpha, const int8_t *A_limbs, const int8_t *B_limbs,
                   uint32_t beta, int32_t *C, int64_t ldc, void *stream);
 
+/* ---- ftrsm: triangular solve with a matrix right-hand side ---------------
+ * PAPER.md Sec. 4 (l.346-356, the BLAS trsm operation over Z/pZ) by the
+ * block recursive Algorithm 1 (l.366-384) on the tensor-core fgemm, with the
+ * nb x nb diagonal blocks inverted once so the leaves are GEMMs too
+ * (DESIGN.md §13):
+ *
+ *   side = 'L':  op(A) X = alpha B,  op(A) m x m;   side = 'R':  X op(A) = alpha B,  op(A) n x n;
+ *
+ * X (m x n) overwrites B.  op(A) = A ('N') or A^T ('T'); uplo ('U'/'L')
+ * names the triangle of A that is read -- the other one is never
+ * referenced; diag = 'U': unit diagonal, not read; 'N': the diagonal must be
+ * invertible mod p (not checked: as in BLAS, a singular A gives an
+ * undefined X).  A (lda >= max(1, dim)) and B (ldb >= max(1, n)) are dev,
+ * row-major, int32, any values (reduced mod p); A must not overlap B.
+ * Output canonical in [0, p).  Codes, BLAS order: -1 p, -2 side, -3 uplo,
+ * -4 transA, -5 diag, -6 m, -7 n, -9 A, -10 lda, -11 B, -12 ldb,
+ * -15 workspace; positive FF_ERR_*.  ff_trsm allocates its workspace
+ * (cudaMalloc/cudaFree: synchronous); ff_trsm_ex takes a caller workspace
+ * (>= ff_trsm_workspace_size bytes, 256-byte aligned) and a stream and is
+ * asynchronous. */
+int ff_trsm(uint32_t p, char side, char uplo, char transA, char diag, int64_t m, int64_t n,
+            uint32_t alpha, const int32_t *A, int64_t lda, int32_t *B, int64_t ldb);
+
+size_t ff_trsm_workspace_size(uint32_t p, char side, int64_t m, int64_t n, const ff_opts *opts);
+
+int ff_trsm_ex(uint32_t p, char side, char uplo, char transA, char diag, int64_t m, int64_t n,
+               uint32_t alpha, const int32_t *A, int64_t lda, int32_t *B, int64_t ldb,
+               const ff_opts *opts, void *workspace, size_t workspace_bytes, void *stream);
+
 /* ---- synthetic inputs (device twin of ffgen/__init__.py) -----------------
  * X[r*ld + c] = v[index0 + r*cols + c] for r < rows, c < cols, where v is the
  * (seed, stream_id) sequence of ffgen: v[i] = (mix64(key + (i+1)*GAMMA) >> 11)

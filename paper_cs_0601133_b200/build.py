@@ -1,6 +1,7 @@
 """Build the in-tree CUDA library ``lib/libffgemm.so`` for sm_100a with nvcc.
 
-Usage: ``python -m paper_cs_0601133_b200.build [--force]``.  Sources are in
+Usage: ``python paper_cs_0601133_b200/build.py [--force]`` (by path: the package
+import needs the built library).  Sources are in
 ``csrc/``; the public header is ``include/ffgemm.h`` at the repo root.
 """
 from __future__ import annotations

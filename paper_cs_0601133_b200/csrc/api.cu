@@ -134,6 +134,12 @@ int use_winograd(const Plan& pl, const ff_opts* opts, int64_t m, int64_t n, int6
     return even && winograd_auto_wins(pl, m, n, k) ? 1 : 0;
 }
 
+}  // namespace
+
+size_t gemm_ws_bytes(const Plan& pl, int64_t m, int64_t n) { return ws_bytes(pl, m, n); }
+
+namespace {
+
 // The whole path on device pointers.
 int run(const Plan& pl, char transA, char transB, int64_t m, int64_t n, int64_t k, const int32_t* A,
         int64_t lda, const int32_t* B, int64_t ldb, int32_t* C, int64_t ldc, void* ws, cudaStream_t st) {
@@ -149,6 +155,13 @@ int run(const Plan& pl, char transA, char transB, int64_t m, int64_t n, int64_t 
 }
 
 }  // namespace
+
+int gemm_dev(const Plan& pl, char transA, char transB, int64_t m, int64_t n, int64_t k, const int32_t* A,
+             int64_t lda, const int32_t* B, int64_t ldb, int32_t* C, int64_t ldc, void* ws, cudaStream_t st) {
+    return run(pl, transA, transB, m, n, k, A, lda, B, ldb, C, ldc, ws, st);
+}
+
+int check_device() { return arch_check(cur_dev()); }
 
 int num_sms() {
     const int d = cur_dev();

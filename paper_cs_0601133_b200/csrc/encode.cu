@@ -274,14 +274,30 @@ __global__ void __launch_bounds__(256) encode_crt_trans_kernel(ModP M, CrtConsts
 }
 
 // C <- beta * C mod p (k = 0 or alpha = 0); C <- 0 when beta = 0 (C not read).
-__global__ void scale_c_kernel(ModP M, int64_t m, int64_t n, int32_t* __restrict__ C, int64_t ldc) {
-    const int64_t total = m * n;
-    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-         idx += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = idx / n, j = idx - i * n;
-        int32_t* c = C + i * ldc + j;
-        *c = M.beta == 0 ? 0
-                         : static_cast<int32_t>(mulmod_shoup(residue_i32(*c, M), M.beta, M.beta_sh, M.p));
+// Rows on grid.y, 4 columns per thread (16-byte accesses when aligned).
+__global__ void __launch_bounds__(256) scale_c_kernel(ModP M, int64_t m, int64_t n, int32_t* __restrict__ C,
+                                                      int64_t ldc, int vec_ok) {
+    for (int64_t r = blockIdx.y; r < m; r += gridDim.y) {
+        int32_t* row = C + r * ldc;
+        for (int64_t c = 4 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x); c < n;
+             c += 4 * (int64_t)gridDim.x * blockDim.x) {
+            if (vec_ok && c + 4 <= n) {
+                int4 v = make_int4(0, 0, 0, 0);
+                if (M.beta != 0) {
+                    v = *reinterpret_cast<const int4*>(row + c);
+                    v.x = static_cast<int32_t>(mulmod_shoup(residue_i32(v.x, M), M.beta, M.beta_sh, M.p));
+                    v.y = static_cast<int32_t>(mulmod_shoup(residue_i32(v.y, M), M.beta, M.beta_sh, M.p));
+                    v.z = static_cast<int32_t>(mulmod_shoup(residue_i32(v.z, M), M.beta, M.beta_sh, M.p));
+                    v.w = static_cast<int32_t>(mulmod_shoup(residue_i32(v.w, M), M.beta, M.beta_sh, M.p));
+                }
+                *reinterpret_cast<int4*>(row + c) = v;
+            } else {
+                for (int64_t t = c; t < c + 4 && t < n; ++t)
+                    row[t] = M.beta == 0 ? 0
+                                         : static_cast<int32_t>(mulmod_shoup(residue_i32(row[t], M), M.beta,
+                                                                             M.beta_sh, M.p));
+            }
+        }
     }
 }
 
@@ -357,7 +373,14 @@ cudaError_t launch_encode(const Plan& pl, int kmajor_src, int64_t rows, int64_t 
 
 cudaError_t launch_scale_c(const ModP& mp, int64_t m, int64_t n, int32_t* C, int64_t ldc, cudaStream_t st) {
     if (m == 0 || n == 0) return cudaSuccess;
-    scale_c_kernel<<<grid_for(m * n, 256), 256, 0, st>>>(mp, m, n, C, ldc);
+    int gx = static_cast<int>((n + 4 * 256 - 1) / (4 * 256));
+    if (gx > 64) gx = 64;
+    int64_t gy = (int64_t)num_sms() * 8 / gx;
+    if (gy > m) gy = m;
+    if (gy > 65535) gy = 65535;
+    if (gy < 1) gy = 1;
+    const int vec_ok = ((ldc % 4) == 0 && (reinterpret_cast<uintptr_t>(C) & 15) == 0) ? 1 : 0;
+    scale_c_kernel<<<dim3(gx, static_cast<unsigned>(gy)), 256, 0, st>>>(mp, m, n, C, ldc, vec_ok);
     return cudaGetLastError();
 }
 

@@ -107,6 +107,13 @@ cudaError_t launch_fill_uniform(int32_t* X, int64_t rows, int64_t cols, int64_t 
 
 int num_sms();
 
+// api.cu: the classical device path (encode A, encode B, tcgen05 GEMM) for
+// callers inside the library (trsm.cu), and its workspace size.
+int gemm_dev(const Plan& pl, char transA, char transB, int64_t m, int64_t n, int64_t k, const int32_t* A,
+             int64_t lda, const int32_t* B, int64_t ldb, int32_t* C, int64_t ldc, void* ws, cudaStream_t st);
+size_t gemm_ws_bytes(const Plan& pl, int64_t m, int64_t n);
+int check_device();
+
 // dies.cu: SM -> die map and per-launch counter ring for the die-aware schedule
 bool die_schedule(const uint8_t** die_map, int** sched);
 

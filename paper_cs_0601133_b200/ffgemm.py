@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(_HERE, "lib", "libffgemm.so")
 if not os.path.exists(LIB_PATH):
     raise ImportError(
         "paper_cs_0601133_b200: CUDA library %s is missing; build it with "
-        "`python -m paper_cs_0601133_b200.build` (there is no CPU fallback)" % LIB_PATH)
+        "`python paper_cs_0601133_b200/build.py` (there is no CPU fallback)" % LIB_PATH)
 
 _lib = ctypes.CDLL(LIB_PATH)
 
@@ -61,6 +61,10 @@ _SIGS = {
     "ff_gemm_limbs": ([_u32, _i64, _i64, _i64, _OPTS_P, _u32, _p, _p, _u32, _p, _i64, _p],
                       ctypes.c_int),
     "ff_fill_uniform": ([_p, _i64, _i64, _i64, _u32, _u64, _u32, _i64, _p], ctypes.c_int),
+    "ff_trsm": ([_u32, _ch, _ch, _ch, _ch, _i64, _i64, _u32, _p, _i64, _p, _i64], ctypes.c_int),
+    "ff_trsm_workspace_size": ([_u32, _ch, _i64, _i64, _OPTS_P], _sz),
+    "ff_trsm_ex": ([_u32, _ch, _ch, _ch, _ch, _i64, _i64, _u32, _p, _i64, _p, _i64, _OPTS_P, _p, _sz, _p],
+                   ctypes.c_int),
 }
 for _name, (_args, _res) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -162,6 +166,22 @@ def ff_fill_uniform(X, rows, cols, ld, p, seed, stream_id, index0=0, stream=None
                                 _stream(stream)), "ff_fill_uniform")
 
 
+def ff_trsm(p, side, uplo, transA, diag, m, n, alpha, A, lda, B, ldb) -> None:
+    _check(_lib.ff_trsm(p, _tr(side), _tr(uplo), _tr(transA), _tr(diag), m, n, alpha % 2 ** 32, _ptr(A), lda,
+                        _ptr(B), ldb), "ff_trsm")
+
+
+def ff_trsm_workspace_size(p, side, m, n, opts=None) -> int:
+    return _lib.ff_trsm_workspace_size(p, _tr(side), m, n, _opts(opts))
+
+
+def ff_trsm_ex(p, side, uplo, transA, diag, m, n, alpha, A, lda, B, ldb, opts=None, workspace=None,
+               workspace_bytes=0, stream=None) -> None:
+    _check(_lib.ff_trsm_ex(p, _tr(side), _tr(uplo), _tr(transA), _tr(diag), m, n, alpha % 2 ** 32, _ptr(A),
+                           lda, _ptr(B), ldb, _opts(opts), _ptr(workspace), workspace_bytes, _stream(stream)),
+           "ff_trsm_ex")
+
+
 # ---------------------------------------------------------------- marshalling helpers
 
 def _ptr(x):
@@ -217,3 +237,22 @@ def fgemm(p: int, A, B, C=None, alpha: int = 1, beta: int = 0, transA: str = "N"
     ff_gemm_ex(p, transA, transB, m, n, k, alpha, A, _ld(A), B, _ld(B), beta, C, _ld(C), opts,
                None, 0, stream)
     return C
+
+
+def ftrsm(p: int, A, B, side: str = "L", uplo: str = "U", transA: str = "N", diag: str = "N",
+          alpha: int = 1, opts=None, stream=None):
+    """B <- X with op(A) X = alpha B (side 'L') or X op(A) = alpha B ('R'), mod p,
+    on int32 CUDA tensors (Sec. 4); the workspace is a torch tensor
+    from the caching allocator, the work runs on torch's current stream."""
+    import torch
+    m, n = B.shape
+    d = m if side in "Ll" else n
+    if A.shape[0] < d or A.shape[1] < d:
+        raise ValueError("A must be at least %d x %d" % (d, d))
+    for t in (A, B):
+        if t.dtype != torch.int32 or not t.is_cuda:
+            raise TypeError("ftrsm takes int32 CUDA tensors")
+    nbytes = ff_trsm_workspace_size(p, side, m, n, opts)
+    ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=B.device)
+    ff_trsm_ex(p, side, uplo, transA, diag, m, n, alpha, A, _ld(A), B, _ld(B), opts, ws, nbytes, stream)
+    return B
