@@ -88,6 +88,8 @@ struct GemmArgs {
     uint32_t kinv, kinv_sh;     // k-outer: 256^-(G-1) mod p
     const uint8_t* die_map;     // die-aware schedule (dies.cu): die of each %smid, or null
     int* sched;                 // per-launch counters: [0],[1] clusters per die, [2] arrivals
+    int* progress;              // throttle (FF_THROTTLE=S): tile pairs started, all clusters
+    int32_t throttle;           // slack S in tile pairs (0: off)
     int32_t crt;                // 1: groups are CRT moduli
     CrtConsts cc;
     uint8_t* scratch;           // CRT: per CTA and slot, G-1 byte planes of kCrtPlane bytes
@@ -232,7 +234,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint64_t polB = polA;
             if (a.hints & 4) { polA = ptx::policy_evict_last(); polB = ptx::policy_evict_first(); }
             if (a.hints & 8) { polA = ptx::policy_evict_first(); polB = ptx::policy_evict_last(); }
-            for_each_step(a, unit, nunits, tbase, tcount, [&](int tile, int, int g, int kb) {
+            int pair_idx = 0;
+            for_each_step(a, unit, nunits, tbase, tcount, [&](int tile, int slot, int g, int kb) {
+                if (a.throttle && leader && slot == 0 && kb == 0 && g == a.G - 1) {
+                    // soft lockstep: start tile pair j only once every cluster (on
+                    // average) has started pair j - S, so the tiles in flight stay a
+                    // compact part of the raster and share their operands in L2
+                    atomicAdd(a.progress, 1);
+                    const int need = (pair_idx + 1 - a.throttle) * nunits;
+                    if (need > 0)
+                        while (*reinterpret_cast<volatile int*>(a.progress) < need) __nanosleep(128);
+                    ++pair_idx;
+                }
                 int tm, tn;
                 tile_coords(a, tile, tm, tn);
                 const int arow = tm * K::BM + static_cast<int>(rank) * 128;
@@ -610,6 +623,20 @@ int launch_impl(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A
     for (int w = 0; w < I.groups; ++w) {
         a.group_first[w] = static_cast<int8_t>(pl.group_first[w]);
         a.group_len[w] = static_cast<int8_t>(pl.group_len[w]);
+    }
+    a.throttle = 0;
+    a.progress = nullptr;
+    if (const char* e = getenv("FF_THROTTLE")) {        // experiment: soft lockstep of the clusters
+        static int* ring = nullptr;
+        static unsigned slot = 0;
+        if (!ring && cudaMalloc(&ring, 4096 * sizeof(int)) != cudaSuccess) ring = nullptr;
+        if (ring && atoi(e) > 0) {
+            int* c = ring + (slot++ % 4096);
+            if (cudaMemsetAsync(c, 0, sizeof(int), st) == cudaSuccess) {
+                a.progress = c;
+                a.throttle = atoi(e);
+            }
+        }
     }
     a.crt = pl.crt ? 1 : 0;
     a.cc = pl.cc;
