@@ -70,6 +70,13 @@ extern "C" {
 #define FF_SCHEME_T 2
 #define FF_SCHEME_CRT 3
 #define FF_MAX_MODULI 16
+/* FP64: the paper-literal "Zpz-double" engine: centred
+ * residues as doubles on the fp64 tensor cores (DMMA), lambda products
+ * accumulated exactly between floating-point reductions, lambda from Eq. (2)
+ * with gamma = 53.  Only when chosen explicitly; needs lambda >= 4, i.e.
+ * p <= 2^26 + 1 (the paper's feasibility bound, l.882).  Not available for
+ * ff_encode / ff_gemm_limbs / ff_gemm_host / Winograd (FF_ERR_OPTS). */
+#define FF_SCHEME_FP64 4
 
 /* Options for the _ex / split entry points.  Zero-initialise and set fields;
  * a NULL pointer means all defaults. */
@@ -90,7 +97,10 @@ typedef struct ff_opts {
     int32_t korder;         /* step order of the kernel: 0 auto, 1 group-outer (each weight
                                group over all of k), 2 k-outer (each k-block through all
                                groups: L2 locality) */
-    int32_t reserved[4];
+    int32_t debug_unchecked_kb; /* test builds only: accept a kb_override above the safe
+                               bound (to show that the bound is needed); results are then
+                               not guaranteed */
+    int32_t reserved[3];
 } ff_opts;
 
 /* The plan the library derives from (p, k, opts): host-only, no GPU needed. */
@@ -98,7 +108,7 @@ typedef struct ff_plan_info {
     uint32_t p;
     int32_t L;               /* int8 planes per operand: limbs (1..4) or, for
                                 FF_SCHEME_CRT, moduli (2..FF_MAX_MODULI) */
-    int32_t scheme;          /* FF_SCHEME_S, FF_SCHEME_T or FF_SCHEME_CRT */
+    int32_t scheme;          /* FF_SCHEME_S, FF_SCHEME_T, FF_SCHEME_CRT or FF_SCHEME_FP64 */
     int32_t groups;          /* accumulation groups: 2L-1 weight groups w = i+j
                                 (limbs) or L moduli (CRT) */
     int32_t limb_signed[4];  /* 1 if limb i is s8, 0 if u8 (limb schemes) */

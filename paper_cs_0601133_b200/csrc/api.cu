@@ -116,6 +116,7 @@ bool winograd_auto_wins(const Plan& pl, int64_t m, int64_t n, int64_t k) {
 }
 
 size_t ws_bytes(const Plan& pl, int64_t m, int64_t n) {
+    if (pl.fp64) return f64_ws_bytes(pl, m, n);
     const size_t L = static_cast<size_t>(pl.info.L), kp = static_cast<size_t>(pl.info.k_pad);
     return align256(L * static_cast<size_t>(m) * kp) + align256(L * static_cast<size_t>(n) * kp) +
            align256(crt_scratch_bytes(pl));
@@ -128,6 +129,7 @@ int cuda_rc(cudaError_t e) { return e == cudaSuccess ? 0 : FF_ERR_CUDA; }
 // or FF_ERR_OPTS (forced but the shape is not even).
 int use_winograd(const Plan& pl, const ff_opts* opts, int64_t m, int64_t n, int64_t k) {
     const int w = opts ? opts->winograd : 0;
+    if (pl.fp64) return w == 1 ? -FF_ERR_OPTS : 0;     // the fp64 engine is classical only
     const bool even = (m % 2 == 0) && (n % 2 == 0) && (k % 2 == 0) && m >= 512 && n >= 512 && k >= 256;
     if (w == 1) return even ? 1 : -FF_ERR_OPTS;
     if (w < 0) return 0;
@@ -144,6 +146,7 @@ namespace {
 int run(const Plan& pl, char transA, char transB, int64_t m, int64_t n, int64_t k, const int32_t* A,
         int64_t lda, const int32_t* B, int64_t ldb, int32_t* C, int64_t ldc, void* ws, cudaStream_t st) {
     if (k == 0 || pl.mp.alpha == 0) return cuda_rc(launch_scale_c(pl.mp, m, n, C, ldc, st));
+    if (pl.fp64) return run_f64(pl, is_t(transA), is_t(transB), m, n, k, A, lda, B, ldb, C, ldc, ws, st);
     int8_t* al = static_cast<int8_t*>(ws);
     int8_t* bl = al + align256(static_cast<size_t>(pl.info.L) * m * pl.info.k_pad);
     int8_t* scratch = bl + align256(static_cast<size_t>(pl.info.L) * n * pl.info.k_pad);
@@ -301,6 +304,7 @@ int ff_gemm_host(uint32_t p, char transA, char transB, int64_t m, int64_t n, int
     Plan pl;
     e = make_plan(p, k, opts, &pl);
     if (e) return e;
+    if (pl.fp64) return FF_ERR_OPTS;                 // the fp64 engine has no host pipeline
     if (opts && opts->host_block < 0) return FF_ERR_OPTS;
     set_scalars(&pl, alpha, beta);
     const int dev = cur_dev();
@@ -449,6 +453,7 @@ int ff_encode(uint32_t p, int64_t k, const ff_opts* opts, int kmajor_src, int64_
     Plan pl;
     int e = make_plan(p, k, opts, &pl);
     if (e) return e;
+    if (pl.fp64) return FF_ERR_OPTS;                 // int8 planes only
     e = arch_check(cur_dev());
     if (e) return e;
     return cuda_rc(launch_encode(pl, kmajor_src, rows, k, X, ldx, limbs, static_cast<cudaStream_t>(stream)));
@@ -469,6 +474,7 @@ int ff_gemm_limbs(uint32_t p, int64_t m, int64_t n, int64_t k, const ff_opts* op
     Plan pl;
     int e = make_plan(p, k, opts, &pl);
     if (e) return e;
+    if (pl.fp64) return FF_ERR_OPTS;                 // int8 planes only
     set_scalars(&pl, alpha, beta);
     e = arch_check(cur_dev());
     if (e) return e;

@@ -56,6 +56,7 @@ struct Plan {
     ff_plan_info info;
     ModP mp;
     bool crt;                        // FF_SCHEME_CRT: groups are moduli, one pair (i, i) each
+    bool fp64;                       // FF_SCHEME_FP64: the paper-literal DMMA engine (gemm_f64.cu)
     CrtConsts cc;
     int npairs;                      // L*L (limbs) or L (CRT)
     int pair_i[kMaxPairs];
@@ -99,6 +100,11 @@ int launch_gemm_tc(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t
 size_t winograd_ws_bytes(const Plan& half, int64_t m, int64_t n, int64_t k);
 int run_winograd(const Plan& half, bool transA, bool transB, int64_t m, int64_t n, int64_t k, const int32_t* A,
                  int64_t lda, const int32_t* B, int64_t ldb, int32_t* C, int64_t ldc, void* ws, cudaStream_t st);
+
+// gemm_f64.cu: the paper-literal fp64 engine (workspace = two double planes)
+size_t f64_ws_bytes(const Plan& pl, int64_t m, int64_t n);
+int run_f64(const Plan& pl, bool transA, bool transB, int64_t m, int64_t n, int64_t k, const int32_t* A,
+            int64_t lda, const int32_t* B, int64_t ldb, int32_t* C, int64_t ldc, void* ws, cudaStream_t st);
 
 // gen.cu
 cudaError_t launch_fill_uniform(int32_t* X, int64_t rows, int64_t cols, int64_t ld, uint32_t p,

@@ -180,6 +180,41 @@ int make_crt_plan(uint32_t p, int64_t k, const ff_opts& o, int64_t cmax, Plan& p
     return 0;
 }
 
+// The paper-literal fp64 engine: Eq. (2) with gamma = 53,
+// lambda ((p-1)/2)^2 < 2^52, lambda >= 4 (one DMMA k-step);
+// the accumulator also carries one reduced value (|r| <= p), which the factor-2
+// headroom of 2^52 < 2^53 covers.  kb is a multiple of 4 (the DMMA k).
+int make_f64_plan(int64_t k, const ff_opts& o, int64_t cmax, Plan& pl) {
+    ff_plan_info& I = pl.info;
+    const int64_t c2 = cmax * cmax;
+    const int64_t lam = c2 > 0 ? ((((int64_t)1) << 52) - 1) / c2 : ((int64_t)1 << 40);
+    if (lam < 4) return FF_ERR_OPTS;
+    pl.fp64 = true;
+    I.scheme = FF_SCHEME_FP64;
+    I.L = 1;
+    I.groups = 1;
+    I.digit_max[0] = (int32_t)cmax;
+    I.limb_signed[0] = 1;
+    I.group_bound[0] = c2;
+    I.group_bound_max = c2;
+    I.carry_max = 2 * cmax + 1;
+    I.kb_max = lam;
+    int64_t kb = lam;
+    if (o.kb_override > 0) {
+        if ((o.kb_override > lam && !o.debug_unchecked_kb) || o.kb_override < 4) return FF_ERR_OPTS;
+        kb = o.kb_override;
+    }
+    kb = (kb / 4) * 4;
+    if (kb > ((int64_t)1 << 30)) kb = (int64_t)1 << 30;
+    I.kb = kb;
+    I.k_pad = (k + 15) / 16 * 16;
+    I.num_kblocks = k > 0 ? (k + kb - 1) / kb : 0;
+    pl.korder = 1;
+    I.korder = 1;
+    pl.npairs = 0;
+    return 0;
+}
+
 // Limb schemes S / T: digit bounds, group bounds, the
 // Eq. (2) k-block and the (i, j) pairs of each weight group.
 int make_limb_plan(uint32_t p, int64_t k, const ff_opts& o, int64_t half, int64_t neg, int64_t cmax, int scheme,
@@ -269,7 +304,7 @@ int make_plan(uint32_t p, int64_t k, const ff_opts* opts, Plan* out) {
     ff_opts o;
     std::memset(&o, 0, sizeof(o));
     if (opts) o = *opts;
-    if (o.scheme < FF_SCHEME_AUTO || o.scheme > FF_SCHEME_CRT) return FF_ERR_OPTS;
+    if (o.scheme < FF_SCHEME_AUTO || o.scheme > FF_SCHEME_FP64) return FF_ERR_OPTS;
     if (o.winograd < -1 || o.winograd > 1) return FF_ERR_OPTS;
     if (o.kb_override < 0) return FF_ERR_OPTS;
     if (o.cta_group < 0 || o.cta_group > 2) return FF_ERR_OPTS;
@@ -303,9 +338,13 @@ int make_plan(uint32_t p, int64_t k, const ff_opts* opts, Plan* out) {
         const int e = make_crt_plan(p, k, o, cmax, pl);
         if (e) return e;
     }
+    if (scheme == FF_SCHEME_FP64) {
+        const int e = make_f64_plan(k, o, cmax, pl);
+        if (e) return e;
+    }
     const int L = scheme == FF_SCHEME_S ? LS : scheme == FF_SCHEME_T ? LT : 0;
     bool int_wb = false;
-    if (scheme != FF_SCHEME_CRT) {
+    if (scheme == FF_SCHEME_S || scheme == FF_SCHEME_T) {
         const int e = make_limb_plan(p, k, o, half, neg, cmax, scheme, L, pl, int_wb);
         if (e) return e;
     }

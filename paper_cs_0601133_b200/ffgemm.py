@@ -22,7 +22,7 @@ if not os.path.exists(LIB_PATH):
 _lib = ctypes.CDLL(LIB_PATH)
 
 FF_OK, FF_ERR_CUDA, FF_ERR_NOMEM, FF_ERR_ARCH, FF_ERR_OPTS, FF_ERR_INTERNAL = 0, 1, 2, 3, 4, 5
-FF_SCHEME_AUTO, FF_SCHEME_S, FF_SCHEME_T, FF_SCHEME_CRT = 0, 1, 2, 3
+FF_SCHEME_AUTO, FF_SCHEME_S, FF_SCHEME_T, FF_SCHEME_CRT, FF_SCHEME_FP64 = 0, 1, 2, 3, 4
 FF_MAX_MODULI = 16
 
 _i32, _i64, _u32, _u64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, ctypes.c_uint64
@@ -32,7 +32,7 @@ _p, _ch, _sz = ctypes.c_void_p, ctypes.c_char, ctypes.c_size_t
 class ff_opts(ctypes.Structure):
     _fields_ = [("winograd", _i32), ("scheme", _i32), ("kb_override", _i64),
                 ("debug_saturate", _i32), ("cta_group", _i32), ("host_block", _i32),
-                ("korder", _i32), ("reserved", _i32 * 4)]
+                ("korder", _i32), ("debug_unchecked_kb", _i32), ("reserved", _i32 * 3)]
 
 
 class ff_plan_info(ctypes.Structure):
@@ -116,7 +116,7 @@ def ff_plan_query(p: int, k: int, opts=None) -> dict:
     info = ff_plan_info()
     _check(_lib.ff_plan_query(p, k, _opts(opts), ctypes.byref(info)), "ff_plan_query")
     L, G = info.L, info.groups
-    return {"p": info.p, "L": L, "scheme": {1: "S", 2: "T", 3: "CRT"}[info.scheme], "groups": G,
+    return {"p": info.p, "L": L, "scheme": {1: "S", 2: "T", 3: "CRT", 4: "FP64"}[info.scheme], "groups": G,
             "limb_signed": list(info.limb_signed[:min(L, 4)]), "digit_max": list(info.digit_max[:min(L, 4)]),
             "group_bound": list(info.group_bound[:min(G, 7)]), "group_bound_max": info.group_bound_max,
             "kb_max": info.kb_max, "kb": info.kb, "k_pad": info.k_pad,

@@ -189,3 +189,18 @@ def test_kb_override_rules(ff):
         ff.ff_plan_query(65521, 5000, {"kb_override": 40000})   # above the safe bound
     with pytest.raises(ff.FFError):
         ff.ff_plan_query(65521, 5000, {"kb_override": 64})      # below one stage
+
+
+def test_f64_plan_is_paper_eq2(ff):
+    """The fp64 engine's lambda is Eq. (2) with gamma = 53,
+    SURVEY §8(f) NEXT-3: 4196352 (p = 65521), 256 (8388593), 4 (67108859)."""
+    from oracle import bounds
+    for p, lam in [(65521, 4196352), (8388593, 256), (67108859, 4)]:
+        info = ff.ff_plan_query(p, 1000, {"scheme": 4})
+        assert info["scheme"] == "FP64" and info["kb_max"] == lam
+        assert lam == bounds.lambda_dot(p, 53, balanced=True)
+        assert info["kb"] == lam // 4 * 4 and info["kb"] % 4 == 0
+    with pytest.raises(ff.FFError):
+        ff.ff_plan_query(2 ** 27 - 39, 10, {"scheme": 4})       # lambda < 4: beyond the paper's 2^26 bound
+    with pytest.raises(ff.FFError):
+        ff.ff_plan_query(65521, 10, {"scheme": 4, "kb_override": 2 ** 23})
