@@ -60,6 +60,8 @@ def _load():
         lib.oracle_trsm.argtypes = [_u32, _char, _char, _char, _char, _i64, _i64, _u32, _p, _i64,
                                     _p, _i64, ctypes.c_int]
         lib.oracle_trsm.restype = ctypes.c_int
+        lib.oracle_rank_det.argtypes = [_u32, _i64, _i64, _p, _i64, _p, _p]
+        lib.oracle_rank_det.restype = ctypes.c_int
         _lib = lib
     return _lib
 
@@ -160,3 +162,21 @@ def trsm(p: int, side: str, uplo: str, transA: str, diag: str, alpha: int, A: np
     if e:
         raise MemoryError("oracle_trsm")
     return X
+
+
+def rank_det(p: int, X: np.ndarray):
+    """(rank, det) of X over Z/pZ by plain Gaussian elimination (det is None
+    unless X is square).  PAPER.md Sec. 6 (l.655-657)."""
+    lib = _load()
+    X = _c32(X)
+    m, n = X.shape
+    r = ctypes.c_int64(0)
+    d = ctypes.c_int64(-1)
+    e = lib.oracle_rank_det(p, m, n, _ptr(X), _ld(X), ctypes.byref(r), ctypes.byref(d))
+    if e < 0:
+        raise ValueError("oracle_rank_det argument %d invalid" % -e)
+    if e == 1:
+        raise ZeroDivisionError("oracle_rank_det: pivot not invertible (p not prime)")
+    if e:
+        raise MemoryError("oracle_rank_det")
+    return r.value, (d.value if m == n else None)

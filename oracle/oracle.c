@@ -288,6 +288,58 @@ int oracle_trsm(uint32_t p, char side, char uplo, char transA, char diag, int64_
     return 0;
 }
 
+/* ------------------------------------------------------------------------
+ * rank and determinant over Z/pZ (Sec. 6, l.655-657: "the rank is
+ * the number of non-zero rows in U; the determinant is the product of the
+ * diagonal elements of U"), by plain Gaussian elimination: for each column,
+ * the first row (from the current one down) with a non-zero entry is the
+ * pivot; rows are swapped (each swap flips the sign of the determinant) and
+ * the rows below are eliminated.  X (m x n, row-major, ld) is copied, never
+ * modified.  Returns 0, -i for an invalid argument i, 1 if a pivot is not
+ * invertible mod p (p not prime), 2 on allocation failure.  det is written
+ * only for m == n (0 when singular).
+ * ------------------------------------------------------------------------ */
+int oracle_rank_det(uint32_t p, int64_t m, int64_t n, const int32_t *X, int64_t ld,
+                    int64_t *rank_out, int64_t *det_out)
+{
+    if (p < 2 || p >= (1u << 31)) return -1;
+    if (m < 0) return -2;
+    if (n < 0) return -3;
+    if (ld < (n > 1 ? n : 1)) return -5;
+    const int64_t P = (int64_t)p;
+    uint64_t *a = (uint64_t *)malloc((size_t)(m * n > 0 ? m * n : 1) * sizeof(uint64_t));
+    if (!a) return 2;
+    for (int64_t i = 0; i < m; ++i)
+        for (int64_t j = 0; j < n; ++j) a[i * n + j] = residue(X[i * ld + j], P);
+    int64_t r = 0;
+    uint64_t det = 1;
+    int neg = 0;
+    for (int64_t col = 0; col < n && r < m; ++col) {
+        int64_t piv = -1;
+        for (int64_t i = r; i < m; ++i)
+            if (a[i * n + col]) { piv = i; break; }
+        if (piv < 0) { det = 0; continue; }
+        if (piv != r) {
+            for (int64_t j = 0; j < n; ++j) { uint64_t t = a[r * n + j]; a[r * n + j] = a[piv * n + j]; a[piv * n + j] = t; }
+            neg ^= 1;
+        }
+        const int64_t iv = inv_mod(a[r * n + col], P);
+        if (iv < 0) { free(a); return 1; }
+        det = (uint64_t)(((u128)det * a[r * n + col]) % P);
+        for (int64_t i = r + 1; i < m; ++i) {
+            const uint64_t f = (uint64_t)(((u128)a[i * n + col] * (uint64_t)iv) % P);
+            if (!f) continue;
+            for (int64_t j = col; j < n; ++j)
+                a[i * n + j] = (uint64_t)((a[i * n + j] + (u128)(P - f) * a[r * n + j]) % P);
+        }
+        ++r;
+    }
+    if (rank_out) *rank_out = r;
+    if (det_out && m == n) *det_out = (r < m) ? 0 : (int64_t)(neg && det ? P - det : det);
+    free(a);
+    return 0;
+}
+
 int oracle_max_threads(void)
 {
 #ifdef _OPENMP

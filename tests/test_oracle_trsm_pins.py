@@ -209,3 +209,68 @@ def test_dot_product_and_winograd_bounds():
     p, g = 65521, 53
     kw = bounds.k_winograd(p, g, 1)
     assert 4 * ((kw - 1) // 2) * (p - 1) ** 2 < 2 ** (g + 2) * 2 // 2
+
+
+# ---------------------------------------------------------------- rank / det oracle (Sec. 6)
+
+def _span_size(rows, p):
+    """|row space| by enumerating every linear combination (tiny cases only)."""
+    n = len(rows[0]) if rows else 0
+    seen = set()
+    for coeffs in itertools.product(range(p), repeat=len(rows)):
+        v = tuple(sum(c * r[j] for c, r in zip(coeffs, rows)) % p for j in range(n))
+        seen.add(v)
+    return len(seen)
+
+
+def _leibniz_det(M, p):
+    n = len(M)
+    tot = 0
+    for perm in itertools.permutations(range(n)):
+        inv = sum(1 for i in range(n) for j in range(i + 1, n) if perm[i] > perm[j])
+        term = 1
+        for i in range(n):
+            term *= M[i][perm[i]]
+        tot += -term if inv % 2 else term
+    return tot % p
+
+
+@pytest.mark.parametrize("p", [2, 3, 5])
+def test_rank_det_brute_force(p):
+    """rank = log_p |row space| (enumerated); det = Leibniz's permutation sum."""
+    rng = np.random.default_rng(p)
+    for trial in range(60):
+        m, n = int(rng.integers(1, 4)), int(rng.integers(1, 5))
+        X = rng.integers(0, p, size=(m, n))
+        if trial % 3 == 0 and m > 1:
+            X[-1] = (X[0] * int(rng.integers(0, p))) % p       # a dependent row
+        r, d = oracle.rank_det(p, X.astype(np.int32))
+        assert p ** r == _span_size(X.tolist(), p)
+        if m == n:
+            assert d == _leibniz_det(X.tolist(), p)
+        else:
+            assert d is None
+
+
+@pytest.mark.parametrize("p", [65521, 8388593, 2 ** 31 - 1])
+def test_rank_det_structured(p):
+    rng = np.random.default_rng(p % 997)
+    n = 40
+    assert oracle.rank_det(p, np.eye(n, dtype=np.int32)) == (n, 1)
+    assert oracle.rank_det(p, np.zeros((n, n + 3), np.int32))[0] == 0
+    # det of a product is the product of dets; det of a triangular matrix is its diagonal product
+    U = np.triu(rng.integers(0, p, size=(n, n))).astype(np.int64)
+    U[np.arange(n), np.arange(n)] = rng.integers(1, p, size=n)
+    dU = 1
+    for i in range(n):
+        dU = dU * int(U[i, i]) % p
+    assert oracle.rank_det(p, U.astype(np.int32))[1] == dU
+    # a row swap flips the sign; rank of an outer product u v^T (u, v != 0) is 1
+    S = U.copy()
+    S[[0, 5]] = S[[5, 0]]
+    assert oracle.rank_det(p, S.astype(np.int32))[1] == (p - dU) % p
+    u = rng.integers(1, p, size=(n, 1))
+    v = rng.integers(1, p, size=(1, n + 7))
+    assert oracle.rank_det(p, ((u * v) % p).astype(np.int32))[0] == 1
+    # non-canonical input is reduced
+    assert oracle.rank_det(p, (U.astype(np.int64) - p).astype(np.int32))[1] == dU
