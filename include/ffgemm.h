@@ -231,6 +231,38 @@ int ff_trsm_ex(uint32_t p, char side, char uplo, char transA, char diag, int64_t
                uint32_t alpha, const int32_t *A, int64_t lda, int32_t *B, int64_t ldb,
                const ff_opts *opts, void *workspace, size_t workspace_bytes, void *stream);
 
+/* ---- LQUP, rank, determinant -----------------------------------------------
+ * The rank-revealing triangular factorization of PAPER.md Sec. 5.1 (l.575-590)
+ * reduced to the tensor-core fgemm, returned in place in the
+ * PLUQ arrangement (reading R20): with Q[i] = the original row now at row i
+ * and P[j] = the original column now at column j,
+ *     A[Q[i]][P[j]] = sum_{k < r} L[i][k] U[k][j]  (mod p),
+ * L (m x r) unit lower triangular, stored strictly below the diagonal of the
+ * first r columns of A; U (r x n) upper triangular with a non-zero diagonal,
+ * stored on and above the diagonal of the first r rows; rows >= r hold their
+ * L entries and zeros.  Pivoting: the first non-zero entry of each row (rows in
+ * order), so the pivot columns are the row-echelon pivots.  A: dev, int32,
+ * any values (reduced mod p), lda >= max(1, n).  Q (m), P (n), rank: HOST
+ * outputs.  Synchronous (the host needs each panel's rank).  p prime (pivots
+ * are inverted).  Codes: -1 p, -2 m, -3 n, -4 A, -5 lda, -6 Q, -7 P, -8 rank,
+ * -10 workspace.  ff_lqup allocates its workspace; ff_lqup_ex takes one
+ * (>= ff_lqup_workspace_size bytes, 256-byte aligned) and a stream. */
+int ff_lqup(uint32_t p, int64_t m, int64_t n, int32_t *A, int64_t lda, int64_t *Q, int64_t *P,
+            int64_t *rank);
+
+size_t ff_lqup_workspace_size(uint32_t p, int64_t m, int64_t n, const ff_opts *opts);
+
+int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t *A, int64_t lda, int64_t *Q, int64_t *P,
+               int64_t *rank, const ff_opts *opts, void *workspace, size_t workspace_bytes, void *stream);
+
+/* Rank (and, for m == n, the determinant in [0, p)) of A (dev, not modified),
+ * PAPER.md Sec. 6 (l.655-657): "the rank is the number of non-zero rows in U;
+ * the determinant is the product of the diagonal elements of U" (times the
+ * signs of the permutations).  det may be NULL.  Codes: -1 p, -2 m, -3 n, -4 A,
+ * -5 lda, -6 rank, -7 det requested for m != n. */
+int ff_rank_det(uint32_t p, int64_t m, int64_t n, const int32_t *A, int64_t lda, int64_t *rank,
+                uint32_t *det);
+
 /* ---- synthetic inputs (device twin of ffgen/__init__.py) -----------------
  * X[r*ld + c] = v[index0 + r*cols + c] for r < rows, c < cols, where v is the
  * (seed, stream_id) sequence of ffgen: v[i] = (mix64(key + (i+1)*GAMMA) >> 11)

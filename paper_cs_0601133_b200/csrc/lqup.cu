@@ -1,0 +1,531 @@
+// lqup.cu -- rank-revealing triangular factorization on the tensor-core fgemm
+// (Sec. 5.1, l.575-590), with rank and
+// determinant (Sec. 6, l.655-657).
+//
+// The paper's LQUP (A = L Q U P, after Ibarra-Moran-Hui) recurses on row
+// halves and reduces to trsm + fgemm.  On the B200 the same reduction is done
+// right-looking by panels of kH rows, because the GPU pays per
+// launch and per pivot decision, not per flop:
+//   1. panel kernel (one CTA): factor the kH panel rows restricted to a column
+//      window [c, c+W) with "first non-zero in the row" pivoting (column swaps),
+//      in a workspace copy; it also inverts the panel's L11 (unit lower) and
+//      U11 (upper).  If a panel row has no pivot inside the window the window
+//      is widened (ultimately to all remaining columns) and the panel redone.
+//   2. U of the pivot rows beyond the window: U_rest = L11^-1 A_rest  (fgemm).
+//   3. trailing rows: G = X U11^-1 (their L entries, fgemm), Z <- Z - G U12 (fgemm,
+//      alpha = p-1, beta = 1) -- the paper's "GT = X via trsm ... Z = Z - GY".
+//   4. rows that reduced to zero (rank deficiency) move to the bottom.
+// Output, in place: with the row permutation Q (rows Q[0..m) of A) and column
+// permutation P (columns P[0..n)),  (QAP)[i][j] = sum_k L[i][k] U[k][j],  L unit
+// lower (m x r, stored strictly below the diagonal of the first r columns), U
+// upper (r x n, on and above the diagonal of the first r rows); rows >= r hold
+// only their L entries (zeros elsewhere).  This is the "PLUQ" arrangement of the
+// paper's LQUP (reading R20).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "internal.h"
+#include "modp.cuh"
+
+namespace ff {
+
+namespace {
+
+constexpr int kH = 128;          // panel rows
+constexpr int kThr = 1024;
+constexpr int kMaxSwaps = 2 * kH;
+constexpr int kSmemBytes = kH * kH * 8;   // the window in shared memory (doubles)
+
+int fail_cuda_now() {
+    cudaGetLastError();
+    return FF_ERR_CUDA;
+}
+
+struct PanelArgs {
+    int32_t* A;
+    int64_t lda;
+    int64_t i0, hr;              // panel rows [i0, i0 + hr)
+    int64_t c, W;                // window columns [c, c + W)
+    int32_t full;                // 1: the window reaches the last column (zero rows allowed)
+    uint32_t p;
+    double dp, invp;             // p, fl(1/p)
+    double* win;                 // workspace hr x W (ld W): the window, residues as exact doubles
+    int32_t* Linv;               // kH x kH
+    int32_t* Uinv;               // kH x kH
+    double* tmp;                 // kH x kH scratch for the inverses
+    int32_t* out;                // [0] kk, [1] fail, [2] ncol, [3] nrow, then col swaps (a,b)..., row swaps (a,b)...
+};
+
+// a b mod p for residues a, b < p < 2^31 held as doubles: the product is split
+// exactly (hi + lo, fma), the quotient estimated with the fp reciprocal (the
+// paper's "floating point inverse": off by at most one),
+// and corrected.  No integer<->float conversions.
+__device__ __forceinline__ double mulm(double a, double b, double p, double invp) {
+    const double hi = a * b;
+    const double lo = fma(a, b, -hi);
+    const double q = rint(hi * invp);
+    double r = fma(-q, p, hi) + lo;
+    if (r < 0) r += p;
+    if (r >= p) r -= p;
+    return r;
+}
+__device__ __forceinline__ double subm(double x, double t, double p) {
+    const double r = x - t;
+    return r < 0 ? r + p : r;
+}
+
+// a^-1 mod p by the extended Euclid algorithm in 32-bit integers (p < 2^31:
+// remainders < 2^31, Bezout coefficients |s| < p); on the panel's critical path.
+__device__ uint32_t inv_dev(uint32_t a, uint32_t p) {
+    int32_t r0 = static_cast<int32_t>(p), r1 = static_cast<int32_t>(a), s0 = 0, s1 = 1;
+    while (r1 != 0) {
+        const int32_t q = r0 / r1, t = r0 - q * r1, u = s0 - q * s1;
+        r0 = r1; r1 = t; s0 = s1; s1 = u;
+    }
+    return static_cast<uint32_t>(s0 < 0 ? s0 + static_cast<int32_t>(p) : s0);
+}
+
+// One CTA of 32 x 32 threads factors the panel window (see the file header).
+// kSmem: the window (<= kH x kH doubles, 128 KB) lives in shared memory (the
+// generic case); otherwise in the global workspace (widened windows).
+template <bool kSmem>
+__global__ void __launch_bounds__(kThr) panel_kernel(PanelArgs P) {
+    extern __shared__ double dyn_smem[];
+    __shared__ int s_j;
+    __shared__ double s_inv;
+    __shared__ int s_ncol, s_nrow, s_kk, s_fail;
+    __shared__ int colsw[kMaxSwaps][2];
+    __shared__ int rowsw[kMaxSwaps][2];
+    __shared__ double dinv[kH];                    // inverses of the pivots (U11's diagonal)
+    const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+    const int64_t hr = P.hr, W = P.W;
+    const double p = P.dp, invp = P.invp;
+    double* w = kSmem ? dyn_smem : P.win;
+    // copy in (canonical residues)
+    for (int64_t r = ty; r < hr; r += 32)
+        for (int64_t cc = tx; cc < W; cc += 32) {
+            const int64_t v = static_cast<int64_t>(P.A[(P.i0 + r) * P.lda + P.c + cc]) % static_cast<int64_t>(P.p);
+            w[r * W + cc] = static_cast<double>(v < 0 ? v + P.p : v);
+        }
+    if (tid == 0) { s_ncol = 0; s_nrow = 0; s_kk = 0; s_fail = 0; }
+    __syncthreads();
+    for (int64_t i = 0; i < hr; ++i) {
+        const int kk = s_kk;
+        if (tid == 0) s_j = INT32_MAX;
+        __syncthreads();
+        // first non-zero of row i in columns [kk, W)
+        for (int64_t cc = kk + tid; cc < W; cc += kThr)
+            if (w[i * W + cc] != 0.0) atomicMin(&s_j, static_cast<int>(cc));
+        __syncthreads();
+        const int j = s_j;
+        if (j == INT32_MAX) {                      // no pivot in the window
+            if (!P.full) { if (tid == 0) s_fail = 1; __syncthreads(); break; }
+            __syncthreads();
+            continue;                              // a zero row (stays below the pivot rows)
+        }
+        // column swap kk <-> j (all panel rows), row swap i <-> kk
+        if (j != kk) {
+            for (int64_t r = tid; r < hr; r += kThr) {
+                const double t = w[r * W + kk]; w[r * W + kk] = w[r * W + j]; w[r * W + j] = t;
+            }
+            if (tid == 0) { colsw[s_ncol][0] = kk; colsw[s_ncol][1] = j; ++s_ncol; }
+        }
+        __syncthreads();
+        if (i != kk) {
+            for (int64_t cc = tid; cc < W; cc += kThr) {
+                const double t = w[i * W + cc]; w[i * W + cc] = w[kk * W + cc]; w[kk * W + cc] = t;
+            }
+            if (tid == 0) { rowsw[s_nrow][0] = kk; rowsw[s_nrow][1] = static_cast<int>(i); ++s_nrow; }
+            __syncthreads();
+        }
+        if (tid == 0) {
+            s_inv = static_cast<double>(inv_dev(static_cast<uint32_t>(w[kk * W + kk]), P.p));
+            dinv[kk] = s_inv;
+        }
+        __syncthreads();
+        // eliminate the unprocessed rows i+1..hr-1 (the zero rows kk+1..i are zero from kk on):
+        // multipliers (column kk), then columns kk+1..W-1
+        const double inv = s_inv;
+        for (int64_t r = i + 1 + tid; r < hr; r += kThr) w[r * W + kk] = mulm(w[r * W + kk], inv, p, invp);
+        __syncthreads();
+        for (int64_t r = i + 1 + ty; r < hr; r += 32) {
+            const double f = w[r * W + kk];
+            if (f == 0.0) continue;
+            for (int64_t cc = kk + 1 + tx; cc < W; cc += 32)
+                w[r * W + cc] = subm(w[r * W + cc], mulm(f, w[kk * W + cc], p, invp), p);
+        }
+        if (tid == 0) s_kk = kk + 1;
+        __syncthreads();
+    }
+    const int kk = s_kk;
+    if (!s_fail) {
+        // Linv = L11^-1 (unit lower) and Uinv = U11^-1 (upper) by row sweeps;
+        // 8 threads per column share each dot product (shuffle-reduced).
+        double* T = P.tmp;                              // rows of the inverse being built (kH x kH)
+        const int jj = tid >> 3, part = tid & 7;
+        auto dot8 = [&](double s) {                     // sum over the 8 lanes of a column group, mod p
+            for (int o = 4; o > 0; o >>= 1) {
+                const double t = __shfl_down_sync(0xffffffffu, s, o, 8);
+                s = s + t;
+                if (s >= p) s -= p;
+            }
+            return __shfl_sync(0xffffffffu, s, 0, 8);
+        };
+        for (int i = 0; i < kk; ++i) {                  // Linv_i = e_i - sum_{jj<=l<i} L_il Linv_l
+            double s = 0.0;
+            if (jj < i)
+                for (int l = jj + part; l < i; l += 8) {
+                    s += mulm(w[i * W + l], T[l * kH + jj], p, invp);
+                    if (s >= p) s -= p;
+                }
+            s = dot8(s);
+            if (part == 0 && jj < kk) T[i * kH + jj] = (jj == i) ? 1.0 : (jj < i ? (s == 0.0 ? 0.0 : p - s) : 0.0);
+            __syncthreads();
+        }
+        for (int64_t e = tid; e < static_cast<int64_t>(kk) * kk; e += kThr)
+            P.Linv[(e / kk) * kH + e % kk] = static_cast<int32_t>(T[(e / kk) * kH + e % kk]);
+        __syncthreads();
+        for (int i = kk - 1; i >= 0; --i) {             // Uinv_i = (e_i - sum_{i<l<=jj} U_il Uinv_l) / U_ii
+            double s = 0.0;
+            if (jj > i && jj < kk)
+                for (int l = i + 1 + part; l <= jj; l += 8) {
+                    s += mulm(w[i * W + l], T[l * kH + jj], p, invp);
+                    if (s >= p) s -= p;
+                }
+            s = dot8(s);
+            __syncthreads();
+            if (part == 0 && jj < kk) {
+                double v = 0.0;
+                if (jj >= i) v = mulm(jj == i ? 1.0 : (s == 0.0 ? 0.0 : p - s), dinv[i], p, invp);
+                T[i * kH + jj] = v;
+            }
+            __syncthreads();
+        }
+        for (int64_t e = tid; e < static_cast<int64_t>(kk) * kk; e += kThr)
+            P.Uinv[(e / kk) * kH + e % kk] = static_cast<int32_t>(T[(e / kk) * kH + e % kk]);
+        // copy back
+        for (int64_t r = ty; r < hr; r += 32)
+            for (int64_t cc = tx; cc < W; cc += 32)
+                P.A[(P.i0 + r) * P.lda + P.c + cc] = static_cast<int32_t>(w[r * W + cc]);
+    }
+    if (tid == 0) {
+        P.out[0] = kk;
+        P.out[1] = s_fail;
+        P.out[2] = s_ncol;
+        P.out[3] = s_nrow;
+        for (int s = 0; s < s_ncol; ++s) { P.out[4 + 2 * s] = colsw[s][0]; P.out[5 + 2 * s] = colsw[s][1]; }
+        for (int s = 0; s < s_nrow; ++s) {
+            P.out[4 + 2 * kMaxSwaps + 2 * s] = rowsw[s][0];
+            P.out[5 + 2 * kMaxSwaps + 2 * s] = rowsw[s][1];
+        }
+    }
+}
+
+// Column transpositions (in order) applied to the rows outside [skip0, skip1).
+__global__ void colswap_kernel(int32_t* A, int64_t lda, int64_t m, int64_t skip0, int64_t skip1,
+                               const int* sw, int nsw, int64_t c) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x) {
+        if (r >= skip0 && r < skip1) continue;
+        int32_t* row = A + r * lda + c;
+        for (int s = 0; s < nsw; ++s) {
+            const int a = sw[2 * s], b = sw[2 * s + 1];
+            const int32_t t = row[a]; row[a] = row[b]; row[b] = t;
+        }
+    }
+}
+
+// Swap columns [c0, c1) of rows ra and rb, for each pair.
+__global__ void rowswap_kernel(int32_t* A, int64_t lda, const int64_t* pairs, int npairs, int64_t c0, int64_t c1) {
+    for (int s = 0; s < npairs; ++s) {
+        int32_t* a = A + pairs[2 * s] * lda;
+        int32_t* b = A + pairs[2 * s + 1] * lda;
+        for (int64_t cc = c0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; cc < c1;
+             cc += (int64_t)gridDim.x * blockDim.x) {
+            const int32_t t = a[cc]; a[cc] = b[cc]; b[cc] = t;
+        }
+    }
+}
+
+// Zero the columns [c0, n) of rows [r0, r1) (the U part of rows that reduced to zero).
+__global__ void zero_kernel(int32_t* A, int64_t lda, int64_t r0, int64_t r1, int64_t c0, int64_t n) {
+    for (int64_t r = r0 + blockIdx.y; r < r1; r += gridDim.y)
+        for (int64_t cc = c0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; cc < n;
+             cc += (int64_t)gridDim.x * blockDim.x)
+            A[r * lda + cc] = 0;
+}
+
+int gemm_plain(uint32_t p, const ff_opts* opts, char tX, char tY, int64_t m, int64_t n, int64_t k, uint32_t alpha,
+               const int32_t* X, int64_t ldx, const int32_t* Y, int64_t ldy, uint32_t beta, int32_t* C, int64_t ldc,
+               void* ws, cudaStream_t st) {
+    if (m == 0 || n == 0) return 0;
+    Plan pl;
+    int e = make_plan(p, k, opts, &pl);
+    if (e) return e;
+    set_scalars(&pl, alpha, beta);
+    return gemm_dev(pl, tX, tY, m, n, k, X, ldx, Y, ldy, C, ldc, ws, st);
+}
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct LqupWs {
+    size_t win, linv, uinv, out, pairs, gemm;
+    size_t total() const { return win + linv + uinv + out + pairs + gemm; }
+};
+
+int lqup_ws(uint32_t p, int64_t m, int64_t n, const ff_opts* opts, LqupWs* w) {
+    w->win = align256(static_cast<size_t>(kH) * std::max<int64_t>(n, 1) * 8 + static_cast<size_t>(kH) * kH * 8);
+    w->linv = w->uinv = align256(static_cast<size_t>(kH) * kH * 4);
+    w->out = align256((4 + 4 * kMaxSwaps) * 4);
+    w->pairs = align256(4 * kMaxSwaps * 8);
+    // GEMMs: K <= kH; M <= m, N <= n (a CRT plan for short K has the most planes)
+    size_t g = 0;
+    for (int crt = 0; crt < 2; ++crt) {
+        ff_opts o;
+        std::memset(&o, 0, sizeof(o));
+        if (opts) o = *opts;
+        if (crt) { o.scheme = FF_SCHEME_CRT; o.kb_override = 0; }
+        Plan pl;
+        if (make_plan(p, kH, &o, &pl) == 0) g = std::max(g, gemm_ws_bytes(pl, m, n));
+        else if (!crt) return FF_ERR_OPTS;
+    }
+    w->gemm = align256(g);
+    return 0;
+}
+
+// product of the first r diagonal entries of A mod p (one CTA: tree of Barrett products)
+__global__ void diag_prod_kernel(const int32_t* A, int64_t lda, int64_t r, uint32_t p, unsigned long long mu64,
+                                 uint32_t* out) {
+    __shared__ uint32_t part[256];
+    unsigned long long acc = 1 % p;
+    for (int64_t i = threadIdx.x; i < r; i += 256)
+        acc = residue_u64(acc * static_cast<uint32_t>(A[i * lda + i]), mu64, p);
+    part[threadIdx.x] = static_cast<uint32_t>(acc);
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+        if (threadIdx.x < s)
+            part[threadIdx.x] = static_cast<uint32_t>(
+                residue_u64(static_cast<unsigned long long>(part[threadIdx.x]) * part[threadIdx.x + s], mu64, p));
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = part[0];
+}
+
+int perm_parity(const int64_t* v, int64_t n) {   // 0 even, 1 odd (cycle decomposition)
+    std::vector<char> seen(static_cast<size_t>(n), 0);
+    int par = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        if (seen[i]) continue;
+        int64_t len = 0;
+        for (int64_t j = i; !seen[j]; j = v[j]) { seen[j] = 1; ++len; }
+        par ^= static_cast<int>((len - 1) & 1);
+    }
+    return par;
+}
+}  // namespace
+
+}  // namespace ff
+
+using namespace ff;
+
+extern "C" {
+
+size_t ff_lqup_workspace_size(uint32_t p, int64_t m, int64_t n, const ff_opts* opts) {
+    if (p < 2 || p >= (1u << 31) || m < 0 || n < 0) return 0;
+    LqupWs w;
+    if (lqup_ws(p, m, n, opts, &w)) return 0;
+    return w.total();
+}
+
+int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t* A, int64_t lda, int64_t* Q, int64_t* P, int64_t* rank,
+               const ff_opts* opts, void* workspace, size_t workspace_bytes, void* stream) {
+    if (p < 2 || p >= (1u << 31)) return -1;
+    if (m < 0) return -2;
+    if (n < 0) return -3;
+    if (!A && m > 0 && n > 0) return -4;
+    if (lda < (n > 1 ? n : 1)) return -5;
+    if (!Q && m > 0) return -6;
+    if (!P && n > 0) return -7;
+    if (!rank) return -8;
+    for (int64_t i = 0; i < m; ++i) Q[i] = i;
+    for (int64_t j = 0; j < n; ++j) P[j] = j;
+    *rank = 0;
+    if (m == 0 || n == 0) return 0;
+    int e = check_device();
+    if (e) return e;
+    LqupWs w;
+    if ((e = lqup_ws(p, m, n, opts, &w))) return e;
+    if (!workspace || workspace_bytes < w.total() || (reinterpret_cast<uintptr_t>(workspace) & 255)) return -10;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    uint8_t* ws = static_cast<uint8_t*>(workspace);
+    double* win = reinterpret_cast<double*>(ws);
+    double* tmpd = win + static_cast<size_t>(kH) * std::max<int64_t>(n, 1);
+    int32_t* Linv = reinterpret_cast<int32_t*>(ws + w.win);
+    int32_t* Uinv = reinterpret_cast<int32_t*>(ws + w.win + w.linv);
+    int32_t* dout = reinterpret_cast<int32_t*>(ws + w.win + w.linv + w.uinv);
+    int64_t* dpairs = reinterpret_cast<int64_t*>(ws + w.win + w.linv + w.uinv + w.out);
+    void* gws = ws + w.win + w.linv + w.uinv + w.out + w.pairs;
+    std::vector<int32_t> hout(4 + 4 * kMaxSwaps);
+    std::vector<int64_t> hp(4 * kMaxSwaps);
+    const uint32_t neg1 = p - 1;
+    static bool attr = false;
+    if (!attr) {
+        if (cudaFuncSetAttribute(panel_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes) !=
+            cudaSuccess)
+            return fail_cuda_now();
+        attr = true;
+    }
+    int64_t i0 = 0, c = 0, m_active = m, r = 0;
+    int64_t W = std::min<int64_t>(n, kH);
+    auto fail_cuda = [&]() { cudaGetLastError(); return FF_ERR_CUDA; };
+    while (i0 < m_active && c < n) {
+        const int64_t hr = std::min<int64_t>(kH, m_active - i0);
+        const int64_t Wc = std::min<int64_t>(W, n - c);
+        PanelArgs pa;
+        pa.A = A; pa.lda = lda; pa.i0 = i0; pa.hr = hr; pa.c = c; pa.W = Wc;
+        pa.full = (c + Wc == n) ? 1 : 0;
+        pa.p = p; pa.dp = static_cast<double>(p); pa.invp = 1.0 / static_cast<double>(p);
+        pa.win = win; pa.tmp = tmpd; pa.Linv = Linv; pa.Uinv = Uinv; pa.out = dout;
+        if (Wc <= kH) panel_kernel<true><<<1, kThr, kSmemBytes, st>>>(pa);
+        else panel_kernel<false><<<1, kThr, 0, st>>>(pa);
+        if (cudaGetLastError() != cudaSuccess) return fail_cuda();
+        if (cudaMemcpyAsync(hout.data(), dout, hout.size() * 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess)
+            return fail_cuda();
+        const int64_t kk = hout[0];
+        if (hout[1]) {                       // a row without pivot in the window: widen and redo
+            W = std::min<int64_t>(n, 4 * Wc);
+            continue;
+        }
+        const int ncol = hout[2], nrow = hout[3];
+        // column swaps (window coordinates) on all rows outside the panel + bookkeeping
+        if (ncol > 0) {
+            colswap_kernel<<<static_cast<unsigned>(std::min<int64_t>((m + 255) / 256, 4096)), 256, 0, st>>>(
+                A, lda, m, i0, i0 + hr, dout + 4, ncol, c);
+            for (int s = 0; s < ncol; ++s) std::swap(P[c + hout[4 + 2 * s]], P[c + hout[5 + 2 * s]]);
+        }
+        // row swaps inside the panel: the L parts (columns [0, c)) of those rows follow
+        if (nrow > 0) {
+            for (int s = 0; s < nrow; ++s) {
+                const int64_t a = i0 + hout[4 + 2 * kMaxSwaps + 2 * s], b = i0 + hout[5 + 2 * kMaxSwaps + 2 * s];
+                hp[2 * s] = a; hp[2 * s + 1] = b;
+                std::swap(Q[a], Q[b]);
+            }
+            if (c > 0) {
+                if (cudaMemcpyAsync(dpairs, hp.data(), 2 * nrow * 8, cudaMemcpyHostToDevice, st) != cudaSuccess)
+                    return fail_cuda();
+                rowswap_kernel<<<static_cast<unsigned>(std::min<int64_t>((c + 255) / 256, 1024)), 256, 0, st>>>(
+                    A, lda, dpairs, nrow, 0, c);
+            }
+        }
+        if (kk > 0) {
+            // U of the pivot rows beyond the window: U_rest = L11^-1 A_rest (in place, beta = 0)
+            if (c + Wc < n) {
+                int32_t* Ar = A + i0 * lda + c + Wc;
+                if ((e = gemm_plain(p, opts, 'N', 'N', kk, n - c - Wc, kk, 1, Linv, kH, Ar, lda, 0, Ar, lda, gws, st)))
+                    return e;
+            }
+            // trailing rows [i0 + hr, m_active): G = X U11^-1, Z <- Z - G U12
+            const int64_t mt = m_active - (i0 + hr);
+            if (mt > 0) {
+                int32_t* X = A + (i0 + hr) * lda + c;
+                if ((e = gemm_plain(p, opts, 'N', 'N', mt, kk, kk, 1, X, lda, Uinv, kH, 0, X, lda, gws, st)))
+                    return e;
+                if (c + kk < n &&
+                    (e = gemm_plain(p, opts, 'N', 'N', mt, n - c - kk, kk, neg1, X, lda, A + i0 * lda + c + kk, lda,
+                                    1, X + kk, lda, gws, st)))
+                    return e;
+            }
+        }
+        // rows of the panel that reduced to zero (full window only): to the bottom of the active rows
+        const int64_t z = hr - kk;
+        if (z > 0) {
+            zero_kernel<<<dim3(64, static_cast<unsigned>(std::min<int64_t>(z, 1024))), 256, 0, st>>>(
+                A, lda, i0 + kk, i0 + hr, c + kk, n);
+            // zero rows Zs = [i0+kk, i0+hr) go to Tb = [m_active-z, m_active): swap
+            // Zs \ Tb with Tb \ Zs (trailing rows, already updated above)
+            const int64_t dst0 = m_active - z;
+            const int64_t b0 = std::max(dst0, i0 + hr);
+            int np = 0;
+            for (int64_t a = i0 + kk, b = b0; a < std::min(dst0, i0 + hr); ++a, ++b) {
+                hp[2 * np] = a; hp[2 * np + 1] = b; ++np;
+                std::swap(Q[a], Q[b]);
+            }
+            if (np > 0) {
+                if (cudaMemcpyAsync(dpairs, hp.data(), 2 * np * 8, cudaMemcpyHostToDevice, st) != cudaSuccess)
+                    return fail_cuda();
+                rowswap_kernel<<<static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 1024)), 256, 0, st>>>(
+                    A, lda, dpairs, np, 0, n);
+            }
+            m_active -= z;
+        }
+        i0 += kk;
+        c += kk;
+        r += kk;
+        W = std::min<int64_t>(n, kH);
+    }
+    // rows that never got a pivot (c reached n): their U part is already zero
+    *rank = r;
+    return cudaStreamSynchronize(st) == cudaSuccess ? 0 : FF_ERR_CUDA;
+}
+
+int ff_rank_det(uint32_t p, int64_t m, int64_t n, const int32_t* A, int64_t lda, int64_t* rank, uint32_t* det) {
+    if (p < 2 || p >= (1u << 31)) return -1;
+    if (m < 0) return -2;
+    if (n < 0) return -3;
+    if (!A && m > 0 && n > 0) return -4;
+    if (lda < (n > 1 ? n : 1)) return -5;
+    if (!rank) return -6;
+    if (det && m != n) return -7;
+    const size_t need = ff_lqup_workspace_size(p, m, n, nullptr);
+    if (need == 0) return FF_ERR_INTERNAL;
+    const size_t abytes = (static_cast<size_t>(m) * std::max<int64_t>(n, 1) * 4 + 255) & ~size_t(255);
+    void* ws = nullptr;
+    if (cudaMalloc(&ws, need + abytes + 256) != cudaSuccess) {
+        cudaGetLastError();
+        return FF_ERR_NOMEM;
+    }
+    int32_t* Ac = static_cast<int32_t*>(ws);
+    uint32_t* dprod = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(ws) + abytes);
+    std::vector<int64_t> Q(static_cast<size_t>(std::max<int64_t>(m, 1))), P(static_cast<size_t>(std::max<int64_t>(n, 1)));
+    int e = 0;
+    if (m > 0 && n > 0 && cudaMemcpy2D(Ac, n * 4, A, lda * 4, n * 4, m, cudaMemcpyDeviceToDevice) != cudaSuccess)
+        e = FF_ERR_CUDA;
+    if (!e) e = ff_lqup_ex(p, m, n, Ac, n, Q.data(), P.data(), rank, nullptr, static_cast<uint8_t*>(ws) + abytes + 256,
+                           need, nullptr);
+    if (!e && det) {
+        if (*rank < m) {
+            *det = 0;
+        } else {
+            // det A = sign(Q) sign(P) prod_i U_ii  (Q A P = L U, L unit lower)
+            const unsigned long long mu64 = static_cast<unsigned long long>((static_cast<unsigned __int128>(1) << 64) / p);
+            diag_prod_kernel<<<1, 256>>>(Ac, n, *rank, p, mu64, dprod);
+            uint32_t d = 0;
+            if (cudaMemcpy(&d, dprod, 4, cudaMemcpyDeviceToHost) != cudaSuccess) e = FF_ERR_CUDA;
+            const int odd = perm_parity(Q.data(), m) ^ perm_parity(P.data(), n);
+            *det = (odd && d) ? p - d : d;
+        }
+    }
+    cudaFree(ws);
+    return e;
+}
+
+int ff_lqup(uint32_t p, int64_t m, int64_t n, int32_t* A, int64_t lda, int64_t* Q, int64_t* P, int64_t* rank) {
+    if (p < 2 || p >= (1u << 31)) return -1;
+    if (m < 0) return -2;
+    if (n < 0) return -3;
+    const size_t need = ff_lqup_workspace_size(p, m, n, nullptr);
+    if (need == 0) return FF_ERR_INTERNAL;
+    void* ws = nullptr;
+    if (cudaMalloc(&ws, need) != cudaSuccess) {
+        cudaGetLastError();
+        return FF_ERR_NOMEM;
+    }
+    const int e = ff_lqup_ex(p, m, n, A, lda, Q, P, rank, nullptr, ws, need, nullptr);
+    cudaFree(ws);
+    return e;
+}
+
+}  // extern "C"

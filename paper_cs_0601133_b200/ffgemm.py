@@ -65,6 +65,10 @@ _SIGS = {
     "ff_trsm_workspace_size": ([_u32, _ch, _i64, _i64, _OPTS_P], _sz),
     "ff_trsm_ex": ([_u32, _ch, _ch, _ch, _ch, _i64, _i64, _u32, _p, _i64, _p, _i64, _OPTS_P, _p, _sz, _p],
                    ctypes.c_int),
+    "ff_lqup": ([_u32, _i64, _i64, _p, _i64, _p, _p, _p], ctypes.c_int),
+    "ff_lqup_workspace_size": ([_u32, _i64, _i64, _OPTS_P], _sz),
+    "ff_lqup_ex": ([_u32, _i64, _i64, _p, _i64, _p, _p, _p, _OPTS_P, _p, _sz, _p], ctypes.c_int),
+    "ff_rank_det": ([_u32, _i64, _i64, _p, _i64, _p, _p], ctypes.c_int),
 }
 for _name, (_args, _res) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -256,3 +260,31 @@ def ftrsm(p: int, A, B, side: str = "L", uplo: str = "U", transA: str = "N", dia
     ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=B.device)
     ff_trsm_ex(p, side, uplo, transA, diag, m, n, alpha, A, _ld(A), B, _ld(B), opts, ws, nbytes, stream)
     return B
+
+
+def lqup(p: int, A, opts=None, stream=None):
+    """In-place LQUP (PLUQ arrangement, include/ffgemm.h) of the int32 CUDA
+    tensor A; returns (Q, P, rank) with Q, P numpy int64 permutation arrays."""
+    import numpy as np
+    import torch
+    if A.dtype != torch.int32 or not A.is_cuda:
+        raise TypeError("lqup takes an int32 CUDA tensor")
+    m, n = A.shape
+    Q = np.zeros(max(m, 1), dtype=np.int64)
+    P = np.zeros(max(n, 1), dtype=np.int64)
+    r = ctypes.c_int64(0)
+    nbytes = _lib.ff_lqup_workspace_size(p, m, n, _opts(opts))
+    ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=A.device)
+    _check(_lib.ff_lqup_ex(p, m, n, _ptr(A), _ld(A), Q.ctypes.data, P.ctypes.data, ctypes.byref(r), _opts(opts),
+                           _ptr(ws), nbytes, _stream(stream)), "ff_lqup_ex")
+    return Q[:m], P[:n], r.value
+
+
+def rank_det(p: int, A):
+    """(rank, det or None) of the int32 CUDA tensor A (not modified)."""
+    m, n = A.shape
+    r = ctypes.c_int64(0)
+    d = ctypes.c_uint32(0)
+    _check(_lib.ff_rank_det(p, m, n, _ptr(A), _ld(A), ctypes.byref(r), ctypes.byref(d) if m == n else None),
+           "ff_rank_det")
+    return r.value, (d.value if m == n else None)

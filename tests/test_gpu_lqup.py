@@ -1,0 +1,121 @@
+"""GPU LQUP / rank / determinant (Sec. 5.1 and 6)
+against the oracle.  The factorization is not unique, so the tests check
+what is unique (rank, determinant) against oracle.rank_det and that the rest
+is valid: Q, P permutations, L unit lower, U upper with a non-zero diagonal,
+zero rows beyond the rank, and A[Q][:, P] = L U (mod p) exactly."""
+import numpy as np
+import pytest
+
+import ffgen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+    import paper_cs_0601133_b200 as ff
+    assert torch.cuda.is_available()
+    torch.cuda.set_device(0)
+    return torch, ff
+
+
+def _factor(torch, ff, p, A):
+    dA = torch.from_numpy(np.ascontiguousarray(A)).cuda()
+    Q, P, r = ff.lqup(p, dA)
+    torch.cuda.synchronize()
+    return dA.cpu().numpy(), Q, P, r
+
+
+def _check_valid(p, A, F, Q, P, r, full_product=True):
+    m, n = A.shape
+    assert sorted(Q.tolist()) == list(range(m)) and sorted(P.tolist()) == list(range(n))
+    assert 0 <= r <= min(m, n)
+    assert F.min() >= 0 and F.max() < p
+    L = np.zeros((m, r), np.int64)
+    for k in range(r):
+        L[k + 1:, k] = F[k + 1:, k]
+        L[k, k] = 1
+    U = np.triu(F[:r, :].astype(np.int64))
+    assert (np.diagonal(U[:, :r]) != 0).all()                 # U_kk != 0 for k < r
+    assert (F[r:, r:] == 0).all()                             # zero rows beyond the rank
+    Ap = np.ascontiguousarray(np.mod(A.astype(np.int64), p)[Q][:, P].astype(np.int32))
+    if full_product:
+        LU = oracle.fgemm(p, "N", "N", 1, L.astype(np.int32), U.astype(np.int32), 0, m=m, n=n, k=r) if r \
+            else np.zeros((m, n), np.int32)
+        np.testing.assert_array_equal(LU, Ap)
+    else:                                                     # Freivalds: A' x = L (U x)
+        for t in range(3):
+            x = ffgen.uniform_vector(p, 77, 30 + t, n)
+            lhs = oracle.matvec(p, "N", Ap, x)
+            ux = oracle.matvec(p, "N", U.astype(np.int32), x) if r else np.zeros(0, np.int32)
+            rhs = oracle.matvec(p, "N", L.astype(np.int32), ux) if r else np.zeros(m, np.int32)
+            np.testing.assert_array_equal(lhs, rhs)
+
+
+def _low_rank(rng, p, m, n, r):
+    X = rng.integers(0, p, size=(m, r)).astype(np.int32)
+    Y = rng.integers(0, p, size=(r, n)).astype(np.int32)
+    return oracle.fgemm(p, "N", "N", 1, X, Y, 0, m=m, n=n, k=r) if r else np.zeros((m, n), np.int32)
+
+
+@pytest.mark.parametrize("p", [3, 65521, 8388593, 67108859])
+@pytest.mark.parametrize("m,n,r", [(300, 300, None), (200, 530, None), (530, 200, None), (400, 400, 0),
+                                   (400, 400, 1), (400, 380, 5), (520, 600, 130), (257, 1000, 256)])
+def test_lqup_vs_oracle_rank(env, p, m, n, r):
+    torch, ff = env
+    rng = np.random.default_rng(m * 3 + n + (r or 0) + p % 101)
+    A = rng.integers(-2 ** 31, 2 ** 31, size=(m, n), dtype=np.int64).astype(np.int32) if r is None \
+        else _low_rank(rng, p, m, n, r)
+    F, Q, P, rk = _factor(torch, ff, p, A)
+    want_r, want_d = oracle.rank_det(p, A)
+    assert rk == want_r
+    _check_valid(p, A, F, Q, P, rk)
+    dA = torch.from_numpy(A).cuda()
+    got_r, got_d = ff.rank_det(p, dA)
+    assert got_r == want_r and got_d == want_d
+    assert torch.equal(dA.cpu(), torch.from_numpy(A))        # rank_det leaves A untouched
+
+
+def test_lqup_structured_rank_deficiency(env):
+    """Zero rows, repeated rows, zero leading columns, a rank-deficient first
+    panel and a window that must be widened (pivots beyond 256 columns)."""
+    torch, ff = env
+    p = 65521
+    rng = np.random.default_rng(5)
+    m, n = 300, 900
+    A = rng.integers(0, p, size=(m, n)).astype(np.int32)
+    A[0] = 0
+    A[3] = A[1]
+    A[10] = (2 * A[2].astype(np.int64) % p).astype(np.int32)
+    A[:, :40] = 0
+    A[20:60, :] = 0
+    A[70, :700] = 0                                           # first non-zero beyond the initial window
+    A[130:260, :] = A[0:130, :]                               # the second panel repeats the first
+    F, Q, P, rk = _factor(torch, ff, p, A)
+    assert rk == oracle.rank_det(p, A)[0]
+    _check_valid(p, A, F, Q, P, rk)
+
+
+@pytest.mark.parametrize("p", [65521, 67108859])
+def test_det_small_and_signs(env, p):
+    torch, ff = env
+    rng = np.random.default_rng(p % 31)
+    for n in [1, 2, 3, 7, 129, 260]:
+        A = rng.integers(0, p, size=(n, n)).astype(np.int32)
+        assert ff.rank_det(p, torch.from_numpy(A).cuda()) == oracle.rank_det(p, A)
+        S = A.copy()
+        S[:, [0, n - 1]] = S[:, [n - 1, 0]]
+        if n > 1:
+            assert ff.rank_det(p, torch.from_numpy(S).cuda())[1] == (p - oracle.rank_det(p, A)[1]) % p
+
+
+def test_lqup_large_freivalds(env):
+    torch, ff = env
+    p = 65521
+    N = 2048
+    A = ffgen.uniform_matrix(p, 21, ffgen.STREAM_A, N, N)
+    F, Q, P, rk = _factor(torch, ff, p, A)
+    assert rk == oracle.rank_det(p, A)[0]
+    _check_valid(p, A, F, Q, P, rk, full_product=False)
