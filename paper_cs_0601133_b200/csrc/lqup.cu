@@ -26,6 +26,8 @@
 #include <algorithm>
 #include <cstring>
 #include <vector>
+#include <cstdio>
+#include <cstdlib>
 
 #include "internal.h"
 #include "modp.cuh"
@@ -37,7 +39,7 @@ namespace {
 constexpr int kH = 128;          // panel rows
 constexpr int kThr = 1024;
 constexpr int kMaxSwaps = 2 * kH;
-constexpr int kSmemBytes = kH * kH * 8;   // the window in shared memory (doubles)
+constexpr int kSmemBytes = 2 * kH * kH * 4;   // the window + the inverse scratch in shared memory (uint32)
 
 int fail_cuda_now() {
     cudaGetLastError();
@@ -52,6 +54,7 @@ struct PanelArgs {
     int32_t full;                // 1: the window reaches the last column (zero rows allowed)
     uint32_t p;
     double dp, invp;             // p, fl(1/p)
+    unsigned long long mu64;     // floor(2^64 / p)
     double* win;                 // workspace hr x W (ld W): the window, residues as exact doubles
     int32_t* Linv;               // kH x kH
     int32_t* Uinv;               // kH x kH
@@ -88,130 +91,194 @@ __device__ uint32_t inv_dev(uint32_t a, uint32_t p) {
     return static_cast<uint32_t>(s0 < 0 ? s0 + static_cast<int32_t>(p) : s0);
 }
 
+// Shoup's constant floor(w 2^32 / p) for w < p < 2^31 from mu64 = floor(2^64 / p):
+// (w mu64) >> 32 is the floor or one less (w eps / 2^32 < 1/2); one 64-bit check
+// makes it exact.  Integer instructions only.
+__device__ __forceinline__ uint32_t shoup_c(uint32_t w, uint32_t p, unsigned long long mu64) {
+    const unsigned long long lo = static_cast<unsigned long long>(w) * static_cast<uint32_t>(mu64);
+    const unsigned long long hi = static_cast<unsigned long long>(w) * static_cast<uint32_t>(mu64 >> 32);
+    uint64_t c = (hi + (lo >> 32)) ;     // (w mu64) >> 32  (w < 2^31: no overflow of the sum)
+    if ((c + 1) * p <= (static_cast<uint64_t>(w) << 32)) ++c;
+    return static_cast<uint32_t>(c);
+}
+// x w mod p for x, w < p (Shoup): one mulhi, two multiplies, one correction.
+__device__ __forceinline__ uint32_t shoup_m(uint32_t x, uint32_t w, uint32_t wsh, uint32_t p) {
+    const uint32_t q = __umulhi(x, wsh);
+    const uint32_t r = x * w - q * p;
+    return r >= p ? r - p : r;
+}
+__device__ __forceinline__ uint32_t subm_u(uint32_t a, uint32_t b, uint32_t p) { return a >= b ? a - b : a + p - b; }
+
 // One CTA of 32 x 32 threads factors the panel window (see the file header).
-// kSmem: the window (<= kH x kH doubles, 128 KB) lives in shared memory (the
-// generic case); otherwise in the global workspace (widened windows).
+// kSmem: the window (<= kH x kH residues) and the inverse scratch live in
+// shared memory (the generic case); otherwise in the global workspace.
+//
+// Fraction-free elimination keeps the modular inverse off the critical path:
+// at pivot k (raw value pi_k) every unprocessed row becomes
+// pi_k row_s - a_s row_k, so all rows below and the next pivot row carry the
+// same scale S_k = prod_{k'<k} pi_k'; hence the true multiplier is
+// L_sk = a_s / pi_k (the scales cancel) and the true U row k is row_k / S_k.
+// After the elimination the pi_k are inverted in parallel and the raw
+// multipliers and U rows rescaled.  L11^-1 and U11^-1 are then formed by
+// Gauss-Jordan phases (one barrier and a few products per phase).  All
+// products are Shoup multiplications by a per-row or per-step constant.
 template <bool kSmem>
 __global__ void __launch_bounds__(kThr) panel_kernel(PanelArgs P) {
-    extern __shared__ double dyn_smem[];
+    extern __shared__ uint32_t dyn_smem[];
     __shared__ int s_j;
-    __shared__ double s_inv;
     __shared__ int s_ncol, s_nrow, s_kk, s_fail;
     __shared__ int colsw[kMaxSwaps][2];
     __shared__ int rowsw[kMaxSwaps][2];
-    __shared__ double dinv[kH];                    // inverses of the pivots (U11's diagonal)
+    __shared__ uint32_t piv[kH], pinv[kH], sinv[kH], sfw[kH];
+    __shared__ int orig[kH];                      // original panel row now at each position
     const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
     const int64_t hr = P.hr, W = P.W;
-    const double p = P.dp, invp = P.invp;
-    double* w = kSmem ? dyn_smem : P.win;
+    const uint32_t p = P.p;
+    const unsigned long long c32 = P.mu64;             // floor(2^64 / p), for shoup_c
+    uint32_t* w = kSmem ? dyn_smem : reinterpret_cast<uint32_t*>(P.win);
+    uint32_t* E = kSmem ? dyn_smem + kH * kH : reinterpret_cast<uint32_t*>(P.tmp);   // kH x kH
+    long long t_0 = clock64();
     // copy in (canonical residues)
     for (int64_t r = ty; r < hr; r += 32)
         for (int64_t cc = tx; cc < W; cc += 32) {
-            const int64_t v = static_cast<int64_t>(P.A[(P.i0 + r) * P.lda + P.c + cc]) % static_cast<int64_t>(P.p);
-            w[r * W + cc] = static_cast<double>(v < 0 ? v + P.p : v);
+            const int64_t v = static_cast<int64_t>(P.A[(P.i0 + r) * P.lda + P.c + cc]) % static_cast<int64_t>(p);
+            w[r * W + cc] = static_cast<uint32_t>(v < 0 ? v + p : v);
         }
-    if (tid == 0) { s_ncol = 0; s_nrow = 0; s_kk = 0; s_fail = 0; }
+    // E = I (kH x kH): the same row operations turn it into S L^-1 (see below)
+    for (int e = tid; e < kH * kH; e += kThr) E[e] = ((e / kH) == (e % kH)) ? 1u : 0u;
+    for (int e = tid; e < kH; e += kThr) orig[e] = e;
+    if (tid == 0) { s_ncol = 0; s_nrow = 0; s_kk = 0; s_fail = 0; s_j = INT32_MAX; }
     __syncthreads();
     for (int64_t i = 0; i < hr; ++i) {
         const int kk = s_kk;
-        if (tid == 0) s_j = INT32_MAX;
-        __syncthreads();
-        // first non-zero of row i in columns [kk, W)
-        for (int64_t cc = kk + tid; cc < W; cc += kThr)
-            if (w[i * W + cc] != 0.0) atomicMin(&s_j, static_cast<int>(cc));
+        // first non-zero of row i in columns [kk, W): ballot per warp, one atomic per warp
+        for (int64_t c0 = kk + 32 * ty; c0 < W; c0 += kThr) {
+            const int64_t cc = c0 + tx;
+            const unsigned bal = __ballot_sync(0xffffffffu, cc < W && w[i * W + cc] != 0u);
+            if (bal) { if (tx == 0) atomicMin(&s_j, static_cast<int>(c0) + __ffs(bal) - 1); break; }
+        }
         __syncthreads();
         const int j = s_j;
         if (j == INT32_MAX) {                      // no pivot in the window
             if (!P.full) { if (tid == 0) s_fail = 1; __syncthreads(); break; }
-            __syncthreads();
+            __syncthreads();                       // (everyone has read s_j before the next search)
             continue;                              // a zero row (stays below the pivot rows)
         }
-        // column swap kk <-> j (all panel rows), row swap i <-> kk
-        if (j != kk) {
+        // column swap kk <-> j (all panel rows) and row swap i <-> kk, disjoint cells first
+        if (j != kk)
             for (int64_t r = tid; r < hr; r += kThr) {
-                const double t = w[r * W + kk]; w[r * W + kk] = w[r * W + j]; w[r * W + j] = t;
+                const uint32_t t = w[r * W + kk]; w[r * W + kk] = w[r * W + j]; w[r * W + j] = t;
             }
-            if (tid == 0) { colsw[s_ncol][0] = kk; colsw[s_ncol][1] = j; ++s_ncol; }
-        }
-        __syncthreads();
         if (i != kk) {
             for (int64_t cc = tid; cc < W; cc += kThr) {
-                const double t = w[i * W + cc]; w[i * W + cc] = w[kk * W + cc]; w[kk * W + cc] = t;
+                if (cc == kk || cc == j) continue;
+                const uint32_t t = w[i * W + cc]; w[i * W + cc] = w[kk * W + cc]; w[kk * W + cc] = t;
             }
-            if (tid == 0) { rowsw[s_nrow][0] = kk; rowsw[s_nrow][1] = static_cast<int>(i); ++s_nrow; }
-            __syncthreads();
+            for (int c = tid; c < kH; c += kThr) {     // E rows follow (rows i, kk)
+                const uint32_t t = E[i * kH + c]; E[i * kH + c] = E[kk * kH + c]; E[kk * kH + c] = t;
+            }
         }
+        __syncthreads();
         if (tid == 0) {
-            s_inv = static_cast<double>(inv_dev(static_cast<uint32_t>(w[kk * W + kk]), P.p));
-            dinv[kk] = s_inv;
+            if (i != kk) {                         // the swapped columns of the swapped rows
+                uint32_t t = w[i * W + kk]; w[i * W + kk] = w[kk * W + kk]; w[kk * W + kk] = t;
+                if (j != kk) { t = w[i * W + j]; w[i * W + j] = w[kk * W + j]; w[kk * W + j] = t; }
+            }
+            if (j != kk) { colsw[s_ncol][0] = kk; colsw[s_ncol][1] = j; ++s_ncol; }
+            if (i != kk) {
+                rowsw[s_nrow][0] = kk; rowsw[s_nrow][1] = static_cast<int>(i); ++s_nrow;
+                const int t = orig[kk]; orig[kk] = orig[i]; orig[i] = t;
+            }
+            s_j = INT32_MAX;
         }
         __syncthreads();
-        // eliminate the unprocessed rows i+1..hr-1 (the zero rows kk+1..i are zero from kk on):
-        // multipliers (column kk), then columns kk+1..W-1
-        const double inv = s_inv;
-        for (int64_t r = i + 1 + tid; r < hr; r += kThr) w[r * W + kk] = mulm(w[r * W + kk], inv, p, invp);
-        __syncthreads();
+        const uint32_t pk = w[kk * W + kk];
+        const uint32_t pk_sh = shoup_c(pk, p, c32);
+        if (tid == 0) piv[kk] = pk;
+        // fraction-free update of the unprocessed rows i+1..hr-1 (raw a_s stays in column kk)
         for (int64_t r = i + 1 + ty; r < hr; r += 32) {
-            const double f = w[r * W + kk];
-            if (f == 0.0) continue;
-            for (int64_t cc = kk + 1 + tx; cc < W; cc += 32)
-                w[r * W + cc] = subm(w[r * W + cc], mulm(f, w[kk * W + cc], p, invp), p);
+            const uint32_t as = w[r * W + kk];
+            if (as == 0u) {
+                for (int64_t cc = kk + 1 + tx; cc < W; cc += 32) w[r * W + cc] = shoup_m(w[r * W + cc], pk, pk_sh, p);
+                for (int c = tx; c <= static_cast<int>(i); c += 32) E[r * kH + c] = shoup_m(E[r * kH + c], pk, pk_sh, p);
+                if (tx == 0) E[r * kH + r] = shoup_m(E[r * kH + r], pk, pk_sh, p);   // E_r's own column r > i
+            } else {
+                const uint32_t as_sh = shoup_c(as, p, c32);
+                for (int64_t cc = kk + 1 + tx; cc < W; cc += 32)
+                    w[r * W + cc] = subm_u(shoup_m(w[r * W + cc], pk, pk_sh, p), shoup_m(w[kk * W + cc], as, as_sh, p), p);
+                for (int c = tx; c <= static_cast<int>(i); c += 32)
+                    E[r * kH + c] = subm_u(shoup_m(E[r * kH + c], pk, pk_sh, p), shoup_m(E[kk * kH + c], as, as_sh, p), p);
+                if (tx == 0) E[r * kH + r] = shoup_m(E[r * kH + r], pk, pk_sh, p);   // (E_kk has no column r)
+            }
         }
         if (tid == 0) s_kk = kk + 1;
         __syncthreads();
     }
     const int kk = s_kk;
+    long long t_1 = clock64(), t_2 = 0, t_3 = 0, t_4 = 0;
     if (!s_fail) {
-        // Linv = L11^-1 (unit lower) and Uinv = U11^-1 (upper) by row sweeps;
-        // 8 threads per column share each dot product (shuffle-reduced).
-        double* T = P.tmp;                              // rows of the inverse being built (kH x kH)
-        const int jj = tid >> 3, part = tid & 7;
-        auto dot8 = [&](double s) {                     // sum over the 8 lanes of a column group, mod p
-            for (int o = 4; o > 0; o >>= 1) {
-                const double t = __shfl_down_sync(0xffffffffu, s, o, 8);
-                s = s + t;
-                if (s >= p) s -= p;
-            }
-            return __shfl_sync(0xffffffffu, s, 0, 8);
-        };
-        for (int i = 0; i < kk; ++i) {                  // Linv_i = e_i - sum_{jj<=l<i} L_il Linv_l
-            double s = 0.0;
-            if (jj < i)
-                for (int l = jj + part; l < i; l += 8) {
-                    s += mulm(w[i * W + l], T[l * kH + jj], p, invp);
-                    if (s >= p) s -= p;
-                }
-            s = dot8(s);
-            if (part == 0 && jj < kk) T[i * kH + jj] = (jj == i) ? 1.0 : (jj < i ? (s == 0.0 ? 0.0 : p - s) : 0.0);
-            __syncthreads();
-        }
-        for (int64_t e = tid; e < static_cast<int64_t>(kk) * kk; e += kThr)
-            P.Linv[(e / kk) * kH + e % kk] = static_cast<int32_t>(T[(e / kk) * kH + e % kk]);
+        // pivot inverses (parallel), prefix products S_k^-1 and S_k
+        for (int k = tid; k < kk; k += kThr) pinv[k] = inv_dev(piv[k], p);
         __syncthreads();
-        for (int i = kk - 1; i >= 0; --i) {             // Uinv_i = (e_i - sum_{i<l<=jj} U_il Uinv_l) / U_ii
-            double s = 0.0;
-            if (jj > i && jj < kk)
-                for (int l = i + 1 + part; l <= jj; l += 8) {
-                    s += mulm(w[i * W + l], T[l * kH + jj], p, invp);
-                    if (s >= p) s -= p;
-                }
-            s = dot8(s);
-            __syncthreads();
-            if (part == 0 && jj < kk) {
-                double v = 0.0;
-                if (jj >= i) v = mulm(jj == i ? 1.0 : (s == 0.0 ? 0.0 : p - s), dinv[i], p, invp);
-                T[i * kH + jj] = v;
+        if (tid == 0) {
+            uint32_t sacc = 1 % p, facc = 1 % p;
+            for (int k = 0; k < kk; ++k) {
+                sinv[k] = sacc; sacc = shoup_m(sacc, pinv[k], shoup_c(pinv[k], p, c32), p);
+                sfw[k] = facc; facc = shoup_m(facc, piv[k], shoup_c(piv[k], p, c32), p);
+            }
+        }
+        __syncthreads();
+        // true L (w[s][k] = a_s / pi_k for k < min(s, kk)) and true U (row k / S_k)
+        for (int64_t r = ty; r < hr; r += 32) {
+            const uint32_t si = r < kk ? sinv[r] : 0u;
+            const uint32_t si_sh = r < kk ? shoup_c(si, p, c32) : 0u;
+            for (int64_t cc = tx; cc < W; cc += 32) {
+                const uint32_t x = w[r * W + cc];
+                if (cc < r && cc < kk) w[r * W + cc] = shoup_m(x, pinv[cc], shoup_c(pinv[cc], p, c32), p);
+                else if (r < kk && cc >= r) w[r * W + cc] = shoup_m(x, si, si_sh, p);
+            }
+        }
+        t_2 = clock64();
+        // Linv = L11^-1: E = S L^-1 Pi with Pi the panel's row permutation (E's columns
+        // are original row indices), so Linv[r][c] = E[r][orig[c]] / S_r
+        for (int e = tid; e < kk * kk; e += kThr) {
+            const int r = e / kk, c = e % kk;
+            P.Linv[r * kH + c] =
+                static_cast<int32_t>(c <= r ? shoup_m(E[r * kH + orig[c]], sinv[r], shoup_c(sinv[r], p, c32), p) : 0u);
+        }
+        __syncthreads();
+        t_3 = clock64();
+        // Uinv: F <- I; phase k = kk-1..0: rows r < k: F_r -= (u_rk / u_kk) F_k; at the end
+        // F_k *= 1/u_kk (the true u_kk = pi_k / S_k, so 1/u_kk = pi_k^-1 S_k)
+        for (int e = tid; e < kk * kH; e += kThr) E[e] = ((e / kH) == (e % kH)) ? 1u : 0u;
+        __syncthreads();
+        for (int k = kk - 1; k > 0; --k) {
+            const uint32_t iu = shoup_m(pinv[k], sfw[k], shoup_c(sfw[k], p, c32), p);
+            for (int r = ty; r < k; r += 32) {
+                const uint32_t u = w[r * W + k];
+                if (u == 0u) continue;
+                const uint32_t m = shoup_m(u, iu, shoup_c(iu, p, c32), p);
+                const uint32_t m_sh = shoup_c(m, p, c32);
+                for (int c = k + tx; c < kk; c += 32) E[r * kH + c] = subm_u(E[r * kH + c], shoup_m(E[k * kH + c], m, m_sh, p), p);
             }
             __syncthreads();
         }
-        for (int64_t e = tid; e < static_cast<int64_t>(kk) * kk; e += kThr)
-            P.Uinv[(e / kk) * kH + e % kk] = static_cast<int32_t>(T[(e / kk) * kH + e % kk]);
+        for (int e = tid; e < kk * kk; e += kThr) {
+            const int r = e / kk;
+            const uint32_t iu = shoup_m(pinv[r], sfw[r], shoup_c(sfw[r], p, c32), p);
+            E[r * kH + e % kk] = shoup_m(E[r * kH + e % kk], iu, shoup_c(iu, p, c32), p);
+        }
+        __syncthreads();
+        for (int e = tid; e < kk * kk; e += kThr) P.Uinv[(e / kk) * kH + e % kk] = static_cast<int32_t>(E[(e / kk) * kH + e % kk]);
+        t_4 = clock64();
         // copy back
         for (int64_t r = ty; r < hr; r += 32)
             for (int64_t cc = tx; cc < W; cc += 32)
                 P.A[(P.i0 + r) * P.lda + P.c + cc] = static_cast<int32_t>(w[r * W + cc]);
     }
     if (tid == 0) {
+        long long* tt = reinterpret_cast<long long*>(P.out + 4 + 4 * kMaxSwaps);
+        tt[0] = t_1 - t_0; tt[1] = t_2 - t_1; tt[2] = t_3 - t_2; tt[3] = t_4 - t_3; tt[4] = clock64() - t_4;
         P.out[0] = kk;
         P.out[1] = s_fail;
         P.out[2] = s_ncol;
@@ -278,7 +345,7 @@ struct LqupWs {
 int lqup_ws(uint32_t p, int64_t m, int64_t n, const ff_opts* opts, LqupWs* w) {
     w->win = align256(static_cast<size_t>(kH) * std::max<int64_t>(n, 1) * 8 + static_cast<size_t>(kH) * kH * 8);
     w->linv = w->uinv = align256(static_cast<size_t>(kH) * kH * 4);
-    w->out = align256((4 + 4 * kMaxSwaps) * 4);
+    w->out = align256((4 + 4 * kMaxSwaps) * 4 + 64);
     w->pairs = align256(4 * kMaxSwaps * 8);
     // GEMMs: K <= kH; M <= m, N <= n (a CRT plan for short K has the most planes)
     size_t g = 0;
@@ -387,6 +454,7 @@ int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t* A, int64_t lda, int64_
         pa.A = A; pa.lda = lda; pa.i0 = i0; pa.hr = hr; pa.c = c; pa.W = Wc;
         pa.full = (c + Wc == n) ? 1 : 0;
         pa.p = p; pa.dp = static_cast<double>(p); pa.invp = 1.0 / static_cast<double>(p);
+        pa.mu64 = static_cast<unsigned long long>((static_cast<unsigned __int128>(1) << 64) / p);
         pa.win = win; pa.tmp = tmpd; pa.Linv = Linv; pa.Uinv = Uinv; pa.out = dout;
         if (Wc <= kH) panel_kernel<true><<<1, kThr, kSmemBytes, st>>>(pa);
         else panel_kernel<false><<<1, kThr, 0, st>>>(pa);
@@ -395,6 +463,12 @@ int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t* A, int64_t lda, int64_
             cudaStreamSynchronize(st) != cudaSuccess)
             return fail_cuda();
         const int64_t kk = hout[0];
+        if (getenv("FF_LQUP_TRACE")) {
+            long long tt[5];
+            cudaMemcpy(tt, dout + 4 + 4 * kMaxSwaps, sizeof(tt), cudaMemcpyDeviceToHost);
+            fprintf(stderr, "[lqup panel i0=%lld kk=%lld W=%lld] cycles: elim %lld  rescale %lld  Linv %lld  Uinv %lld  copy %lld\n",
+                    (long long)i0, (long long)kk, (long long)Wc, tt[0], tt[1], tt[2], tt[3], tt[4]);
+        }
         if (hout[1]) {                       // a row without pivot in the window: widen and redo
             W = std::min<int64_t>(n, 4 * Wc);
             continue;
