@@ -192,12 +192,22 @@ __global__ void __launch_bounds__(256) encode_crt_direct_kernel(ModP M, CrtConst
                 c[t] = centre(residue_i32(c[t], M), M);
                 dg[t] = crt_split(c[t]);
             }
+            uint32_t* dst = reinterpret_cast<uint32_t*>(planes + r * k_pad);
+            // plane 0 is q = 256 (the planner picks 256 first): the low byte of c
+            dst[g] = (static_cast<uint32_t>(c[0]) & 0xFFu) | ((static_cast<uint32_t>(c[1]) & 0xFFu) << 8) |
+                     ((static_cast<uint32_t>(c[2]) & 0xFFu) << 16) | (static_cast<uint32_t>(c[3]) << 24);
 #pragma unroll
-            for (int i = 0; i < kMaxMod; ++i) {
+            for (int i = 1; i < kMaxMod; ++i) {
                 if (i < C.nq) {
+                    const float fq = C.fq[i], fi = C.finv[i], fw = C.fw15[i];
                     uint32_t w = 0;
 #pragma unroll
-                    for (int t = 0; t < 4; ++t) w |= crt_digit(c[t], dg[t], C, i) << (8 * t);
+                    for (int t = 0; t < 4; ++t) {
+                        const float sv = fmaf(dg[t].h1, fw, dg[t].h0);
+                        const float tq = fmaf(sv, fi, 12582912.0f) - 12582912.0f;
+                        const float rr = fmaf(-fq, tq, sv);
+                        w |= (__float_as_uint(rr + 12582912.0f) & 0xFFu) << (8 * t);
+                    }
                     dst[g + i * (plane / 4)] = w;
                 }
             }
@@ -242,6 +252,17 @@ __global__ void __launch_bounds__(256) encode_crt_trans_kernel(ModP M, CrtConsts
         const int64_t r = r0 + wr;
         const int64_t kc = kk0 + wc;
         for (int b0 = 0; b0 < C.nq; b0 += 4) {
+            // this batch's constants in registers (runtime-indexed parameter
+            // loads inside the digit loop dominated the instruction count)
+            float fq[4], fi[4], fw[4];
+            bool q256[4], live[4];
+#pragma unroll
+            for (int l = 0; l < 4; ++l) {
+                const int pl = b0 + l < C.nq ? b0 + l : 0;
+                live[l] = b0 + l < C.nq;
+                q256[l] = C.q[pl] == 256u;
+                fq[l] = C.fq[pl]; fi[l] = C.finv[pl]; fw[l] = C.fw15[pl];
+            }
             __syncthreads();
 #pragma unroll
             for (int g = 0; g < 4; ++g) {
@@ -249,14 +270,20 @@ __global__ void __launch_bounds__(256) encode_crt_trans_kernel(ModP M, CrtConsts
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     const int32_t c = cv[4 * g + e];
-                    const CrtDigitsIn dg = crt_split(c);
+                    const CrtDigitsIn d = crt_split(c);
 #pragma unroll
-                    for (int l = 0; l < 4; ++l)
-                        if (b0 + l < C.nq) w[l] |= crt_digit(c, dg, C, b0 + l) << (8 * e);
+                    for (int l = 0; l < 4; ++l) {
+                        const float sv = fmaf(d.h1, fw[l], d.h0);
+                        const float t = fmaf(sv, fi[l], 12582912.0f) - 12582912.0f;
+                        const float rr = fmaf(-fq[l], t, sv);
+                        const uint32_t byte = q256[l] ? (static_cast<uint32_t>(c) & 0xFFu)
+                                                      : (__float_as_uint(rr + 12582912.0f) & 0xFFu);
+                        w[l] |= byte << (8 * e);
+                    }
                 }
 #pragma unroll
                 for (int l = 0; l < 4; ++l)
-                    if (b0 + l < C.nq) *reinterpret_cast<uint32_t*>(&tile[l][lr][4 * lk + 32 * g]) = w[l];
+                    if (live[l]) *reinterpret_cast<uint32_t*>(&tile[l][lr][4 * lk + 32 * g]) = w[l];
             }
             __syncthreads();
             if (r < rows && kc < k_pad) {

@@ -31,6 +31,7 @@ def test_crt_moduli_cover_the_dot_product_bound(ff, p, k):
     q = info["moduli"]
     assert info["scheme"] == "CRT" and info["L"] == info["nmod"] == info["groups"] == len(q) >= 1
     assert all(2 <= x <= 256 for x in q) and q == sorted(q, reverse=True)
+    assert q[0] == 256                         # the encoders take plane 0 as the low byte
     for i in range(len(q)):
         for j in range(i):
             assert math.gcd(q[i], q[j]) == 1, (q[i], q[j])
