@@ -688,7 +688,7 @@ int launch_impl(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A
             return FF_ERR_CUDA;
         attr_set = true;
     }
-    const int64_t units = num_sms() / kPair;
+    const int64_t units = (num_sms() - pl.reserve_sms) / kPair;
     const int grid = static_cast<int>((nt < units ? nt : units) * kPair);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);

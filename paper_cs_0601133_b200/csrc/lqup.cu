@@ -326,12 +326,13 @@ __global__ void zero_kernel(int32_t* A, int64_t lda, int64_t r0, int64_t r1, int
 
 int gemm_plain(uint32_t p, const ff_opts* opts, char tX, char tY, int64_t m, int64_t n, int64_t k, uint32_t alpha,
                const int32_t* X, int64_t ldx, const int32_t* Y, int64_t ldy, uint32_t beta, int32_t* C, int64_t ldc,
-               void* ws, cudaStream_t st) {
+               void* ws, cudaStream_t st, int reserve_sms = 0) {
     if (m == 0 || n == 0) return 0;
     Plan pl;
     int e = make_plan(p, k, opts, &pl);
     if (e) return e;
     set_scalars(&pl, alpha, beta);
+    pl.reserve_sms = reserve_sms;
     return gemm_dev(pl, tX, tY, m, n, k, X, ldx, Y, ldy, C, ldc, ws, st);
 }
 
@@ -344,8 +345,8 @@ struct LqupWs {
 
 int lqup_ws(uint32_t p, int64_t m, int64_t n, const ff_opts* opts, LqupWs* w) {
     w->win = align256(static_cast<size_t>(kH) * std::max<int64_t>(n, 1) * 8 + static_cast<size_t>(kH) * kH * 8);
-    w->linv = w->uinv = align256(static_cast<size_t>(kH) * kH * 4);
-    w->out = align256((4 + 4 * kMaxSwaps) * 4 + 64);
+    w->linv = w->uinv = align256(2 * static_cast<size_t>(kH) * kH * 4);          // double-buffered (lookahead)
+    w->out = align256(2 * ((4 + 4 * kMaxSwaps) * 4 + 64));
     w->pairs = align256(4 * kMaxSwaps * 8);
     // GEMMs: K <= kH; M <= m, N <= n (a CRT plan for short K has the most planes)
     size_t g = 0;
@@ -429,9 +430,10 @@ int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t* A, int64_t lda, int64_
     uint8_t* ws = static_cast<uint8_t*>(workspace);
     double* win = reinterpret_cast<double*>(ws);
     double* tmpd = win + static_cast<size_t>(kH) * std::max<int64_t>(n, 1);
-    int32_t* Linv = reinterpret_cast<int32_t*>(ws + w.win);
-    int32_t* Uinv = reinterpret_cast<int32_t*>(ws + w.win + w.linv);
-    int32_t* dout = reinterpret_cast<int32_t*>(ws + w.win + w.linv + w.uinv);
+    int32_t* Linv2 = reinterpret_cast<int32_t*>(ws + w.win);
+    int32_t* Uinv2 = reinterpret_cast<int32_t*>(ws + w.win + w.linv);
+    int32_t* dout2 = reinterpret_cast<int32_t*>(ws + w.win + w.linv + w.uinv);
+    const size_t out_stride = ((4 + 4 * kMaxSwaps) * 4 + 64) / 4;
     int64_t* dpairs = reinterpret_cast<int64_t*>(ws + w.win + w.linv + w.uinv + w.out);
     void* gws = ws + w.win + w.linv + w.uinv + w.out + w.pairs;
     std::vector<int32_t> hout(4 + 4 * kMaxSwaps);
@@ -447,7 +449,26 @@ int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t* A, int64_t lda, int64_
     int64_t i0 = 0, c = 0, m_active = m, r = 0;
     int64_t W = std::min<int64_t>(n, kH);
     auto fail_cuda = [&]() { cudaGetLastError(); return FF_ERR_CUDA; };
+    // Lookahead: the panel kernel of the next panel runs on its own stream, on
+    // SMs the big trailing GEMM leaves free (kReserve), as soon as the next
+    // panel's rows are updated; Linv/Uinv/out are double-buffered for that.
+    constexpr int kReserve = 2;
+    cudaStream_t ps = nullptr;
+    cudaEvent_t ev_ready = nullptr, ev_panel = nullptr;
+    if (cudaStreamCreateWithFlags(&ps, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ev_ready, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ev_panel, cudaEventDisableTiming) != cudaSuccess)
+        return fail_cuda();
+    struct Cleanup {
+        cudaStream_t s; cudaEvent_t a, b;
+        ~Cleanup() { cudaStreamSynchronize(s); cudaStreamDestroy(s); cudaEventDestroy(a); cudaEventDestroy(b); }
+    } cleanup{ps, ev_ready, ev_panel};
+    if (cudaEventRecord(ev_ready, st) != cudaSuccess) return fail_cuda();
+    int buf = 0;
     while (i0 < m_active && c < n) {
+        int32_t* Linv = Linv2 + static_cast<size_t>(buf) * kH * kH;
+        int32_t* Uinv = Uinv2 + static_cast<size_t>(buf) * kH * kH;
+        int32_t* dout = dout2 + static_cast<size_t>(buf) * out_stride;
         const int64_t hr = std::min<int64_t>(kH, m_active - i0);
         const int64_t Wc = std::min<int64_t>(W, n - c);
         PanelArgs pa;
@@ -456,12 +477,14 @@ int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t* A, int64_t lda, int64_
         pa.p = p; pa.dp = static_cast<double>(p); pa.invp = 1.0 / static_cast<double>(p);
         pa.mu64 = static_cast<unsigned long long>((static_cast<unsigned __int128>(1) << 64) / p);
         pa.win = win; pa.tmp = tmpd; pa.Linv = Linv; pa.Uinv = Uinv; pa.out = dout;
-        if (Wc <= kH) panel_kernel<true><<<1, kThr, kSmemBytes, st>>>(pa);
-        else panel_kernel<false><<<1, kThr, 0, st>>>(pa);
+        if (cudaStreamWaitEvent(ps, ev_ready, 0) != cudaSuccess) return fail_cuda();
+        if (Wc <= kH) panel_kernel<true><<<1, kThr, kSmemBytes, ps>>>(pa);
+        else panel_kernel<false><<<1, kThr, 0, ps>>>(pa);
         if (cudaGetLastError() != cudaSuccess) return fail_cuda();
-        if (cudaMemcpyAsync(hout.data(), dout, hout.size() * 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
-            cudaStreamSynchronize(st) != cudaSuccess)
+        if (cudaMemcpyAsync(hout.data(), dout, hout.size() * 4, cudaMemcpyDeviceToHost, ps) != cudaSuccess ||
+            cudaEventRecord(ev_panel, ps) != cudaSuccess || cudaStreamSynchronize(ps) != cudaSuccess)
             return fail_cuda();
+        if (cudaStreamWaitEvent(st, ev_panel, 0) != cudaSuccess) return fail_cuda();
         const int64_t kk = hout[0];
         if (getenv("FF_LQUP_TRACE")) {
             long long tt[5];
@@ -473,6 +496,7 @@ int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t* A, int64_t lda, int64_
             W = std::min<int64_t>(n, 4 * Wc);
             continue;
         }
+        buf ^= 1;
         const int ncol = hout[2], nrow = hout[3];
         // column swaps (window coordinates) on all rows outside the panel + bookkeeping
         if (ncol > 0) {
@@ -494,6 +518,8 @@ int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t* A, int64_t lda, int64_
                     A, lda, dpairs, nrow, 0, c);
             }
         }
+        const int64_t z = hr - kk;
+        bool ready_recorded = false;
         if (kk > 0) {
             // U of the pivot rows beyond the window: U_rest = L11^-1 A_rest (in place, beta = 0)
             if (c + Wc < n) {
@@ -501,20 +527,30 @@ int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t* A, int64_t lda, int64_
                 if ((e = gemm_plain(p, opts, 'N', 'N', kk, n - c - Wc, kk, 1, Linv, kH, Ar, lda, 0, Ar, lda, gws, st)))
                     return e;
             }
-            // trailing rows [i0 + hr, m_active): G = X U11^-1, Z <- Z - G U12
-            const int64_t mt = m_active - (i0 + hr);
-            if (mt > 0) {
-                int32_t* X = A + (i0 + hr) * lda + c;
-                if ((e = gemm_plain(p, opts, 'N', 'N', mt, kk, kk, 1, X, lda, Uinv, kH, 0, X, lda, gws, st)))
-                    return e;
-                if (c + kk < n &&
-                    (e = gemm_plain(p, opts, 'N', 'N', mt, n - c - kk, kk, neg1, X, lda, A + i0 * lda + c + kk, lda,
-                                    1, X + kk, lda, gws, st)))
-                    return e;
+            // trailing rows [i0 + hr, m_active): G = X U11^-1, Z <- Z - G U12; without zero
+            // rows the next panel's rows go first and release the next panel kernel
+            auto trailing = [&](int64_t r0, int64_t r1, int reserve) -> int {
+                if (r1 <= r0) return 0;
+                int32_t* X = A + r0 * lda + c;
+                int ee = gemm_plain(p, opts, 'N', 'N', r1 - r0, kk, kk, 1, X, lda, Uinv, kH, 0, X, lda, gws, st, reserve);
+                if (ee) return ee;
+                if (c + kk < n)
+                    ee = gemm_plain(p, opts, 'N', 'N', r1 - r0, n - c - kk, kk, neg1, X, lda, A + i0 * lda + c + kk,
+                                    lda, 1, X + kk, lda, gws, st, reserve);
+                return ee;
+            };
+            const int64_t t0 = i0 + hr;
+            if (z == 0) {
+                const int64_t t1 = std::min<int64_t>(m_active, t0 + kH);
+                if ((e = trailing(t0, t1, 0))) return e;
+                if (cudaEventRecord(ev_ready, st) != cudaSuccess) return fail_cuda();
+                ready_recorded = true;
+                if ((e = trailing(t1, m_active, kReserve))) return e;
+            } else if ((e = trailing(t0, m_active, 0))) {
+                return e;
             }
         }
         // rows of the panel that reduced to zero (full window only): to the bottom of the active rows
-        const int64_t z = hr - kk;
         if (z > 0) {
             zero_kernel<<<dim3(64, static_cast<unsigned>(std::min<int64_t>(z, 1024))), 256, 0, st>>>(
                 A, lda, i0 + kk, i0 + hr, c + kk, n);
@@ -535,6 +571,7 @@ int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t* A, int64_t lda, int64_
             }
             m_active -= z;
         }
+        if (!ready_recorded && cudaEventRecord(ev_ready, st) != cudaSuccess) return fail_cuda();
         i0 += kk;
         c += kk;
         r += kk;
