@@ -94,9 +94,10 @@ typedef struct ff_opts {
                                256x256 CTA-pair (tcgen05 cta_group::2) kernel */
     int32_t host_block;     /* ff_gemm_host only: rows/columns of C per pipelined block
                                (rounded up to 256); 0 = auto (~4096) */
-    int32_t korder;         /* step order of the kernel: 0 auto, 1 group-outer (each weight
-                               group over all of k), 2 k-outer (each k-block through all
-                               groups: L2 locality) */
+    int32_t korder;         /* step order of the kernel: 0 auto (k-outer when the operand
+                               planes exceed ~192 MB, else group-outer), 1 group-outer (each
+                               weight group over all of k), 2 k-outer (each k-block through
+                               all groups: L2 locality) */
     int32_t debug_unchecked_kb; /* test builds only: accept a kb_override above the safe
                                bound (to show that the bound is needed); results are then
                                not guaranteed */

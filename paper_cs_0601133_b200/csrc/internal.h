@@ -67,6 +67,8 @@ struct Plan {
     int force_pair;                  // 0 auto, 1 single-CTA kernel, 2 CTA-pair kernel
     int reserve_sms;                 // leave this many SMs free (LQUP lookahead: a panel kernel co-runs)
     int korder;                      // 1 group-outer, 2 k-outer step order
+    bool korder_auto;                // k-outer chosen by default (no option, no kb_override):
+                                     // the launch may fall back to group-outer for L2-sized operands
     uint32_t kinv, kinv_sh;          // 256^-(G-1) mod p and its Shoup constant (k-outer carry)
 };
 

@@ -259,7 +259,8 @@ int make_limb_plan(uint32_t p, int64_t k, const ff_opts& o, int64_t half, int64_
     I.kb_max = bmax > 0 ? (((int64_t)1 << 31) - 1 - carry) / bmax : ((int64_t)1 << 40);
     // Step order: k-outer needs 256 invertible mod p when there are several groups.
     int korder = o.korder == 0 ? 2 : o.korder;
-    if (const char* e = getenv("FF_KORDER")) korder = atoi(e) == 1 ? 1 : 2;  // experiment only
+    pl.korder_auto = (o.korder == 0 && o.kb_override == 0);
+    if (const char* e = getenv("FF_KORDER")) { korder = atoi(e) == 1 ? 1 : 2; pl.korder_auto = false; }  // experiment only
     if (korder == 2 && L > 1 && (p % 2) == 0) korder = 1;
     pl.korder = korder;
     I.korder = korder;
