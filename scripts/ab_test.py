@@ -57,7 +57,7 @@ def main():
     ff.ff_fill_uniform(A, *cfg.a_shape, cfg.a_shape[1], cfg.p, cfg.seed, 0)
     ff.ff_fill_uniform(B, *cfg.b_shape, cfg.b_shape[1], cfg.p, cfg.seed, 1)
     info = ff.ff_plan_query(cfg.p, cfg.k)
-    ops = cfg.useful_ops() * info["L"] ** 2
+    ops = cfg.useful_ops() * (info["L"] if info["scheme"] == "CRT" else info["L"] ** 2)
     ref = None
     for rnd in range(rounds):
         for vi, opts in enumerate(variants):

@@ -43,7 +43,7 @@ def main(names, reps=5):
             ts.append(e0.elapsed_time(e1))
         t = min(ts) / 1e3
         useful = 2.0 * m * n * k
-        mma = useful * info["L"] ** 2
+        mma = useful * (info["L"] if info["scheme"] == "CRT" else info["L"] ** 2)   # int8 products per output
         print("%s p=%d L=%d  t=%.3f ms  useful %.1f TOPS  int8-MMA %.1f TOPS (%.1f%% of 3305)" % (
             name, p, info["L"], t * 1e3, useful / t / 1e12, mma / t / 1e12, 100 * mma / t / 3.305e15),
             flush=True)
