@@ -369,9 +369,10 @@ int ff_trsm_ex(uint32_t p, char side, char uplo, char transA, char diag, int64_t
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     Plan pl0;
     if ((e = make_plan(p, 1, opts, &pl0))) return e;
-    // B <- alpha B mod p (also brings every entry to [0, p)); alpha = 0 gives X = 0.
+    // B <- alpha B mod p; alpha = 0 gives X = 0.  Skipped for alpha = 1: every
+    // read of B below reduces it (the encoders, and the beta = 1 epilogue).
     set_scalars(&pl0, 1, alpha);
-    if (launch_scale_c(pl0.mp, m, n, B, ldb, st) != cudaSuccess) return FF_ERR_CUDA;
+    if (pl0.mp.beta != 1 % p && launch_scale_c(pl0.mp, m, n, B, ldb, st) != cudaSuccess) return FF_ERR_CUDA;
     if (pl0.mp.beta == 0) return 0;
     uint8_t* ws = static_cast<uint8_t*>(workspace);
     Ctx c;

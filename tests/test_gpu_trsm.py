@@ -81,7 +81,8 @@ def test_trsm_medium_vs_oracle(env, p, side, uplo, trans, diag, m, n):
     rng = np.random.default_rng(m * 7 + n)
     d = m if side == "L" else n
     A = _tri(rng, p, d, uplo, diag)
-    B = rng.integers(0, p, size=(m, n)).astype(np.int32)
+    # alpha = 1 skips the scaling pass: B may be any int32 (reduced where it is read)
+    B = rng.integers(-2 ** 31, 2 ** 31, size=(m, n), dtype=np.int64).astype(np.int32)
     got = _run(torch, ff, p, side, uplo, trans, diag, 1, A, B)
     np.testing.assert_array_equal(got, oracle.trsm(p, side, uplo, trans, diag, 1, A, B))
 
