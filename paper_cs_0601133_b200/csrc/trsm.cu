@@ -45,59 +45,82 @@ struct InvArgs {
     int32_t* W;                     // out: [nblk][kNb][kNb] inverses of the diagonal blocks of A
 };
 
-__device__ int64_t inv_mod_dev(int64_t a, int64_t p) {
-    int64_t r0 = p, r1 = a % p, s0 = 0, s1 = 1;
+__device__ uint32_t inv32(uint32_t a, uint32_t p) {        // a^-1 mod p, extended Euclid in 32 bits
+    int32_t r0 = static_cast<int32_t>(p), r1 = static_cast<int32_t>(a), s0 = 0, s1 = 1;
     while (r1 != 0) {
-        const int64_t q = r0 / r1, t = r0 - q * r1, u = s0 - q * s1;
+        const int32_t q = r0 / r1, t = r0 - q * r1, u = s0 - q * s1;
         r0 = r1; r1 = t; s0 = s1; s1 = u;
     }
-    return ((s0 % p) + p) % p;      // 0 if not invertible (singular: result undefined, as BLAS)
+    return static_cast<uint32_t>(s0 < 0 ? s0 + static_cast<int32_t>(p) : s0);
 }
 
-// One CTA per diagonal block D (db x db, db <= kNb): thread j computes column j
-// of W = D^{-1} by substitution, W_ij = (delta_ij - sum_l D_il W_lj) D_ii^{-1}.
-__global__ void __launch_bounds__(kNb) trsm_diag_inv_kernel(InvArgs a) {
+constexpr int kInvThreads = 1024;
+constexpr int kInvSmem = (2 * kNb * kNb + kNb) * 4;
+
+// One CTA (32 x 32 threads) per diagonal block D (db x db, db <= kNb):
+// W = D^-1 by Gauss-Jordan phases on [D | I] (D and the identity in shared
+// memory).  Upper D: for k = db-1 .. 1, rows r < k: E_r -= (D_rk / D_kk) E_k
+// (the multipliers use the original D: eliminating columns to the right of k
+// never changes column k); then W_k = E_k / D_kk.  Lower D mirrors it.  One
+// barrier per phase; the dependent chain per phase is a single product.
+__global__ void __launch_bounds__(kInvThreads) trsm_diag_inv_kernel(InvArgs a) {
     extern __shared__ uint32_t sm[];
-    uint32_t* D = sm;                    // [kNb][kNb + 1], residues
-    uint32_t* Wt = sm + kNb * (kNb + 1); // [kNb][kNb + 1], W transposed (column j at row j)
-    uint32_t* dinv = Wt + kNb * (kNb + 1);
+    uint32_t* D = sm;                    // [kNb][kNb]
+    uint32_t* E = sm + kNb * kNb;        // [kNb][kNb]
+    uint32_t* dinv = E + kNb * kNb;      // [kNb]
     const int64_t r0 = static_cast<int64_t>(blockIdx.x) * kNb;
     const int db = static_cast<int>(a.d - r0 < kNb ? a.d - r0 : kNb);
-    const int j = threadIdx.x;
+    const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
     const uint32_t p = a.p;
-    for (int i = 0; i < db; ++i) {
-        if (j < db) {
-            const int32_t x = a.A[(r0 + i) * a.lda + r0 + j];
-            const int64_t r = ((static_cast<int64_t>(x) % p) + p) % p;
-            const bool inside = a.upper ? (j > i) : (j < i);
-            D[i * (kNb + 1) + j] = inside ? static_cast<uint32_t>(r) : 0u;
-            if (i == j) dinv[i] = a.unit ? 1u : static_cast<uint32_t>(inv_mod_dev(r, p));
+    for (int e = tid; e < kNb * kNb; e += kInvThreads) {
+        const int i = e / kNb, j = e % kNb;
+        uint32_t v = 0;
+        if (i < db && j < db) {
+            const bool inside = a.upper ? (j >= i) : (j <= i);
+            if (inside) {
+                const int64_t x = static_cast<int64_t>(a.A[(r0 + i) * a.lda + r0 + j]) % static_cast<int64_t>(p);
+                v = static_cast<uint32_t>(x < 0 ? x + p : x);
+            }
         }
+        D[e] = v;
+        E[e] = (i == j && i < db) ? 1u : 0u;
     }
     __syncthreads();
-    if (j < db) {
-        uint32_t* w = Wt + j * (kNb + 1);
-        for (int s = 0; s < db; ++s) {
-            // upper: rows i = j, j-1, ..., 0 (W upper); lower: rows i = j, ..., db-1
-            const int i = a.upper ? j - s : j + s;
-            if (i < 0 || i >= db) { continue; }
-            unsigned long long acc = (i == j) ? 1ull : 0ull;      // delta_ij
-            unsigned long long sub = 0;
-            const int l0 = a.upper ? i + 1 : j, l1 = a.upper ? j + 1 : i;   // l with D_il, W_lj both nonzero
-            for (int l = l0; l < l1; ++l) {
-                sub = residue_u64(sub + static_cast<unsigned long long>(D[i * (kNb + 1) + l]) * w[l], a.mu64, p);
+    for (int i = tid; i < db; i += kInvThreads) dinv[i] = a.unit ? 1u : inv32(D[i * kNb + i], p);
+    __syncthreads();
+    if (a.upper) {
+        for (int k = db - 1; k >= 1; --k) {
+            for (int r = ty; r < k; r += 32) {
+                const uint32_t d = D[r * kNb + k];
+                if (d == 0u) continue;
+                const uint32_t mlt = residue_u64(static_cast<unsigned long long>(d) * dinv[k], a.mu64, p);
+                for (int c = k + tx; c < db; c += 32) {
+                    const uint32_t t = residue_u64(static_cast<unsigned long long>(mlt) * E[k * kNb + c], a.mu64, p);
+                    const uint32_t x = E[r * kNb + c];
+                    E[r * kNb + c] = x >= t ? x - t : x + p - t;
+                }
             }
-            const uint32_t v = static_cast<uint32_t>((acc + p - sub) % p);
-            w[i] = residue_u64(static_cast<unsigned long long>(v) * dinv[i], a.mu64, p);
-        }
-        for (int i = 0; i < kNb; ++i) {
-            const bool nz = i < db && (a.upper ? i <= j : i >= j);
-            a.W[static_cast<int64_t>(blockIdx.x) * kNb * kNb + static_cast<int64_t>(i) * kNb + j] =
-                nz ? static_cast<int32_t>(w[i]) : 0;
+            __syncthreads();
         }
     } else {
-        for (int i = 0; i < kNb; ++i)
-            a.W[static_cast<int64_t>(blockIdx.x) * kNb * kNb + static_cast<int64_t>(i) * kNb + j] = 0;
+        for (int k = 0; k + 1 < db; ++k) {
+            for (int r = k + 1 + ty; r < db; r += 32) {
+                const uint32_t d = D[r * kNb + k];
+                if (d == 0u) continue;
+                const uint32_t mlt = residue_u64(static_cast<unsigned long long>(d) * dinv[k], a.mu64, p);
+                for (int c = tx; c <= k; c += 32) {
+                    const uint32_t t = residue_u64(static_cast<unsigned long long>(mlt) * E[k * kNb + c], a.mu64, p);
+                    const uint32_t x = E[r * kNb + c];
+                    E[r * kNb + c] = x >= t ? x - t : x + p - t;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    int32_t* W = a.W + static_cast<int64_t>(blockIdx.x) * kNb * kNb;
+    for (int e = tid; e < kNb * kNb; e += kInvThreads) {
+        const int i = e / kNb;
+        W[e] = (i < db) ? static_cast<int32_t>(residue_u64(static_cast<unsigned long long>(E[e]) * dinv[i], a.mu64, p)) : 0;
     }
 }
 
@@ -402,7 +425,7 @@ int ff_trsm_ex(uint32_t p, char side, char uplo, char transA, char diag, int64_t
     ia.p = p;
     ia.mu64 = static_cast<unsigned long long>((static_cast<unsigned __int128>(1) << 64) / p);
     ia.W = reinterpret_cast<int32_t*>(ws + w.lvl_off[0]);
-    const size_t smem = (2 * kNb * (kNb + 1) + kNb) * sizeof(uint32_t);
+    const size_t smem = kInvSmem;
     static bool attr = false;
     if (!attr) {
         if (cudaFuncSetAttribute(trsm_diag_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
@@ -410,7 +433,7 @@ int ff_trsm_ex(uint32_t p, char side, char uplo, char transA, char diag, int64_t
             return FF_ERR_CUDA;
         attr = true;
     }
-    trsm_diag_inv_kernel<<<static_cast<unsigned>((d + kNb - 1) / kNb), kNb, smem, st>>>(ia);
+    trsm_diag_inv_kernel<<<static_cast<unsigned>((d + kNb - 1) / kNb), kInvThreads, smem, st>>>(ia);
     if (cudaGetLastError() != cudaSuccess) return FF_ERR_CUDA;
     // double the inverted blocks up to kLeaf: W_s = [W1, X; 0, W3] (upper)
     int32_t* T = reinterpret_cast<int32_t*>(ws + w.w_bytes);
