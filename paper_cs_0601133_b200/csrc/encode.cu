@@ -12,10 +12,14 @@
 // HBM-bound: each element is read once (4 B) and written once per limb (L B).
 // Both kernels are templated on (L, scheme) so the digits live in registers,
 // and both write whole 128-byte lines of every limb plane per warp.
+#include <cuda.h>
 #include <cuda_runtime.h>
+
+#include <cstdlib>
 
 #include "internal.h"
 #include "modp.cuh"
+#include "ptx.cuh"
 
 namespace ff {
 
@@ -132,6 +136,112 @@ __global__ void __launch_bounds__(256) encode_trans_kernel(ModP M, int64_t rows,
             }
         }
     }
+}
+
+// TMA-fed variant of the transposed encoder (limb schemes): tiles of 128 k-rows
+// x 32 columns of X (16 KB) stream into a 4-stage shared-memory ring by TMA
+// (one thread issues, zero fill beyond the matrix = the K padding), so the
+// loads no longer wait on the per-thread load latency.  Thread (r, kg) reads
+// the 16 values X[kg*16 .. +16][r] of its row r (bank r: conflict-free), packs
+// their digits and stages them as [L][32][132] bytes; whole 128-byte limb rows
+// are then written as before.
+constexpr int kTmaStages = 4;
+constexpr int kTmaTileBytes = kTK * kTR * 4;     // 128 k-rows x 32 columns of int32
+constexpr int kTmaSmem = kTmaStages * kTmaTileBytes + 4 * kTR * kPitch + 2 * kTmaStages * 8 + 1024;
+
+template <int L, int SCHEME>
+__global__ void __launch_bounds__(256) encode_trans_tma_kernel(const __grid_constant__ CUtensorMap tmX, ModP M,
+                                                               int64_t rows, int64_t k_pad,
+                                                               int8_t* __restrict__ limbs) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int32_t* ring = reinterpret_cast<const int32_t*>(sm);
+    uint8_t (*tile)[kTR][kPitch] = reinterpret_cast<uint8_t (*)[kTR][kPitch]>(sm + kTmaStages * kTmaTileBytes);
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + kTmaStages * kTmaTileBytes + 4 * kTR * kPitch);
+    uint64_t* empty = full + kTmaStages;
+    const int64_t plane = rows * k_pad;
+    const int64_t tiles_r = (rows + kTR - 1) / kTR;
+    const int64_t tiles_k = (k_pad + kTK - 1) / kTK;
+    const int64_t ntiles = tiles_r * tiles_k;
+    const int tid = threadIdx.x, r = tid % kTR, kg = tid / kTR;          // kg: 16 k-values each
+    const int wr = (tid / 32) * 4 + (tid % 32) / 8, wc = (tid % 8) * 16;
+    if (tid == 0) {
+        for (int s = 0; s < kTmaStages; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 256); }
+        ptx::fence_barrier_init();
+    }
+    __syncthreads();
+    const uint64_t pol = ptx::policy_evict_normal();
+    auto issue = [&](int64_t j) {                       // j-th tile of this CTA into stage j % S
+        const int64_t t = blockIdx.x + j * gridDim.x;
+        const int s = static_cast<int>(j % kTmaStages);
+        ptx::mbar_arrive_expect_tx(&full[s], kTmaTileBytes);
+        ptx::tma_load_2d(const_cast<int32_t*>(ring) + s * (kTmaTileBytes / 4), &tmX, &full[s],
+                         static_cast<int32_t>((t % tiles_r) * kTR), static_cast<int32_t>((t / tiles_r) * kTK), pol);
+    };
+    const int64_t mine = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+    if (tid == 0)
+        for (int64_t j = 0; j < kTmaStages && j < mine; ++j) issue(j);
+    for (int64_t j = 0; j < mine; ++j) {
+        const int64_t t = blockIdx.x + j * gridDim.x;
+        const int s = static_cast<int>(j % kTmaStages);
+        const uint32_t par = static_cast<uint32_t>((j / kTmaStages) & 1);
+        ptx::mbar_wait(&full[s], par);
+        const int32_t* T = ring + s * (kTmaTileBytes / 4);     // [128][32]
+        uint32_t w[4][L];
+#pragma unroll
+        for (int g = 0; g < 4; ++g)
+#pragma unroll
+            for (int l = 0; l < L; ++l) w[g][l] = 0;
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+            put_digits<L, SCHEME>(centre(residue_i32(T[(kg * 16 + i) * kTR + r], M), M), i & 3, w[i >> 2]);
+        ptx::mbar_arrive(&empty[s]);                            // this stage may be refilled
+        if (tid == 0 && j + kTmaStages < mine) {
+            ptx::mbar_wait(&empty[s], par);
+            issue(j + kTmaStages);
+        }
+        __syncthreads();                                        // previous tile's write-out done with `tile`
+#pragma unroll
+        for (int l = 0; l < L; ++l)
+#pragma unroll
+            for (int g = 0; g < 4; ++g) *reinterpret_cast<uint32_t*>(&tile[l][r][kg * 16 + 4 * g]) = w[g][l];
+        __syncthreads();
+        const int64_t rr = (t % tiles_r) * kTR + wr;
+        const int64_t kc = (t / tiles_r) * kTK + wc;
+        if (rr < rows && kc < k_pad) {
+            int8_t* dst = limbs + rr * k_pad + kc;
+#pragma unroll
+            for (int l = 0; l < L; ++l) {
+                const uint32_t* src = reinterpret_cast<const uint32_t*>(&tile[l][wr][wc]);
+                *reinterpret_cast<uint4*>(dst + l * plane) = make_uint4(src[0], src[1], src[2], src[3]);
+            }
+        }
+    }
+}
+
+typedef CUresult (*EncodeTiledFnE)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// X stored [k][ld] int32 (the transposed source) as a 2-D tensor map, box 32 x 128.
+bool make_src_map(CUtensorMap* map, const int32_t* X, int64_t rows, int64_t k, int64_t ldx) {
+    static EncodeTiledFnE fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return false;
+        fn = reinterpret_cast<EncodeTiledFnE>(p);
+    }
+    if ((reinterpret_cast<uintptr_t>(X) & 15) || ((ldx * 4) % 16) || rows <= 0 || k <= 0) return false;
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(k)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldx * 4)};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(kTR), static_cast<cuuint32_t>(kTK)};
+    cuuint32_t estr[2] = {1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_INT32, 2, const_cast<int32_t*>(X), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // ---- multi-modular (CRT) planes: plane i holds the centred
@@ -351,6 +461,20 @@ void launch_encode_t(const Plan& pl, int kmajor_src, int64_t rows, int64_t k, in
             pl.mp, rows, k, k_pad, X, ldx, limbs, vec_ok);
     } else {
         const int64_t tiles = ((rows + kTR - 1) / kTR) * ((k_pad + kTK - 1) / kTK);
+        CUtensorMap map;
+        static const bool no_tma = getenv("FF_ENC_NOTMA") != nullptr;    // experiment: the LSU-load version
+        if (!no_tma && make_src_map(&map, X, rows, k, ldx)) {
+            static bool attr = false;
+            if (!attr) {
+                cudaFuncSetAttribute(encode_trans_tma_kernel<L, SCHEME>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kTmaSmem);
+                attr = true;
+            }
+            const int64_t cap = (int64_t)num_sms() * 2;
+            encode_trans_tma_kernel<L, SCHEME><<<static_cast<int>(tiles < cap ? tiles : cap), 256, kTmaSmem, st>>>(
+                map, pl.mp, rows, k_pad, limbs);
+            return;
+        }
         const int64_t cap = (int64_t)num_sms() * 8;
         encode_trans_kernel<L, SCHEME><<<static_cast<int>(tiles < cap ? tiles : cap), 256, 0, st>>>(
             pl.mp, rows, k, k_pad, X, ldx, limbs);
