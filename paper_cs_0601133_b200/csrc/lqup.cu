@@ -164,34 +164,35 @@ __global__ void __launch_bounds__(kThr) panel_kernel(PanelArgs P) {
             __syncthreads();                       // (everyone has read s_j before the next search)
             continue;                              // a zero row (stays below the pivot rows)
         }
-        // column swap kk <-> j (all panel rows) and row swap i <-> kk, disjoint cells first
-        if (j != kk)
-            for (int64_t r = tid; r < hr; r += kThr) {
-                const uint32_t t = w[r * W + kk]; w[r * W + kk] = w[r * W + j]; w[r * W + j] = t;
-            }
-        if (i != kk) {
-            for (int64_t cc = tid; cc < W; cc += kThr) {
-                if (cc == kk || cc == j) continue;
-                const uint32_t t = w[i * W + cc]; w[i * W + cc] = w[kk * W + cc]; w[kk * W + cc] = t;
-            }
-            for (int c = tid; c < kH; c += kThr) {     // E rows follow (rows i, kk)
-                const uint32_t t = E[i * kH + c]; E[i * kH + c] = E[kk * kH + c]; E[kk * kH + c] = t;
-            }
-        }
-        __syncthreads();
-        if (tid == 0) {
-            if (i != kk) {                         // the swapped columns of the swapped rows
-                uint32_t t = w[i * W + kk]; w[i * W + kk] = w[kk * W + kk]; w[kk * W + kk] = t;
-                if (j != kk) { t = w[i * W + j]; w[i * W + j] = w[kk * W + j]; w[kk * W + j] = t; }
-            }
-            if (j != kk) { colsw[s_ncol][0] = kk; colsw[s_ncol][1] = j; ++s_ncol; }
+        if (j != kk || i != kk) {                  // (uniform: rare for generic inputs)
+            // column swap kk <-> j (all panel rows) and row swap i <-> kk, disjoint cells first
+            if (j != kk)
+                for (int64_t r = tid; r < hr; r += kThr) {
+                    const uint32_t t = w[r * W + kk]; w[r * W + kk] = w[r * W + j]; w[r * W + j] = t;
+                }
             if (i != kk) {
-                rowsw[s_nrow][0] = kk; rowsw[s_nrow][1] = static_cast<int>(i); ++s_nrow;
-                const int t = orig[kk]; orig[kk] = orig[i]; orig[i] = t;
+                for (int64_t cc = tid; cc < W; cc += kThr) {
+                    if (cc == kk || cc == j) continue;
+                    const uint32_t t = w[i * W + cc]; w[i * W + cc] = w[kk * W + cc]; w[kk * W + cc] = t;
+                }
+                for (int c = tid; c < kH; c += kThr) {     // E rows follow (rows i, kk)
+                    const uint32_t t = E[i * kH + c]; E[i * kH + c] = E[kk * kH + c]; E[kk * kH + c] = t;
+                }
             }
-            s_j = INT32_MAX;
+            __syncthreads();
+            if (tid == 0) {
+                if (i != kk) {                         // the swapped columns of the swapped rows
+                    uint32_t t = w[i * W + kk]; w[i * W + kk] = w[kk * W + kk]; w[kk * W + kk] = t;
+                    if (j != kk) { t = w[i * W + j]; w[i * W + j] = w[kk * W + j]; w[kk * W + j] = t; }
+                }
+                if (j != kk) { colsw[s_ncol][0] = kk; colsw[s_ncol][1] = j; ++s_ncol; }
+                if (i != kk) {
+                    rowsw[s_nrow][0] = kk; rowsw[s_nrow][1] = static_cast<int>(i); ++s_nrow;
+                    const int t = orig[kk]; orig[kk] = orig[i]; orig[i] = t;
+                }
+            }
+            __syncthreads();
         }
-        __syncthreads();
         const uint32_t pk = w[kk * W + kk];
         const uint32_t pk_sh = shoup_c(pk, p, c32);
         if (tid == 0) piv[kk] = pk;
@@ -211,7 +212,7 @@ __global__ void __launch_bounds__(kThr) panel_kernel(PanelArgs P) {
                 if (tx == 0) E[r * kH + r] = shoup_m(E[r * kH + r], pk, pk_sh, p);   // (E_kk has no column r)
             }
         }
-        if (tid == 0) s_kk = kk + 1;
+        if (tid == 0) { s_kk = kk + 1; s_j = INT32_MAX; }   // (all threads read s_j before the update)
         __syncthreads();
     }
     const int kk = s_kk;
