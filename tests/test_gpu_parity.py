@@ -324,13 +324,14 @@ def test_identity_permutation_on_gpu(env):
     np.testing.assert_array_equal(got, B[sigma])
 
 
-@pytest.mark.parametrize("tA,tB,beta,block", [("T", "N", 1, 0), ("N", "N", 0, 256), ("T", "T", 5, 256),
-                                               ("N", "T", 0, 512)])
-def test_host_entry_point(env, tA, tB, beta, block):
+@pytest.mark.parametrize("tA,tB,beta,block,p", [("T", "N", 1, 0, 8388593), ("N", "N", 0, 256, 8388593),
+                                                 ("T", "T", 5, 256, 8388593), ("N", "T", 0, 512, 8388593),
+                                                 ("N", "N", 3, 256, 67108859), ("T", "N", 0, 0, 67108859)])
+def test_host_entry_point(env, tA, tB, beta, block, p):
     """ff_gemm_host: host buffers, pipelined over blocks of C (block=256 forces
-    several row panels and column chunks, with ragged last blocks)."""
+    several row panels and column chunks, with ragged last blocks); p = 67108859
+    runs the multi-modular (CRT) plan through the same pipeline."""
     torch, ff = env
-    p = 8388593
     rng = np.random.default_rng(5 + block)
     m, n, k = 700, 900, 555
     A = _stored(rng, *((m, k) if tA == "N" else (k, m)), p, 1)
