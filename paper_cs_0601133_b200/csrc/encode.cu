@@ -276,50 +276,57 @@ __device__ __forceinline__ uint32_t crt_digit(int32_t c, const CrtDigitsIn& d, c
     return __float_as_uint(r + 12582912.0f) & 0xFFu;
 }
 
+// 16 consecutive elements per thread: four 16-byte loads, one 16-byte store per
+// plane (the per-element residue arithmetic dominates; wide accesses amortise
+// the address and store instructions).
 __global__ void __launch_bounds__(256) encode_crt_direct_kernel(ModP M, CrtConsts C, int64_t rows, int64_t k,
                                                                 int64_t k_pad, const int32_t* __restrict__ X,
                                                                 int64_t ldx, int8_t* __restrict__ planes,
                                                                 int vec_ok) {
-    const int64_t groups = k_pad / 4;
+    const int64_t groups = k_pad / 16;
     const int64_t plane = rows * k_pad;
     for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
         const int32_t* src = X + r * ldx;
-        uint32_t* dst = reinterpret_cast<uint32_t*>(planes + r * k_pad);
         for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < groups;
              g += (int64_t)gridDim.x * blockDim.x) {
-            const int64_t kk = 4 * g;
-            int32_t c[4];
-            if (vec_ok && kk + 4 <= k) {
-                const int4 v = __ldg(reinterpret_cast<const int4*>(src + kk));
-                c[0] = v.x; c[1] = v.y; c[2] = v.z; c[3] = v.w;
+            const int64_t kk = 16 * g;
+            int32_t c[16];
+            if (vec_ok && kk + 16 <= k) {
+#pragma unroll
+                for (int v4 = 0; v4 < 4; ++v4) {
+                    const int4 v = __ldg(reinterpret_cast<const int4*>(src + kk) + v4);
+                    c[4 * v4] = v.x; c[4 * v4 + 1] = v.y; c[4 * v4 + 2] = v.z; c[4 * v4 + 3] = v.w;
+                }
             } else {
 #pragma unroll
-                for (int t = 0; t < 4; ++t) c[t] = (kk + t < k) ? __ldg(src + kk + t) : 0;
+                for (int t = 0; t < 16; ++t) c[t] = (kk + t < k) ? __ldg(src + kk + t) : 0;
             }
-            CrtDigitsIn dg[4];
+            CrtDigitsIn dg[16];
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
+            for (int t = 0; t < 16; ++t) {
                 c[t] = centre(residue_i32(c[t], M), M);
                 dg[t] = crt_split(c[t]);
             }
-            uint32_t* dst = reinterpret_cast<uint32_t*>(planes + r * k_pad);
+            int8_t* dst = planes + r * k_pad + kk;
             // plane 0 is q = 256 (the planner picks 256 first): the low byte of c
-            dst[g] = (static_cast<uint32_t>(c[0]) & 0xFFu) | ((static_cast<uint32_t>(c[1]) & 0xFFu) << 8) |
-                     ((static_cast<uint32_t>(c[2]) & 0xFFu) << 16) | (static_cast<uint32_t>(c[3]) << 24);
+            uint32_t w0[4];
 #pragma unroll
-            for (int i = 1; i < kMaxMod; ++i) {
-                if (i < C.nq) {
-                    const float fq = C.fq[i], fi = C.finv[i], fw = C.fw15[i];
-                    uint32_t w = 0;
+            for (int q4 = 0; q4 < 4; ++q4)
+                w0[q4] = (static_cast<uint32_t>(c[4 * q4]) & 0xFFu) | ((static_cast<uint32_t>(c[4 * q4 + 1]) & 0xFFu) << 8) |
+                         ((static_cast<uint32_t>(c[4 * q4 + 2]) & 0xFFu) << 16) | (static_cast<uint32_t>(c[4 * q4 + 3]) << 24);
+            *reinterpret_cast<uint4*>(dst) = make_uint4(w0[0], w0[1], w0[2], w0[3]);
+#pragma unroll 1
+            for (int i = 1; i < C.nq; ++i) {
+                const float fq = C.fq[i], fi = C.finv[i], fw = C.fw15[i];
+                uint32_t w[4] = {0, 0, 0, 0};
 #pragma unroll
-                    for (int t = 0; t < 4; ++t) {
-                        const float sv = fmaf(dg[t].h1, fw, dg[t].h0);
-                        const float tq = fmaf(sv, fi, 12582912.0f) - 12582912.0f;
-                        const float rr = fmaf(-fq, tq, sv);
-                        w |= (__float_as_uint(rr + 12582912.0f) & 0xFFu) << (8 * t);
-                    }
-                    dst[g + i * (plane / 4)] = w;
+                for (int t = 0; t < 16; ++t) {
+                    const float sv = fmaf(dg[t].h1, fw, dg[t].h0);
+                    const float tq = fmaf(sv, fi, 12582912.0f) - 12582912.0f;
+                    const float rr = fmaf(-fq, tq, sv);
+                    w[t >> 2] |= (__float_as_uint(rr + 12582912.0f) & 0xFFu) << (8 * (t & 3));
                 }
+                *reinterpret_cast<uint4*>(dst + i * plane) = make_uint4(w[0], w[1], w[2], w[3]);
             }
         }
     }
@@ -489,7 +496,7 @@ cudaError_t launch_encode(const Plan& pl, int kmajor_src, int64_t rows, int64_t 
     if (rows == 0 || k_pad == 0) return cudaSuccess;
     if (pl.crt) {
         if (kmajor_src) {
-            const int64_t groups = k_pad / 4;
+            const int64_t groups = k_pad / 16;
             int gx = static_cast<int>((groups + 255) / 256);
             if (gx > 64) gx = 64;
             int64_t gy = (int64_t)num_sms() * 8 / gx;
