@@ -417,6 +417,97 @@ __global__ void __launch_bounds__(256) encode_crt_trans_kernel(ModP M, CrtConsts
     }
 }
 
+// TMA-fed transposed CRT encoder: as encode_trans_tma_kernel, all n_q planes
+// staged at once ([n_q][32][132] bytes) so each tile needs two barriers, and
+// the per-plane constants are loaded once per plane.
+constexpr int kCrtStages = 2;   // 2 CTAs per SM: the residue arithmetic needs the warps
+constexpr int kCrtTmaSmem = kCrtStages * kTmaTileBytes + kMaxMod * kTR * kPitch + 2 * kCrtStages * 8 + 1024;
+
+__global__ void __launch_bounds__(256) encode_crt_trans_tma_kernel(const __grid_constant__ CUtensorMap tmX, ModP M,
+                                                                   CrtConsts C, int64_t rows, int64_t k_pad,
+                                                                   int8_t* __restrict__ planes) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int32_t* ring = reinterpret_cast<const int32_t*>(sm);
+    uint8_t (*tile)[kTR][kPitch] = reinterpret_cast<uint8_t (*)[kTR][kPitch]>(sm + kCrtStages * kTmaTileBytes);
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + kCrtStages * kTmaTileBytes + kMaxMod * kTR * kPitch);
+    uint64_t* empty = full + kCrtStages;
+    const int64_t plane = rows * k_pad;
+    const int64_t tiles_r = (rows + kTR - 1) / kTR;
+    const int64_t tiles_k = (k_pad + kTK - 1) / kTK;
+    const int64_t ntiles = tiles_r * tiles_k;
+    const int tid = threadIdx.x, r = tid % kTR, kg = tid / kTR;
+    const int wr = (tid / 32) * 4 + (tid % 32) / 8, wc = (tid % 8) * 16;
+    const int nq = C.nq;
+    if (tid == 0) {
+        for (int s = 0; s < kCrtStages; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 256); }
+        ptx::fence_barrier_init();
+    }
+    __syncthreads();
+    const uint64_t pol = ptx::policy_evict_normal();
+    auto issue = [&](int64_t j) {
+        const int64_t t = blockIdx.x + j * gridDim.x;
+        const int s = static_cast<int>(j % kCrtStages);
+        ptx::mbar_arrive_expect_tx(&full[s], kTmaTileBytes);
+        ptx::tma_load_2d(const_cast<int32_t*>(ring) + s * (kTmaTileBytes / 4), &tmX, &full[s],
+                         static_cast<int32_t>((t % tiles_r) * kTR), static_cast<int32_t>((t / tiles_r) * kTK), pol);
+    };
+    const int64_t mine = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+    if (tid == 0)
+        for (int64_t j = 0; j < kCrtStages && j < mine; ++j) issue(j);
+    for (int64_t j = 0; j < mine; ++j) {
+        const int64_t t = blockIdx.x + j * gridDim.x;
+        const int s = static_cast<int>(j % kCrtStages);
+        const uint32_t par = static_cast<uint32_t>((j / kCrtStages) & 1);
+        ptx::mbar_wait(&full[s], par);
+        const int32_t* T = ring + s * (kTmaTileBytes / 4);
+        int32_t c[16];
+        CrtDigitsIn dg[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            c[i] = centre(residue_i32(T[(kg * 16 + i) * kTR + r], M), M);
+            dg[i] = crt_split(c[i]);
+        }
+        ptx::mbar_arrive(&empty[s]);
+        if (tid == 0 && j + kCrtStages < mine) {
+            ptx::mbar_wait(&empty[s], par);
+            issue(j + kCrtStages);
+        }
+        __syncthreads();                                  // previous tile's write-out is done with `tile`
+        {   // plane 0: q = 256, the low byte of c
+#pragma unroll
+            for (int g = 0; g < 4; ++g)
+                *reinterpret_cast<uint32_t*>(&tile[0][r][kg * 16 + 4 * g]) =
+                    (static_cast<uint32_t>(c[4 * g]) & 0xFFu) | ((static_cast<uint32_t>(c[4 * g + 1]) & 0xFFu) << 8) |
+                    ((static_cast<uint32_t>(c[4 * g + 2]) & 0xFFu) << 16) | (static_cast<uint32_t>(c[4 * g + 3]) << 24);
+        }
+#pragma unroll 1
+        for (int pl = 1; pl < nq; ++pl) {
+            const float fq = C.fq[pl], fi = C.finv[pl], fw = C.fw15[pl];
+            uint32_t w[4] = {0, 0, 0, 0};
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const float sv = fmaf(dg[i].h1, fw, dg[i].h0);
+                const float tq = fmaf(sv, fi, 12582912.0f) - 12582912.0f;
+                const float rr = fmaf(-fq, tq, sv);
+                w[i >> 2] |= (__float_as_uint(rr + 12582912.0f) & 0xFFu) << (8 * (i & 3));
+            }
+#pragma unroll
+            for (int g = 0; g < 4; ++g) *reinterpret_cast<uint32_t*>(&tile[pl][r][kg * 16 + 4 * g]) = w[g];
+        }
+        __syncthreads();
+        const int64_t rr = (t % tiles_r) * kTR + wr;
+        const int64_t kc = (t / tiles_r) * kTK + wc;
+        if (rr < rows && kc < k_pad) {
+            int8_t* dst = planes + rr * k_pad + kc;
+            for (int pl = 0; pl < nq; ++pl) {
+                const uint32_t* src = reinterpret_cast<const uint32_t*>(&tile[pl][wr][wc]);
+                *reinterpret_cast<uint4*>(dst + pl * plane) = make_uint4(src[0], src[1], src[2], src[3]);
+            }
+        }
+    }
+}
+
 // C <- beta * C mod p (k = 0 or alpha = 0); C <- 0 when beta = 0 (C not read).
 // Rows on grid.y, 4 columns per thread (16-byte accesses when aligned).
 __global__ void __launch_bounds__(256) scale_c_kernel(ModP M, int64_t m, int64_t n, int32_t* __restrict__ C,
@@ -508,6 +599,20 @@ cudaError_t launch_encode(const Plan& pl, int kmajor_src, int64_t rows, int64_t 
                 pl.mp, pl.cc, rows, k, k_pad, X, ldx, limbs, vec_ok);
         } else {
             const int64_t tiles = ((rows + kTR - 1) / kTR) * ((k_pad + kTK - 1) / kTK);
+            CUtensorMap map;
+            static const bool no_tma = getenv("FF_ENC_NOTMA") != nullptr;
+            if (!no_tma && make_src_map(&map, X, rows, k, ldx)) {
+                static bool attr = false;
+                if (!attr) {
+                    cudaFuncSetAttribute(encode_crt_trans_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kCrtTmaSmem);
+                    attr = true;
+                }
+                const int64_t capt = (int64_t)num_sms() * 2;
+                encode_crt_trans_tma_kernel<<<static_cast<int>(tiles < capt ? tiles : capt), 256, kCrtTmaSmem, st>>>(
+                    map, pl.mp, pl.cc, rows, k_pad, limbs);
+                return cudaGetLastError();
+            }
             const int64_t cap = (int64_t)num_sms() * 8;
             encode_crt_trans_kernel<<<static_cast<int>(tiles < cap ? tiles : cap), 256, 0, st>>>(
                 pl.mp, pl.cc, rows, k, k_pad, X, ldx, limbs);
