@@ -357,6 +357,18 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu, _ = cpu_oracle_sample(cfg)
 
+    # clock-normalised tensor peak: 16384 int8 ops/clk/SM (one
+    # 256x256x32 CTA-pair MMA per 128 cycles), at the median SM clock sampled
+    # during the timed region
+    clocks = clk.summary()
+    try:
+        nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+        if clocks.get("sm_mhz"):
+            clk_peak = nsm * 16384 * clocks["sm_mhz"] * 1e6 / 1e12
+            roofline["clock_peak"] = clk_peak
+            roofline["frac_of_clock_peak"] = achieved / clk_peak
+    except Exception:  # pragma: no cover - informational only
+        pass
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "GOPS", "n_gpus": world, "steps": args.steps,
@@ -373,7 +385,7 @@ def main():
             "e2e": e2e,
             "gpu_launches": launches,
             "gemm_launches": gemm_launches,
-            "clocks": clk.summary(),
+            "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
