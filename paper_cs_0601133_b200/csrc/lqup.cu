@@ -31,6 +31,7 @@
 
 #include "internal.h"
 #include "modp.cuh"
+#include "ptx.cuh"
 
 namespace ff {
 
@@ -292,6 +293,215 @@ __global__ void __launch_bounds__(kThr) panel_kernel(PanelArgs P) {
     }
 }
 
+// ---- the same panel on a CTA pair (cluster of 2) ------------------------------
+// Generic case only (window of kH columns in shared memory, no zero rows): CTA
+// rho owns window columns [64 rho, 64 rho + 64) and the same columns of E.  Per
+// pivot: each CTA searches its columns, one cluster barrier exchanges the two
+// minima (DSMEM), the non-owner of the pivot column reads the pivot and the
+// multipliers a_s from the owner's shared memory, and each CTA updates its own
+// half -- half the work of panel_kernel per SM, one cluster barrier per pivot.
+// A zero row returns fail (the host then runs panel_kernel on this panel).
+constexpr int kHalf = kH / 2;
+constexpr int kPanel2Smem = (3 * kH * kHalf + 2 * kH) * 4;   // w, E, peer U columns, colbuf(+pad)
+
+__device__ __forceinline__ uint32_t dsmem_ld_u32(const void* local_ptr, uint32_t peer) {
+    const uint32_t ra = ptx::mapa(ptx::smem_u32(local_ptr), peer);
+    uint32_t v;
+    asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(ra) : "memory");
+    return v;
+}
+
+__global__ void __launch_bounds__(kThr) panel2_kernel(PanelArgs P) {
+    extern __shared__ uint32_t dyn2[];
+    uint32_t* w = dyn2;                       // [kH][kHalf]: this CTA's window columns
+    uint32_t* E = w + kH * kHalf;             // [kH][kHalf]: this CTA's columns of E (S L^-1, then F for U^-1)
+    uint32_t* Up = E + kH * kHalf;            // [kH][kHalf]: the peer's U columns (Uinv phases)
+    uint32_t* colbuf = Up + kH * kHalf;       // [kH]: the pivot column (multipliers), from its owner
+    __shared__ int s_jloc[2], s_fail, s_kk, s_ncol;
+    __shared__ int colsw[kMaxSwaps][2];
+    __shared__ uint32_t piv[kH], pinv[kH], sinv[kH], sfw[kH];
+    const uint32_t rho = ptx::cluster_ctarank(), peer = rho ^ 1u;
+    const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+    const int64_t hr = P.hr;
+    const uint32_t p = P.p;
+    const unsigned long long c32 = P.mu64;
+    const int c0 = static_cast<int>(rho) * kHalf;            // first global window column of this CTA
+    long long t_0 = clock64();
+    for (int e = tid; e < kH * kHalf; e += kThr) {
+        const int r = e / kHalf, cl = e % kHalf;
+        uint32_t v = 0;
+        if (r < hr) {
+            const int64_t x = static_cast<int64_t>(P.A[(P.i0 + r) * P.lda + P.c + c0 + cl]) % static_cast<int64_t>(p);
+            v = static_cast<uint32_t>(x < 0 ? x + p : x);
+        }
+        w[e] = v;
+        E[e] = (r == c0 + cl) ? 1u : 0u;
+    }
+    if (tid == 0) { s_jloc[0] = s_jloc[1] = INT32_MAX; s_fail = 0; s_kk = 0; s_ncol = 0; }
+    __syncthreads();
+    ptx::cluster_sync();
+    for (int i = 0; i < hr; ++i) {
+        const int kk = i;                                    // no zero rows on this path: kk == i
+        const int par = i & 1;
+        // local search over this CTA's columns >= kk
+        if (ty == 0) {
+            const int cl = tx + 32 * 0, cl2 = tx + 32;       // kHalf = 64: two columns per lane
+            int best = INT32_MAX;
+            if (c0 + cl >= kk && w[i * kHalf + cl] != 0u) best = c0 + cl;
+            if (c0 + cl2 >= kk && w[i * kHalf + cl2] != 0u && c0 + cl2 < best) best = c0 + cl2;
+            for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+            if (tx == 0) s_jloc[par] = best;     // (the peer read step i-2's value before cluster barrier i-1)
+        }
+        __syncthreads();
+        ptx::cluster_sync();                                 // both minima written; pivot columns final
+        const int j = min(s_jloc[par], static_cast<int>(dsmem_ld_u32(&s_jloc[par], peer)));
+        if (j == INT32_MAX) { if (tid == 0) s_fail = 1; break; }
+        const uint32_t own_k = static_cast<uint32_t>(kk / kHalf), own_j = static_cast<uint32_t>(j / kHalf);
+        if (j != kk) {                                       // column swap kk <-> j (rare)
+            if (own_k == own_j) {
+                if (own_k == rho)
+                    for (int r = tid; r < hr; r += kThr) {
+                        const uint32_t t = w[r * kHalf + kk - c0];
+                        w[r * kHalf + kk - c0] = w[r * kHalf + j - c0];
+                        w[r * kHalf + j - c0] = t;
+                    }
+            } else {                                         // across the pair: read the peer's column, then write
+                const int mine = (own_k == rho) ? kk : j, theirs = (own_k == rho) ? j : kk;
+                for (int r = tid; r < hr; r += kThr)
+                    colbuf[r] = dsmem_ld_u32(&w[r * kHalf + theirs - static_cast<int>(peer) * kHalf], peer);
+                __syncthreads();
+                ptx::cluster_sync();
+                for (int r = tid; r < hr; r += kThr) w[r * kHalf + mine - c0] = colbuf[r];
+            }
+            if (tid == 0 && rho == 0) { colsw[s_ncol][0] = kk; colsw[s_ncol][1] = j; ++s_ncol; }
+            __syncthreads();
+            ptx::cluster_sync();
+        }
+        // the pivot column (multipliers a_s, and pi_k) into colbuf
+        if (own_k == rho) {
+            for (int r = kk + tid; r < hr; r += kThr) colbuf[r] = w[r * kHalf + kk - c0];
+        } else {
+            for (int r = kk + tid; r < hr; r += kThr) colbuf[r] = dsmem_ld_u32(&w[r * kHalf + kk - static_cast<int>(peer) * kHalf], peer);
+        }
+        __syncthreads();
+        const uint32_t pk = colbuf[kk];
+        const uint32_t pk_sh = shoup_c(pk, p, c32);
+        if (tid == 0) piv[kk] = pk;
+        // fraction-free update of rows i+1.. on this CTA's columns > kk, and of E; the
+        // (up to 4) rows of a warp are processed together for instruction-level parallelism
+        const int clo = max(kk + 1 - c0, 0);
+        uint32_t as[4], as_sh[4];
+        bool ok[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int r = i + 1 + ty + 32 * q;
+            ok[q] = r < hr;
+            as[q] = ok[q] ? colbuf[r] : 0u;
+            as_sh[q] = shoup_c(as[q], p, c32);
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int cl = tx + 32 * h;
+            const uint32_t pw = w[kk * kHalf + cl], pe = E[kk * kHalf + cl];
+            const int e = c0 + cl;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (!ok[q]) continue;
+                const int r = i + 1 + ty + 32 * q;
+                if (cl >= clo)
+                    w[r * kHalf + cl] = subm_u(shoup_m(w[r * kHalf + cl], pk, pk_sh, p), shoup_m(pw, as[q], as_sh[q], p), p);
+                if (e <= i)
+                    E[r * kHalf + cl] = subm_u(shoup_m(E[r * kHalf + cl], pk, pk_sh, p), shoup_m(pe, as[q], as_sh[q], p), p);
+                else if (e == r)
+                    E[r * kHalf + cl] = shoup_m(E[r * kHalf + cl], pk, pk_sh, p);
+            }
+        }
+        __syncthreads();
+    }
+    int kk = s_fail ? 0 : static_cast<int>(hr);
+    long long t_1 = clock64(), t_2 = 0, t_3 = 0, t_4 = 0;
+    ptx::cluster_sync();
+    const int fail = s_fail | static_cast<int>(dsmem_ld_u32(&s_fail, peer));
+    if (!fail) {
+        for (int k = tid; k < kk; k += kThr) pinv[k] = inv_dev(piv[k], p);
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t sacc = 1 % p, facc = 1 % p;
+            for (int k = 0; k < kk; ++k) {
+                sinv[k] = sacc; sacc = shoup_m(sacc, pinv[k], shoup_c(pinv[k], p, c32), p);
+                sfw[k] = facc; facc = shoup_m(facc, piv[k], shoup_c(piv[k], p, c32), p);
+            }
+        }
+        __syncthreads();
+        for (int r = ty; r < hr; r += 32) {              // true L and U on this CTA's columns
+            const uint32_t si = r < kk ? sinv[r] : 0u;
+            const uint32_t si_sh = r < kk ? shoup_c(si, p, c32) : 0u;
+            for (int cl = tx; cl < kHalf; cl += 32) {
+                const int cc = c0 + cl;
+                const uint32_t x = w[r * kHalf + cl];
+                if (cc < r && cc < kk) w[r * kHalf + cl] = shoup_m(x, pinv[cc], shoup_c(pinv[cc], p, c32), p);
+                else if (r < kk && cc >= r) w[r * kHalf + cl] = shoup_m(x, si, si_sh, p);
+            }
+        }
+        t_2 = clock64();
+        // Linv columns of this CTA: E[r][e] / S_r (no row swaps on this path)
+        for (int e = tid; e < kk * kHalf; e += kThr) {
+            const int r = e / kHalf, cl = e % kHalf, cc = c0 + cl;
+            if (cc < kk)
+                P.Linv[r * kH + cc] = static_cast<int32_t>(cc <= r ? shoup_m(E[r * kHalf + cl], sinv[r], shoup_c(sinv[r], p, c32), p) : 0u);
+        }
+        __syncthreads();
+        ptx::cluster_sync();                                 // both CTAs' U rescaled: copy the peer's U columns
+        for (int e = tid; e < kH * kHalf; e += kThr) Up[e] = dsmem_ld_u32(&w[e], peer);
+        for (int e = tid; e < kH * kHalf; e += kThr) E[e] = ((e / kHalf) == c0 + (e % kHalf)) ? 1u : 0u;
+        __syncthreads();
+        t_3 = clock64();
+        // Uinv (this CTA's columns c >= k): F_r -= (u_rk / u_kk) F_k for r < k, then F_k /= u_kk
+        for (int k = kk - 1; k > 0; --k) {
+            const uint32_t own = static_cast<uint32_t>(k / kHalf);
+            const uint32_t* Ucol = (own == rho) ? w : Up;
+            const int kl = k - static_cast<int>(own) * kHalf;
+            const uint32_t iu = shoup_m(pinv[k], sfw[k], shoup_c(sfw[k], p, c32), p);
+            const int clo = max(k - c0, 0);
+            if (clo < kHalf) {
+                for (int r = ty; r < k; r += 32) {
+                    const uint32_t u = Ucol[r * kHalf + kl];
+                    if (u == 0u) continue;
+                    const uint32_t m = shoup_m(u, iu, shoup_c(iu, p, c32), p);
+                    const uint32_t m_sh = shoup_c(m, p, c32);
+                    for (int cl = clo + tx; cl < kHalf; cl += 32)
+                        E[r * kHalf + cl] = subm_u(E[r * kHalf + cl], shoup_m(E[k * kHalf + cl], m, m_sh, p), p);
+                }
+            }
+            __syncthreads();
+        }
+        for (int e = tid; e < kk * kHalf; e += kThr) {
+            const int r = e / kHalf, cl = e % kHalf, cc = c0 + cl;
+            if (cc < kk) {
+                const uint32_t iu = shoup_m(pinv[r], sfw[r], shoup_c(sfw[r], p, c32), p);
+                P.Uinv[r * kH + cc] = static_cast<int32_t>(shoup_m(E[r * kHalf + cl], iu, shoup_c(iu, p, c32), p));
+            }
+        }
+        t_4 = clock64();
+        for (int e = tid; e < hr * kHalf; e += kThr) {
+            const int r = e / kHalf, cl = e % kHalf;
+            P.A[(P.i0 + r) * P.lda + P.c + c0 + cl] = static_cast<int32_t>(w[e]);
+        }
+    } else {
+        kk = 0;
+    }
+    if (tid == 0 && rho == 0) {
+        long long* tt = reinterpret_cast<long long*>(P.out + 4 + 4 * kMaxSwaps);
+        tt[0] = t_1 - t_0; tt[1] = t_2 - t_1; tt[2] = 0; tt[3] = t_4 - t_3; tt[4] = clock64() - t_4;
+        P.out[0] = kk;
+        P.out[1] = fail;
+        P.out[2] = s_ncol;
+        P.out[3] = 0;
+        for (int s = 0; s < s_ncol; ++s) { P.out[4 + 2 * s] = colsw[s][0]; P.out[5 + 2 * s] = colsw[s][1]; }
+    }
+    ptx::cluster_sync();                                     // the peer is done reading this CTA's shared memory
+}
+
 // Column transpositions (in order) applied to the rows outside [skip0, skip1).
 __global__ void colswap_kernel(int32_t* A, int64_t lda, int64_t m, int64_t skip0, int64_t skip1,
                                const int* sw, int nsw, int64_t c) {
@@ -443,10 +653,13 @@ int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t* A, int64_t lda, int64_
     static bool attr = false;
     if (!attr) {
         if (cudaFuncSetAttribute(panel_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes) !=
-            cudaSuccess)
+                cudaSuccess ||
+            cudaFuncSetAttribute(panel2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPanel2Smem) !=
+                cudaSuccess)
             return fail_cuda_now();
         attr = true;
     }
+    static const bool use_pair = getenv("FF_LQUP_ONECTA") == nullptr;   // experiment: one-CTA panels only
     int64_t i0 = 0, c = 0, m_active = m, r = 0;
     int64_t W = std::min<int64_t>(n, kH);
     auto fail_cuda = [&]() { cudaGetLastError(); return FF_ERR_CUDA; };
@@ -479,11 +692,33 @@ int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t* A, int64_t lda, int64_
         pa.mu64 = static_cast<unsigned long long>((static_cast<unsigned __int128>(1) << 64) / p);
         pa.win = win; pa.tmp = tmpd; pa.Linv = Linv; pa.Uinv = Uinv; pa.out = dout;
         if (cudaStreamWaitEvent(ps, ev_ready, 0) != cudaSuccess) return fail_cuda();
-        if (Wc <= kH) panel_kernel<true><<<1, kThr, kSmemBytes, ps>>>(pa);
-        else panel_kernel<false><<<1, kThr, 0, ps>>>(pa);
-        if (cudaGetLastError() != cudaSuccess) return fail_cuda();
-        if (cudaMemcpyAsync(hout.data(), dout, hout.size() * 4, cudaMemcpyDeviceToHost, ps) != cudaSuccess ||
-            cudaEventRecord(ev_panel, ps) != cudaSuccess || cudaStreamSynchronize(ps) != cudaSuccess)
+        bool used_pair = false;
+        if (Wc == kH && use_pair) {
+            // the panel on a CTA pair (generic case); a zero row makes it report fail
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(2);
+            cfg.blockDim = dim3(kThr);
+            cfg.dynamicSmemBytes = kPanel2Smem;
+            cfg.stream = ps;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            if (cudaLaunchKernelEx(&cfg, panel2_kernel, pa) != cudaSuccess) return fail_cuda();
+            if (cudaMemcpyAsync(hout.data(), dout, hout.size() * 4, cudaMemcpyDeviceToHost, ps) != cudaSuccess ||
+                cudaStreamSynchronize(ps) != cudaSuccess)
+                return fail_cuda();
+            used_pair = !hout[1];
+        }
+        if (!used_pair) {
+            if (Wc <= kH) panel_kernel<true><<<1, kThr, kSmemBytes, ps>>>(pa);
+            else panel_kernel<false><<<1, kThr, 0, ps>>>(pa);
+            if (cudaGetLastError() != cudaSuccess) return fail_cuda();
+            if (cudaMemcpyAsync(hout.data(), dout, hout.size() * 4, cudaMemcpyDeviceToHost, ps) != cudaSuccess)
+                return fail_cuda();
+        }
+        if (cudaEventRecord(ev_panel, ps) != cudaSuccess || cudaStreamSynchronize(ps) != cudaSuccess)
             return fail_cuda();
         if (cudaStreamWaitEvent(st, ev_panel, 0) != cudaSuccess) return fail_cuda();
         const int64_t kk = hout[0];
