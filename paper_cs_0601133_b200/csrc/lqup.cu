@@ -54,32 +54,14 @@ struct PanelArgs {
     int64_t c, W;                // window columns [c, c + W)
     int32_t full;                // 1: the window reaches the last column (zero rows allowed)
     uint32_t p;
-    double dp, invp;             // p, fl(1/p)
     unsigned long long mu64;     // floor(2^64 / p)
+    int32_t red;                 // panel_spec_kernel: reduce 64-bit sums every red products
     double* win;                 // workspace hr x W (ld W): the window, residues as exact doubles
     int32_t* Linv;               // kH x kH
     int32_t* Uinv;               // kH x kH
     double* tmp;                 // kH x kH scratch for the inverses
     int32_t* out;                // [0] kk, [1] fail, [2] ncol, [3] nrow, then col swaps (a,b)..., row swaps (a,b)...
 };
-
-// a b mod p for residues a, b < p < 2^31 held as doubles: the product is split
-// exactly (hi + lo, fma), the quotient estimated with the fp reciprocal (the
-// paper's "floating point inverse": off by at most one),
-// and corrected.  No integer<->float conversions.
-__device__ __forceinline__ double mulm(double a, double b, double p, double invp) {
-    const double hi = a * b;
-    const double lo = fma(a, b, -hi);
-    const double q = rint(hi * invp);
-    double r = fma(-q, p, hi) + lo;
-    if (r < 0) r += p;
-    if (r >= p) r -= p;
-    return r;
-}
-__device__ __forceinline__ double subm(double x, double t, double p) {
-    const double r = x - t;
-    return r < 0 ? r + p : r;
-}
 
 // a^-1 mod p by the extended Euclid algorithm in 32-bit integers (p < 2^31:
 // remainders < 2^31, Bezout coefficients |s| < p); on the panel's critical path.
@@ -317,7 +299,7 @@ __global__ void __launch_bounds__(kThr) panel2_kernel(PanelArgs P) {
     uint32_t* E = w + kH * kHalf;             // [kH][kHalf]: this CTA's columns of E (S L^-1, then F for U^-1)
     uint32_t* Up = E + kH * kHalf;            // [kH][kHalf]: the peer's U columns (Uinv phases)
     uint32_t* colbuf = Up + kH * kHalf;       // [kH]: the pivot column (multipliers), from its owner
-    __shared__ int s_jloc[2], s_fail, s_kk, s_ncol;
+    __shared__ int s_jloc[2], s_fail, s_ncol;
     __shared__ int colsw[kMaxSwaps][2];
     __shared__ uint32_t piv[kH], pinv[kH], sinv[kH], sfw[kH];
     const uint32_t rho = ptx::cluster_ctarank(), peer = rho ^ 1u;
@@ -337,7 +319,7 @@ __global__ void __launch_bounds__(kThr) panel2_kernel(PanelArgs P) {
         w[e] = v;
         E[e] = (r == c0 + cl) ? 1u : 0u;
     }
-    if (tid == 0) { s_jloc[0] = s_jloc[1] = INT32_MAX; s_fail = 0; s_kk = 0; s_ncol = 0; }
+    if (tid == 0) { s_jloc[0] = s_jloc[1] = INT32_MAX; s_fail = 0; s_ncol = 0; }
     __syncthreads();
     ptx::cluster_sync();
     for (int i = 0; i < hr; ++i) {
@@ -502,6 +484,272 @@ __global__ void __launch_bounds__(kThr) panel2_kernel(PanelArgs P) {
     ptx::cluster_sync();                                     // the peer is done reading this CTA's shared memory
 }
 
+// ---- speculative blocked panel -----------------------------------------------
+// For a full kH x kH window the paper's pivot rule ("first non-zero of the row",
+// P:583-588) selects the diagonal entry unless it is zero, which for a random
+// matrix over a large field happens with probability about kH/p per panel.  This
+// kernel assumes no swap at all and factors the window as a blocked LU, kB
+// columns at a time:
+//   (1) fraction-free LDU elimination of the kB x kB diagonal block D (one
+//       element per thread, one barrier per pivot): row operations below the
+//       pivot, tracked in E_L (-> S L_D^-1), and column operations right of it,
+//       tracked in E_U (-> U'^-1 S, U' = the unit upper factor);
+//   (2) the kB pivots inverted together (prefix / suffix products in one warp,
+//       one modular inverse); D, E_L, E_U rescaled to L_D, U_D, L_D^-1, U_D^-1;
+//   (3) U12 = L_D^-1 A12 and L21 = A21 U_D^-1, then A22 <- A22 - L21 U12, as
+//       shared-memory products with delayed reduction (Eq. (1) in 64 bits).
+// The full L11^-1 and U11^-1 follow from the diagonal blocks' inverses by block
+// back-substitution waves.  A zero pivot reports fail and nothing is written:
+// the host then runs panel2_kernel / panel_kernel, whose output is what this
+// kernel produces when no swap occurs (the LU without pivoting is unique).
+constexpr int kB = 32;
+constexpr int kSpecScratch = 2 * kB * (kH - kB);                  // u32: U12 (kB x R) + L21 (R x kB); 6 kB x kB blocks
+constexpr int kSpecSmem = (3 * kH * kH + kSpecScratch) * 4;       // window, Linv, Uinv, scratch: 216 KB
+
+__device__ __forceinline__ uint32_t mulm_b(uint32_t a, uint32_t b, uint32_t p, unsigned long long mu64) {
+    return residue_u64(static_cast<unsigned long long>(a) * b, mu64, p);
+}
+__device__ __forceinline__ uint32_t ffma_b(uint32_t a, uint32_t x, uint32_t b, uint32_t y, uint32_t p,
+                                           unsigned long long mu64) {   // (a x + b y) mod p
+    return residue_u64(static_cast<unsigned long long>(a) * x + static_cast<unsigned long long>(b) * y, mu64, p);
+}
+
+// C = A B (mode 0), C - A B (mode 1) or -(A B) (mode 2) mod p on shared-memory
+// residue matrices; M multiple of 4, N and K of 32; rows of A 16-byte aligned.
+struct MmJob {
+    uint32_t* C;
+    const uint32_t* A;
+    const uint32_t* B;
+    int ldc, lda, ldb, M, N, K, mode;
+};
+
+__device__ __forceinline__ MmJob mm_job(uint32_t* C, int ldc, const uint32_t* A, int lda, const uint32_t* B, int ldb,
+                                        int M, int N, int K, int mode) {
+    MmJob j;
+    j.C = C; j.A = A; j.B = B; j.ldc = ldc; j.lda = lda; j.ldb = ldb; j.M = M; j.N = N; j.K = K; j.mode = mode;
+    return j;
+}
+
+// One job on a group of nthr threads (lt: index in the group).  An item is 4 x 1
+// output cells; a warp takes 4 rows x 32 consecutive columns, so the A reads are
+// broadcasts (16 B: four k at once) and the B reads conflict-free.  Products are
+// summed in 64 bits: kBig reduces every 4 products (any p < 2^31: 4 (p-1)^2 + p
+// < 2^64), otherwise every 32 (the host checks 32 (p-1)^2 + p < 2^64).
+template <bool kBig>
+__device__ __forceinline__ void mm_one(const MmJob J, int lt, int nthr, uint32_t p, unsigned long long mu64) {
+    const int items = (J.M / 4) * J.N;
+    for (int e = lt; e < items; e += nthr) {
+        const int i = (e / J.N) * 4, j = e % J.N;
+        const uint32_t* Ab = J.A + i * J.lda;
+        const uint32_t* Bb = J.B + j;
+        unsigned long long acc[4] = {0ull, 0ull, 0ull, 0ull};
+        for (int k0 = 0; k0 < J.K; k0 += 32) {
+#pragma unroll
+            for (int kk = 0; kk < 32; kk += 4) {
+                const int k = k0 + kk;
+                const uint32_t b0 = Bb[(k + 0) * J.ldb], b1 = Bb[(k + 1) * J.ldb];
+                const uint32_t b2 = Bb[(k + 2) * J.ldb], b3 = Bb[(k + 3) * J.ldb];
+#pragma unroll
+                for (int ii = 0; ii < 4; ++ii) {
+                    const uint4 a = *reinterpret_cast<const uint4*>(Ab + ii * J.lda + k);
+                    acc[ii] += static_cast<unsigned long long>(a.x) * b0 + static_cast<unsigned long long>(a.y) * b1 +
+                               static_cast<unsigned long long>(a.z) * b2 + static_cast<unsigned long long>(a.w) * b3;
+                    if (kBig) acc[ii] = residue_u64(acc[ii], mu64, p);
+                }
+            }
+            if (!kBig) {
+#pragma unroll
+                for (int ii = 0; ii < 4; ++ii) acc[ii] = residue_u64(acc[ii], mu64, p);
+            }
+        }
+#pragma unroll
+        for (int ii = 0; ii < 4; ++ii) {
+            const uint32_t r = static_cast<uint32_t>(acc[ii]);     // already reduced
+            uint32_t* c = J.C + (i + ii) * J.ldc + j;
+            if (J.mode == 0) *c = r;
+            else if (J.mode == 1) *c = subm_u(*c, r, p);
+            else *c = r ? p - r : 0u;
+        }
+    }
+}
+__device__ __forceinline__ void mm_any(bool big, const MmJob& J, int lt, int nthr, uint32_t p, unsigned long long mu64) {
+    if (big) mm_one<true>(J, lt, nthr, p, mu64);
+    else mm_one<false>(J, lt, nthr, p, mu64);
+}
+
+__global__ void __launch_bounds__(kThr) panel_spec_kernel(PanelArgs P) {
+    extern __shared__ __align__(16) uint32_t dyn3[];
+    uint32_t* W = dyn3;                       // [kH][kH] the window -> L (strict lower) and U
+    uint32_t* Li = W + kH * kH;               // [kH][kH] L11^-1
+    uint32_t* Ui = Li + kH * kH;              // [kH][kH] U11^-1
+    uint32_t* T = Ui + kH * kH;               // scratch
+    __shared__ uint32_t ipk[kH], isc[kH], iu[kH];
+    __shared__ uint32_t ash[2][kB], bsh[2][kB];   // Shoup constants of the pivot column / row (by parity)
+    const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+    const uint32_t p = P.p;
+    const unsigned long long mu = P.mu64;
+    const bool big = P.red < 32;
+    long long t_0 = clock64();
+    {
+        constexpr int kPer = kH * kH / kThr;      // all loads in flight before any use
+        int32_t v[kPer];
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+            const int e = tid + q * kThr;
+            v[q] = P.A[(P.i0 + e / kH) * P.lda + P.c + e % kH];
+        }
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+            const int e = tid + q * kThr;
+            W[e] = residue_u64(static_cast<unsigned long long>(static_cast<long long>(v[q]) + (static_cast<long long>(p) << 31)), mu, p);
+            Li[e] = 0u;
+            Ui[e] = 0u;
+        }
+    }
+    __syncthreads();
+    bool fail = false;
+    for (int kb = 0; kb < kH / kB; ++kb) {
+        const int o = kb * kB;
+        uint32_t* D = W + o * kH + o;          // the diagonal block (ld kH)
+        uint32_t* El = Li + o * kH + o;        // E_L, then L_D^-1
+        uint32_t* Eu = Ui + o * kH + o;        // E_U, then U_D^-1
+        uint32_t x = D[ty * kH + tx], el = 0u, eu = 0u;
+        if (tx == 0) ash[0][ty] = shoup_c(x, p, mu);
+        if (ty == 0) bsh[0][tx] = shoup_c(x, p, mu);
+        uint32_t S = 1u % p;                       // S_t = prod_{t' < t} pk_t' (uniform)
+        __syncthreads();
+        // (1) pivot t (pk = D[t][t], scale S_t): rows r > t become pk row_r - a_r row_t --
+        // on D's columns > t (column t keeps the raw a_r) and on E_L's columns <= t; the
+        // columns c > t of E_U become pk col_c - D[t][c] col_t on its rows <= t.  The
+        // diagonals of E_L and E_U are implicitly S_r (never stored), every other
+        // entry outside these ranges stays zero, so each thread updates exactly one
+        // cell (ty, tx) of one of D, E_L, E_U per pivot.  Step t reads row t and column
+        // t only and writes rows / columns > t: one barrier per pivot.  All products
+        // are Shoup multiplications; the constants of the next pivot's row and column
+        // (ash: a_r and the pivot, bsh: D[t][c]) come from the threads that produce them.
+        for (int t = 0; t < kB; ++t) {
+            const int par = t & 1;
+            const uint32_t pk = D[t * kH + t];
+            if (pk == 0u) { fail = true; break; }                       // uniform: speculation failed
+            const uint32_t pk_sh = ash[par][t];
+            if (ty > t) {
+                const uint32_t a = D[ty * kH + t], a_sh = ash[par][ty];
+                if (tx > t) {
+                    x = subm_u(shoup_m(x, pk, pk_sh, p), shoup_m(D[t * kH + tx], a, a_sh, p), p);
+                    D[ty * kH + tx] = x;
+                    if (tx == t + 1) ash[par ^ 1][ty] = shoup_c(x, p, mu);
+                    if (ty == t + 1) bsh[par ^ 1][tx] = shoup_c(x, p, mu);
+                } else {
+                    const uint32_t g = (tx == t) ? S : El[t * kH + tx];
+                    el = subm_u(shoup_m(el, pk, pk_sh, p), shoup_m(g, a, a_sh, p), p);
+                    El[ty * kH + tx] = el;
+                }
+            } else if (tx > t) {
+                const uint32_t h = (ty == t) ? S : Eu[ty * kH + t];
+                eu = subm_u(shoup_m(eu, pk, pk_sh, p), shoup_m(h, D[t * kH + tx], bsh[par][tx], p), p);
+                Eu[ty * kH + tx] = eu;
+            }
+            S = shoup_m(S, pk, pk_sh, p);
+            __syncthreads();
+        }
+        if (fail) break;
+        // (2) prefix P_t and suffix Q_t products of the pivots, one inverse of P_{kB-1}:
+        // 1/S_t = inv Q_t, 1/pk_t = (1/S_{t+1}) P_{t-1}, 1/u_tt = S_t / pk_t
+        if (ty == 0) {
+            const uint32_t v = D[tx * kH + tx];
+            uint32_t pre = v, suf = v;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, pre, d);
+                const uint32_t z = __shfl_down_sync(0xffffffffu, suf, d);
+                if (tx >= d) pre = mulm_b(pre, y, p, mu);
+                if (tx + d < 32) suf = mulm_b(suf, z, p, mu);
+            }
+            const uint32_t total = __shfl_sync(0xffffffffu, pre, 31);
+            const uint32_t inv = inv_dev(total, p);
+            const uint32_t is = mulm_b(inv, suf, p, mu);                  // 1 / S_tx
+            uint32_t is_next = __shfl_down_sync(0xffffffffu, is, 1);      // 1 / S_{tx+1} = 1 / P_tx
+            if (tx == 31) is_next = inv;
+            uint32_t pprev = __shfl_up_sync(0xffffffffu, pre, 1);        // P_{tx-1} = S_tx
+            if (tx == 0) pprev = 1u % p;
+            const uint32_t ip = mulm_b(is_next, pprev, p, mu);
+            isc[o + tx] = is;
+            ipk[o + tx] = ip;
+            iu[o + tx] = mulm_b(pprev, ip, p, mu);
+        }
+        __syncthreads();
+        // true L_D (a / pk_c), U_D (row / S_r); L_D^-1 = E_L / S_r (unit diagonal);
+        // U_D^-1 = E_U / pk_c (E_U col c = S_c U'^-1 col c, U_D^-1 = U'^-1 diag(S_c / pk_c))
+        D[ty * kH + tx] = mulm_b(x, ty > tx ? ipk[o + tx] : isc[o + ty], p, mu);
+        El[ty * kH + tx] = tx < ty ? mulm_b(el, isc[o + ty], p, mu) : (tx == ty ? 1u : 0u);
+        Eu[ty * kH + tx] = ty < tx ? mulm_b(eu, ipk[o + tx], p, mu) : (tx == ty ? iu[o + tx] : 0u);
+        __syncthreads();
+        // (3) U12 = L_D^-1 A12 (T1, kB x R) and L21 = A21 U_D^-1 (T2, R x kB), then
+        // A22 -= L21 U12 while T1, T2 are copied into the window
+        const int R = kH - o - kB;
+        if (R > 0) {
+            uint32_t* T1 = T;
+            uint32_t* T2 = T + kB * R;
+            const int half = kThr / 2, g = tid / half, lt = tid % half;
+            if (g == 0) mm_any(big, mm_job(T1, R, El, kH, W + o * kH + o + kB, kH, kB, R, kB, 0), lt, half, p, mu);
+            else mm_any(big, mm_job(T2, kB, W + (o + kB) * kH + o, kH, Eu, kH, R, kB, kB, 0), lt, half, p, mu);
+            __syncthreads();
+            mm_any(big, mm_job(W + (o + kB) * kH + o + kB, kH, T2, kB, T1, R, R, R, kB, 1), tid, kThr, p, mu);
+            for (int e = tid; e < kB * R; e += kThr) {
+                W[(o + e / R) * kH + o + kB + e % R] = T1[e];
+                W[(o + kB + e / kB) * kH + o + e % kB] = T2[e];
+            }
+            __syncthreads();
+        }
+    }
+    long long t_1 = clock64(), t_2 = 0;
+    if (!fail) {
+        // full inverses by block waves d = j - i (block units), a warp group per block:
+        //   Li_ij = -Li_ii (sum_{k=j}^{i-1} L_ik Li_kj),  Ui_ij = -Ui_ii (sum_{k=i+1}^{j} U_ik Ui_kj)
+        constexpr int nb = kH / kB;
+        for (int d = 1; d < nb; ++d) {
+            const int n = 2 * (nb - d);                  // jobs: (L, U) per block pair; <= 6 scratch blocks
+            const int wpj = 32 / n, q = ty / wpj, lt = tid - q * wpj * 32;
+            const bool on = q < n;
+            const int i = d + q / 2;
+            uint32_t* Tq = T + q * kB * kB;
+            if (on) {
+                if ((q & 1) == 0)
+                    mm_any(big, mm_job(Tq, kB, W + i * kB * kH + (i - d) * kB, kH, Li + (i - d) * kB * kH + (i - d) * kB, kH,
+                                       kB, kB, d * kB, 0), lt, wpj * 32, p, mu);
+                else
+                    mm_any(big, mm_job(Tq, kB, W + (i - d) * kB * kH + (i - d + 1) * kB, kH,
+                                       Ui + (i - d + 1) * kB * kH + i * kB, kH, kB, kB, d * kB, 0), lt, wpj * 32, p, mu);
+            }
+            __syncthreads();
+            if (on) {
+                if ((q & 1) == 0)
+                    mm_any(big, mm_job(Li + i * kB * kH + (i - d) * kB, kH, Li + i * kB * kH + i * kB, kH, Tq, kB, kB, kB, kB, 2),
+                           lt, wpj * 32, p, mu);
+                else
+                    mm_any(big, mm_job(Ui + (i - d) * kB * kH + i * kB, kH, Ui + (i - d) * kB * kH + (i - d) * kB, kH, Tq, kB,
+                                       kB, kB, kB, 2), lt, wpj * 32, p, mu);
+            }
+            __syncthreads();
+        }
+        t_2 = clock64();
+        for (int e = tid; e < kH * kH; e += kThr) {
+            const int r = e / kH, c = e % kH;
+            P.A[(P.i0 + r) * P.lda + P.c + c] = static_cast<int32_t>(W[e]);
+            P.Linv[e] = static_cast<int32_t>(Li[e]);
+            P.Uinv[e] = static_cast<int32_t>(Ui[e]);
+        }
+    }
+    if (tid == 0) {
+        long long* tt = reinterpret_cast<long long*>(P.out + 4 + 4 * kMaxSwaps);
+        tt[0] = t_1 - t_0; tt[1] = 0; tt[2] = 0; tt[3] = t_2 - t_1; tt[4] = clock64() - t_2;
+        P.out[0] = fail ? 0 : kH;
+        P.out[1] = fail ? 1 : 0;
+        P.out[2] = 0;
+        P.out[3] = 0;
+    }
+}
+
 // Column transpositions (in order) applied to the rows outside [skip0, skip1).
 __global__ void colswap_kernel(int32_t* A, int64_t lda, int64_t m, int64_t skip0, int64_t skip1,
                                const int* sw, int nsw, int64_t c) {
@@ -655,11 +903,23 @@ int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t* A, int64_t lda, int64_
         if (cudaFuncSetAttribute(panel_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes) !=
                 cudaSuccess ||
             cudaFuncSetAttribute(panel2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPanel2Smem) !=
+                cudaSuccess ||
+            cudaFuncSetAttribute(panel_spec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSpecSmem) !=
                 cudaSuccess)
             return fail_cuda_now();
         attr = true;
     }
     static const bool use_pair = getenv("FF_LQUP_ONECTA") == nullptr;   // experiment: one-CTA panels only
+    // speculative no-swap panels; given up after kSpecGiveUp failures (small fields)
+    constexpr int kSpecGiveUp = 2;
+    int spec_fails = getenv("FF_LQUP_NOSPEC") ? kSpecGiveUp : 0;
+    // delayed reduction in panel_spec_kernel: red (p-1)^2 + p < 2^64, a multiple of 4, <= 128
+    int red = 4;
+    {
+        const unsigned __int128 lim = (static_cast<unsigned __int128>(1) << 64) - p;
+        const unsigned __int128 sq = static_cast<unsigned __int128>(p - 1) * (p - 1);
+        while (red < 128 && static_cast<unsigned __int128>(red + 4) * sq < lim) red += 4;
+    }
     int64_t i0 = 0, c = 0, m_active = m, r = 0;
     int64_t W = std::min<int64_t>(n, kH);
     auto fail_cuda = [&]() { cudaGetLastError(); return FF_ERR_CUDA; };
@@ -688,12 +948,22 @@ int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t* A, int64_t lda, int64_
         PanelArgs pa;
         pa.A = A; pa.lda = lda; pa.i0 = i0; pa.hr = hr; pa.c = c; pa.W = Wc;
         pa.full = (c + Wc == n) ? 1 : 0;
-        pa.p = p; pa.dp = static_cast<double>(p); pa.invp = 1.0 / static_cast<double>(p);
+        pa.p = p;
         pa.mu64 = static_cast<unsigned long long>((static_cast<unsigned __int128>(1) << 64) / p);
         pa.win = win; pa.tmp = tmpd; pa.Linv = Linv; pa.Uinv = Uinv; pa.out = dout;
+        pa.red = red;
         if (cudaStreamWaitEvent(ps, ev_ready, 0) != cudaSuccess) return fail_cuda();
         bool used_pair = false;
-        if (Wc == kH && use_pair) {
+        if (Wc == kH && hr == kH && spec_fails < kSpecGiveUp) {
+            panel_spec_kernel<<<1, kThr, kSpecSmem, ps>>>(pa);
+            if (cudaGetLastError() != cudaSuccess ||
+                cudaMemcpyAsync(hout.data(), dout, hout.size() * 4, cudaMemcpyDeviceToHost, ps) != cudaSuccess ||
+                cudaStreamSynchronize(ps) != cudaSuccess)
+                return fail_cuda();
+            used_pair = !hout[1];
+            if (hout[1]) ++spec_fails;
+        }
+        if (!used_pair && Wc == kH && use_pair) {
             // the panel on a CTA pair (generic case); a zero row makes it report fail
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = dim3(2);

@@ -119,3 +119,40 @@ def test_lqup_large_freivalds(env):
     F, Q, P, rk = _factor(torch, ff, p, A)
     assert rk == oracle.rank_det(p, A)[0]
     _check_valid(p, A, F, Q, P, rk, full_product=False)
+
+
+@pytest.mark.parametrize("p", [65521, 8388593, 2147483647])
+def test_lqup_speculative_panel_matches_pivoting_panel(env, p, monkeypatch):
+    """Full 128 x 128 windows go to the speculative blocked panel (no pivot
+    search).  Without swaps the LU is unique, so the result must
+    be bit-identical to the pivoting panels' (FF_LQUP_NOSPEC), including the
+    trailing GEMMs that consume its L11^-1 / U11^-1; p = 2^31 - 1 exercises
+    the shortest delayed-reduction cadence (4 products)."""
+    torch, ff = env
+    m, n = 640, 520
+    A = ffgen.uniform_matrix(p, 33, ffgen.STREAM_A, m, n)
+    F1, Q1, P1, r1 = _factor(torch, ff, p, A)
+    monkeypatch.setenv("FF_LQUP_NOSPEC", "1")
+    F2, Q2, P2, r2 = _factor(torch, ff, p, A)
+    assert r1 == r2 == min(m, n)
+    np.testing.assert_array_equal(Q1, Q2)
+    np.testing.assert_array_equal(P1, P2)
+    np.testing.assert_array_equal(F1, F2)
+    _check_valid(p, A, F1, Q1, P1, r1)
+
+
+@pytest.mark.parametrize("row", [1, 31, 32, 70, 127, 128 + 64])
+def test_lqup_speculation_fails_mid_panel(env, row):
+    """A zero pivot at `row` (its leading minor vanishes but the row does not):
+    the speculative panel must report failure without touching A, and the
+    pivoting panel takes over (a column swap)."""
+    torch, ff = env
+    p = 65521
+    rng = np.random.default_rng(row)
+    m, n = 384, 384
+    A = rng.integers(0, p, size=(m, n)).astype(np.int32)
+    A[row, :row + 1] = A[row - 1, :row + 1]                   # row - 1 and row agree up to the diagonal
+    F, Q, P, rk = _factor(torch, ff, p, A)
+    assert rk == oracle.rank_det(p, A)[0] == n
+    assert (P != np.arange(n)).any()                          # a column swap happened
+    _check_valid(p, A, F, Q, P, rk)
