@@ -40,6 +40,7 @@ namespace {
 constexpr int kH = 128;          // panel rows
 constexpr int kThr = 1024;
 constexpr int kMaxSwaps = 2 * kH;
+constexpr int kGroup = 4;        // panels per deferred trailing update (ff_lqup_ex)
 constexpr int kSmemBytes = 2 * kH * kH * 4;   // the window + the inverse scratch in shared memory (uint32)
 
 int fail_cuda_now() {
@@ -502,9 +503,11 @@ __global__ void __launch_bounds__(kThr) panel2_kernel(PanelArgs P) {
 // back-substitution waves.  A zero pivot reports fail and nothing is written:
 // the host then runs panel2_kernel / panel_kernel, whose output is what this
 // kernel produces when no swap occurs (the LU without pivoting is unique).
-constexpr int kB = 32;
-constexpr int kSpecScratch = 2 * kB * (kH - kB);                  // u32: U12 (kB x R) + L21 (R x kB); 6 kB x kB blocks
-constexpr int kSpecSmem = (3 * kH * kH + kSpecScratch) * 4;       // window, Linv, Uinv, scratch: 216 KB
+constexpr int kB = 16;                                            // block size (kB^2 threads eliminate)
+constexpr int kNb = kH / kB;
+constexpr int kSpecScratch = 2 * kB * (kH - kB);                  // u32: U12 (kB x R) + L21 (R x kB); 2 (kNb-1) blocks
+constexpr int kSpecSmem = (3 * kH * kH + kSpecScratch) * 4;       // window, Linv, Uinv, scratch: 206 KB
+static_assert(kB == 16 || kB == 32, "block size");
 
 __device__ __forceinline__ uint32_t mulm_b(uint32_t a, uint32_t b, uint32_t p, unsigned long long mu64) {
     return residue_u64(static_cast<unsigned long long>(a) * b, mu64, p);
@@ -534,7 +537,8 @@ __device__ __forceinline__ MmJob mm_job(uint32_t* C, int ldc, const uint32_t* A,
 // output cells; a warp takes 4 rows x 32 consecutive columns, so the A reads are
 // broadcasts (16 B: four k at once) and the B reads conflict-free.  Products are
 // summed in 64 bits: kBig reduces every 4 products (any p < 2^31: 4 (p-1)^2 + p
-// < 2^64), otherwise every 32 (the host checks 32 (p-1)^2 + p < 2^64).
+// < 2^64), otherwise every kB (the host checks kB (p-1)^2 + p < 2^64).  K is a
+// multiple of kB.
 template <bool kBig>
 __device__ __forceinline__ void mm_one(const MmJob J, int lt, int nthr, uint32_t p, unsigned long long mu64) {
     const int items = (J.M / 4) * J.N;
@@ -543,9 +547,9 @@ __device__ __forceinline__ void mm_one(const MmJob J, int lt, int nthr, uint32_t
         const uint32_t* Ab = J.A + i * J.lda;
         const uint32_t* Bb = J.B + j;
         unsigned long long acc[4] = {0ull, 0ull, 0ull, 0ull};
-        for (int k0 = 0; k0 < J.K; k0 += 32) {
+        for (int k0 = 0; k0 < J.K; k0 += kB) {
 #pragma unroll
-            for (int kk = 0; kk < 32; kk += 4) {
+            for (int kk = 0; kk < kB; kk += 4) {
                 const int k = k0 + kk;
                 const uint32_t b0 = Bb[(k + 0) * J.ldb], b1 = Bb[(k + 1) * J.ldb];
                 const uint32_t b2 = Bb[(k + 2) * J.ldb], b3 = Bb[(k + 3) * J.ldb];
@@ -585,10 +589,11 @@ __global__ void __launch_bounds__(kThr) panel_spec_kernel(PanelArgs P) {
     uint32_t* T = Ui + kH * kH;               // scratch
     __shared__ uint32_t ipk[kH], isc[kH], iu[kH];
     __shared__ uint32_t ash[2][kB], bsh[2][kB];   // Shoup constants of the pivot column / row (by parity)
+    __shared__ int s_fail;
     const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
     const uint32_t p = P.p;
     const unsigned long long mu = P.mu64;
-    const bool big = P.red < 32;
+    const bool big = P.red < kB;
     long long t_0 = clock64();
     {
         constexpr int kPer = kH * kH / kThr;      // all loads in flight before any use
@@ -606,83 +611,98 @@ __global__ void __launch_bounds__(kThr) panel_spec_kernel(PanelArgs P) {
             Ui[e] = 0u;
         }
     }
+    if (tid == 0) s_fail = 0;
     __syncthreads();
     bool fail = false;
-    for (int kb = 0; kb < kH / kB; ++kb) {
+    // the kB x kB diagonal block is eliminated by threads [0, kB^2), cell (er, ec),
+    // synchronised by named barrier 1; the other warps wait at the next CTA barrier
+    const bool elim = tid < kB * kB;
+    const int er = tid / kB, ec = tid % kB;
+    for (int kb = 0; kb < kNb; ++kb) {
         const int o = kb * kB;
         uint32_t* D = W + o * kH + o;          // the diagonal block (ld kH)
         uint32_t* El = Li + o * kH + o;        // E_L, then L_D^-1
         uint32_t* Eu = Ui + o * kH + o;        // E_U, then U_D^-1
-        uint32_t x = D[ty * kH + tx], el = 0u, eu = 0u;
-        if (tx == 0) ash[0][ty] = shoup_c(x, p, mu);
-        if (ty == 0) bsh[0][tx] = shoup_c(x, p, mu);
-        uint32_t S = 1u % p;                       // S_t = prod_{t' < t} pk_t' (uniform)
-        __syncthreads();
-        // (1) pivot t (pk = D[t][t], scale S_t): rows r > t become pk row_r - a_r row_t --
-        // on D's columns > t (column t keeps the raw a_r) and on E_L's columns <= t; the
-        // columns c > t of E_U become pk col_c - D[t][c] col_t on its rows <= t.  The
-        // diagonals of E_L and E_U are implicitly S_r (never stored), every other
-        // entry outside these ranges stays zero, so each thread updates exactly one
-        // cell (ty, tx) of one of D, E_L, E_U per pivot.  Step t reads row t and column
-        // t only and writes rows / columns > t: one barrier per pivot.  All products
-        // are Shoup multiplications; the constants of the next pivot's row and column
-        // (ash: a_r and the pivot, bsh: D[t][c]) come from the threads that produce them.
-        for (int t = 0; t < kB; ++t) {
-            const int par = t & 1;
-            const uint32_t pk = D[t * kH + t];
-            if (pk == 0u) { fail = true; break; }                       // uniform: speculation failed
-            const uint32_t pk_sh = ash[par][t];
-            if (ty > t) {
-                const uint32_t a = D[ty * kH + t], a_sh = ash[par][ty];
-                if (tx > t) {
-                    x = subm_u(shoup_m(x, pk, pk_sh, p), shoup_m(D[t * kH + tx], a, a_sh, p), p);
-                    D[ty * kH + tx] = x;
-                    if (tx == t + 1) ash[par ^ 1][ty] = shoup_c(x, p, mu);
-                    if (ty == t + 1) bsh[par ^ 1][tx] = shoup_c(x, p, mu);
-                } else {
-                    const uint32_t g = (tx == t) ? S : El[t * kH + tx];
-                    el = subm_u(shoup_m(el, pk, pk_sh, p), shoup_m(g, a, a_sh, p), p);
-                    El[ty * kH + tx] = el;
+        uint32_t x = 0u, el = 0u, eu = 0u;
+        if (elim) {
+            x = D[er * kH + ec];
+            if (ec == 0) ash[0][er] = shoup_c(x, p, mu);
+            if (er == 0) bsh[0][ec] = shoup_c(x, p, mu);
+            uint32_t S = 1u % p;                   // S_t = prod_{t' < t} pk_t' (uniform)
+            ptx::named_bar_sync(1, kB * kB);
+            // (1) pivot t (pk = D[t][t], scale S_t): rows r > t become pk row_r - a_r row_t
+            // -- on D's columns > t (column t keeps the raw a_r) and on E_L's columns <= t;
+            // the columns c > t of E_U become pk col_c - D[t][c] col_t on its rows <= t.
+            // The diagonals of E_L and E_U are implicitly S_r (never stored), every other
+            // entry outside these ranges stays zero, so each thread updates exactly one
+            // cell (er, ec) of one of D, E_L, E_U per pivot.  Step t reads row t and
+            // column t only and writes rows / columns > t: one barrier per pivot.  All
+            // products are Shoup multiplications; the constants of the next pivot's row
+            // and column (ash: a_r and the pivot, bsh: D[t][c]) come from the threads
+            // that produce them.
+            for (int t = 0; t < kB; ++t) {
+                const int par = t & 1;
+                const uint32_t pk = D[t * kH + t];
+                if (pk == 0u) { fail = true; if (tid == 0) s_fail = 1; break; }   // uniform: speculation failed
+                const uint32_t pk_sh = ash[par][t];
+                if (er > t) {
+                    const uint32_t a = D[er * kH + t], a_sh = ash[par][er];
+                    if (ec > t) {
+                        x = subm_u(shoup_m(x, pk, pk_sh, p), shoup_m(D[t * kH + ec], a, a_sh, p), p);
+                        D[er * kH + ec] = x;
+                        if (ec == t + 1) ash[par ^ 1][er] = shoup_c(x, p, mu);
+                        if (er == t + 1) bsh[par ^ 1][ec] = shoup_c(x, p, mu);
+                    } else {
+                        const uint32_t g = (ec == t) ? S : El[t * kH + ec];
+                        el = subm_u(shoup_m(el, pk, pk_sh, p), shoup_m(g, a, a_sh, p), p);
+                        El[er * kH + ec] = el;
+                    }
+                } else if (ec > t) {
+                    const uint32_t h = (er == t) ? S : Eu[er * kH + t];
+                    eu = subm_u(shoup_m(eu, pk, pk_sh, p), shoup_m(h, D[t * kH + ec], bsh[par][ec], p), p);
+                    Eu[er * kH + ec] = eu;
                 }
-            } else if (tx > t) {
-                const uint32_t h = (ty == t) ? S : Eu[ty * kH + t];
-                eu = subm_u(shoup_m(eu, pk, pk_sh, p), shoup_m(h, D[t * kH + tx], bsh[par][tx], p), p);
-                Eu[ty * kH + tx] = eu;
+                S = shoup_m(S, pk, pk_sh, p);
+                ptx::named_bar_sync(1, kB * kB);
             }
-            S = shoup_m(S, pk, pk_sh, p);
-            __syncthreads();
-        }
-        if (fail) break;
-        // (2) prefix P_t and suffix Q_t products of the pivots, one inverse of P_{kB-1}:
-        // 1/S_t = inv Q_t, 1/pk_t = (1/S_{t+1}) P_{t-1}, 1/u_tt = S_t / pk_t
-        if (ty == 0) {
-            const uint32_t v = D[tx * kH + tx];
-            uint32_t pre = v, suf = v;
+            // (2) prefix P_t and suffix Q_t products of the pivots, one inverse of
+            // P_{kB-1}: 1/S_t = inv Q_t, 1/pk_t = (1/S_{t+1}) P_{t-1}, 1/u_tt = S_t / pk_t
+            if (!fail && ty == 0) {
+                const bool on = tx < kB;
+                const uint32_t v = on ? D[tx * kH + tx] : 1u;
+                uint32_t pre = v, suf = v;
 #pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, pre, d);
-                const uint32_t z = __shfl_down_sync(0xffffffffu, suf, d);
-                if (tx >= d) pre = mulm_b(pre, y, p, mu);
-                if (tx + d < 32) suf = mulm_b(suf, z, p, mu);
+                for (int d = 1; d < kB; d <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, pre, d);
+                    const uint32_t z = __shfl_down_sync(0xffffffffu, suf, d);
+                    if (tx >= d) pre = mulm_b(pre, y, p, mu);
+                    if (tx + d < kB) suf = mulm_b(suf, z, p, mu);
+                }
+                const uint32_t total = __shfl_sync(0xffffffffu, pre, kB - 1);
+                const uint32_t inv = inv_dev(total, p);
+                const uint32_t is = mulm_b(inv, suf, p, mu);              // 1 / S_tx
+                uint32_t is_next = __shfl_down_sync(0xffffffffu, is, 1);  // 1 / S_{tx+1} = 1 / P_tx
+                if (tx == kB - 1) is_next = inv;
+                uint32_t pprev = __shfl_up_sync(0xffffffffu, pre, 1);    // P_{tx-1} = S_tx
+                if (tx == 0) pprev = 1u % p;
+                const uint32_t ip = mulm_b(is_next, pprev, p, mu);
+                if (on) {
+                    isc[o + tx] = is;
+                    ipk[o + tx] = ip;
+                    iu[o + tx] = mulm_b(pprev, ip, p, mu);
+                }
             }
-            const uint32_t total = __shfl_sync(0xffffffffu, pre, 31);
-            const uint32_t inv = inv_dev(total, p);
-            const uint32_t is = mulm_b(inv, suf, p, mu);                  // 1 / S_tx
-            uint32_t is_next = __shfl_down_sync(0xffffffffu, is, 1);      // 1 / S_{tx+1} = 1 / P_tx
-            if (tx == 31) is_next = inv;
-            uint32_t pprev = __shfl_up_sync(0xffffffffu, pre, 1);        // P_{tx-1} = S_tx
-            if (tx == 0) pprev = 1u % p;
-            const uint32_t ip = mulm_b(is_next, pprev, p, mu);
-            isc[o + tx] = is;
-            ipk[o + tx] = ip;
-            iu[o + tx] = mulm_b(pprev, ip, p, mu);
         }
         __syncthreads();
+        fail = s_fail != 0;
+        if (fail) break;
         // true L_D (a / pk_c), U_D (row / S_r); L_D^-1 = E_L / S_r (unit diagonal);
         // U_D^-1 = E_U / pk_c (E_U col c = S_c U'^-1 col c, U_D^-1 = U'^-1 diag(S_c / pk_c))
-        D[ty * kH + tx] = mulm_b(x, ty > tx ? ipk[o + tx] : isc[o + ty], p, mu);
-        El[ty * kH + tx] = tx < ty ? mulm_b(el, isc[o + ty], p, mu) : (tx == ty ? 1u : 0u);
-        Eu[ty * kH + tx] = ty < tx ? mulm_b(eu, ipk[o + tx], p, mu) : (tx == ty ? iu[o + tx] : 0u);
+        if (elim) {
+            D[er * kH + ec] = mulm_b(x, er > ec ? ipk[o + ec] : isc[o + er], p, mu);
+            El[er * kH + ec] = ec < er ? mulm_b(el, isc[o + er], p, mu) : (ec == er ? 1u : 0u);
+            Eu[er * kH + ec] = er < ec ? mulm_b(eu, ipk[o + ec], p, mu) : (ec == er ? iu[o + ec] : 0u);
+        }
         __syncthreads();
         // (3) U12 = L_D^-1 A12 (T1, kB x R) and L21 = A21 U_D^-1 (T2, R x kB), then
         // A22 -= L21 U12 while T1, T2 are copied into the window
@@ -706,9 +726,9 @@ __global__ void __launch_bounds__(kThr) panel_spec_kernel(PanelArgs P) {
     if (!fail) {
         // full inverses by block waves d = j - i (block units), a warp group per block:
         //   Li_ij = -Li_ii (sum_{k=j}^{i-1} L_ik Li_kj),  Ui_ij = -Ui_ii (sum_{k=i+1}^{j} U_ik Ui_kj)
-        constexpr int nb = kH / kB;
+        constexpr int nb = kNb;
         for (int d = 1; d < nb; ++d) {
-            const int n = 2 * (nb - d);                  // jobs: (L, U) per block pair; <= 6 scratch blocks
+            const int n = 2 * (nb - d);                  // jobs: (L, U) per block pair; <= 2 (kNb - 1) scratch blocks
             const int wpj = 32 / n, q = ty / wpj, lt = tid - q * wpj * 32;
             const bool on = q < n;
             const int i = d + q / 2;
@@ -807,7 +827,7 @@ int lqup_ws(uint32_t p, int64_t m, int64_t n, const ff_opts* opts, LqupWs* w) {
     w->linv = w->uinv = align256(2 * static_cast<size_t>(kH) * kH * 4);          // double-buffered (lookahead)
     w->out = align256(2 * ((4 + 4 * kMaxSwaps) * 4 + 64));
     w->pairs = align256(4 * kMaxSwaps * 8);
-    // GEMMs: K <= kH; M <= m, N <= n (a CRT plan for short K has the most planes)
+    // GEMMs: K <= kH kGroup; M <= m, N <= n (a CRT plan for short K has the most planes)
     size_t g = 0;
     for (int crt = 0; crt < 2; ++crt) {
         ff_opts o;
@@ -815,8 +835,10 @@ int lqup_ws(uint32_t p, int64_t m, int64_t n, const ff_opts* opts, LqupWs* w) {
         if (opts) o = *opts;
         if (crt) { o.scheme = FF_SCHEME_CRT; o.kb_override = 0; }
         Plan pl;
-        if (make_plan(p, kH, &o, &pl) == 0) g = std::max(g, gemm_ws_bytes(pl, m, n));
-        else if (!crt) return FF_ERR_OPTS;
+        for (int64_t K : {static_cast<int64_t>(kH), static_cast<int64_t>(kH) * kGroup}) {
+            if (make_plan(p, K, &o, &pl) == 0) g = std::max(g, gemm_ws_bytes(pl, m, n));
+            else if (!crt) return FF_ERR_OPTS;
+        }
     }
     w->gemm = align256(g);
     return 0;
@@ -939,6 +961,21 @@ int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t* A, int64_t lda, int64_
     } cleanup{ps, ev_ready, ev_panel};
     if (cudaEventRecord(ev_ready, st) != cudaSuccess) return fail_cuda();
     int buf = 0;
+    const int group = [] {
+        const char* g = getenv("FF_LQUP_GROUP");                // experiment knob (1 = no deferral)
+        const int v = g ? atoi(g) : kGroup;
+        return v < 1 ? 1 : (v > kGroup ? kGroup : v);
+    }();
+    int npend = 0;
+    int64_t pi0 = 0, pc0 = 0;
+    // rows [ra, rb) x columns [ca, cb) -= A[ra.., pc0 .. pc0 + K) A[pi0 .. pi0 + K, ca..cb)
+    auto upd = [&](int64_t ra, int64_t rb, int64_t ca, int64_t cb, int64_t K, int reserve) -> int {
+        rb = std::min<int64_t>(rb, m_active);
+        cb = std::min<int64_t>(cb, n);
+        if (rb <= ra || cb <= ca || K <= 0) return 0;
+        return gemm_plain(p, opts, 'N', 'N', rb - ra, cb - ca, K, neg1, A + ra * lda + pc0, lda, A + pi0 * lda + ca, lda,
+                          1, A + ra * lda + ca, lda, gws, st, reserve);
+    };
     while (i0 < m_active && c < n) {
         int32_t* Linv = Linv2 + static_cast<size_t>(buf) * kH * kH;
         int32_t* Uinv = Uinv2 + static_cast<size_t>(buf) * kH * kH;
@@ -1026,7 +1063,49 @@ int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t* A, int64_t lda, int64_
         }
         const int64_t z = hr - kk;
         bool ready_recorded = false;
-        if (kk > 0) {
+        // Deferred trailing updates: for a group of up to `group` generic
+        // panels (kk = hr = W = kH) the Schur-complement updates of the rows and columns
+        // beyond the group are applied once, as one GEMM with K = kH x (panels); only the
+        // next panel's rows and window columns are brought up to date in between.  The
+        // short-K update GEMM is bound by its epilogue (the C read / write and the
+        // reduction), not by K, so this divides the dominant cost by the group size.
+        // Invariant while npend > 0: the pending panels (rows [pi0, i0), L columns
+        // [pc0, c)) have not yet updated rows >= i0 + kH at columns >= c + kH.
+        const bool generic = group > 1 && kk == kH && hr == kH && Wc == kH;
+        if (npend > 0 && !generic) {                 // bring everything up to date first
+            if ((e = upd(i0 + kH, m_active, c + kH, n, c - pc0, 0))) return e;
+            npend = 0;
+        }
+        if (generic) {
+            if (c + Wc < n) {                        // U_rest = L11^-1 A_rest (rows up to date)
+                int32_t* Ar = A + i0 * lda + c + Wc;
+                if ((e = gemm_plain(p, opts, 'N', 'N', kk, n - c - Wc, kk, 1, Linv, kH, Ar, lda, 0, Ar, lda, gws, st)))
+                    return e;
+            }
+            if (i0 + kH < m_active) {                // G = X U11^-1 (window columns up to date)
+                int32_t* X = A + (i0 + kH) * lda + c;
+                if ((e = gemm_plain(p, opts, 'N', 'N', m_active - i0 - kH, kk, kk, 1, X, lda, Uinv, kH, 0, X, lda, gws, st)))
+                    return e;
+            }
+            if (npend == 0) { pi0 = i0; pc0 = c; }
+            ++npend;
+            const int64_t r1 = i0 + kH, c1 = c + kH, K = c1 - pc0;
+            if (npend == group || r1 + kH >= m_active || c1 + kH >= n) {
+                // flush: the next panel's rows first (they release its panel kernel), then the rest
+                const int64_t rn = std::min<int64_t>(m_active, r1 + kH);
+                if ((e = upd(r1, rn, c1, n, K, 0))) return e;
+                if (cudaEventRecord(ev_ready, st) != cudaSuccess) return fail_cuda();
+                if ((e = upd(rn, m_active, c1, n, K, kReserve))) return e;
+                npend = 0;
+            } else {
+                // lookahead: the next panel's rows (all columns), then the next window's
+                // columns of the rows below it
+                if ((e = upd(r1, r1 + kH, c1, n, K, 0))) return e;
+                if (cudaEventRecord(ev_ready, st) != cudaSuccess) return fail_cuda();
+                if ((e = upd(r1 + kH, m_active, c1, c1 + kH, K, 0))) return e;
+            }
+            ready_recorded = true;
+        } else if (kk > 0) {
             // U of the pivot rows beyond the window: U_rest = L11^-1 A_rest (in place, beta = 0)
             if (c + Wc < n) {
                 int32_t* Ar = A + i0 * lda + c + Wc;
@@ -1082,6 +1161,10 @@ int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t* A, int64_t lda, int64_
         c += kk;
         r += kk;
         W = std::min<int64_t>(n, kH);
+    }
+    if (npend > 0) {                                            // (not reached: the last group flushes)
+        if ((e = upd(i0 + kH, m_active, c + kH, n, c - pc0, 0))) return e;
+        npend = 0;
     }
     // rows that never got a pivot (c reached n): their U part is already zero
     *rank = r;

@@ -241,6 +241,10 @@ __device__ __forceinline__ uint32_t cluster_ctarank() {
     return r;
 }
 
+// named barrier `id` over `n` threads (a multiple of 32)
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
 __device__ __forceinline__ void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }

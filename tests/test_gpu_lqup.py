@@ -156,3 +156,26 @@ def test_lqup_speculation_fails_mid_panel(env, row):
     assert rk == oracle.rank_det(p, A)[0] == n
     assert (P != np.arange(n)).any()                          # a column swap happened
     _check_valid(p, A, F, Q, P, rk)
+
+
+@pytest.mark.parametrize("dep_row", [None, 700, 1000])
+def test_lqup_deferred_updates_match_immediate(env, dep_row, monkeypatch):
+    """Groups of generic panels defer their trailing updates into one GEMM with
+    K = 128 x (panels).  The arithmetic is exact, so the result
+    must be bit-identical to immediate updates (FF_LQUP_GROUP=1); a dependent
+    row inside a later panel (rank deficiency: zero row) forces a flush in the
+    middle of a group."""
+    torch, ff = env
+    p = 65521
+    m, n = 1100, 1060
+    A = ffgen.uniform_matrix(p, 41, ffgen.STREAM_A, m, n)
+    if dep_row is not None:
+        A[dep_row] = ((A[100].astype(np.int64) + 3 * A[200]) % p).astype(np.int32)
+    F1, Q1, P1, r1 = _factor(torch, ff, p, A)
+    monkeypatch.setenv("FF_LQUP_GROUP", "1")
+    F2, Q2, P2, r2 = _factor(torch, ff, p, A)
+    assert r1 == r2 == oracle.rank_det(p, A)[0]
+    np.testing.assert_array_equal(Q1, Q2)
+    np.testing.assert_array_equal(P1, P2)
+    np.testing.assert_array_equal(F1, F2)
+    _check_valid(p, A, F1, Q1, P1, r1)
