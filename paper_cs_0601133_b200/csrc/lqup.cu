@@ -40,7 +40,7 @@ namespace {
 constexpr int kH = 128;          // panel rows
 constexpr int kThr = 1024;
 constexpr int kMaxSwaps = 2 * kH;
-constexpr int kGroup = 4;        // panels per deferred trailing update (ff_lqup_ex)
+constexpr int kGroup = 8;        // panels per deferred trailing update (ff_lqup_ex)
 constexpr int kSmemBytes = 2 * kH * kH * 4;   // the window + the inverse scratch in shared memory (uint32)
 
 int fail_cuda_now() {
