@@ -46,6 +46,7 @@ template <int L, int SCHEME>
 __global__ void __launch_bounds__(256) encode_direct_kernel(ModP M, int64_t rows, int64_t k, int64_t k_pad,
                                                             const int32_t* __restrict__ X, int64_t ldx,
                                                             int8_t* __restrict__ limbs, int vec_ok) {
+    ptx::pdl_trigger();   // the GEMM that consumes these limbs may start its prologue
     const int64_t groups = k_pad / 4;
     const int64_t plane = rows * k_pad;
     for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
@@ -85,6 +86,7 @@ template <int L, int SCHEME>
 __global__ void __launch_bounds__(256) encode_trans_kernel(ModP M, int64_t rows, int64_t k, int64_t k_pad,
                                                            const int32_t* __restrict__ X, int64_t ldx,
                                                            int8_t* __restrict__ limbs) {
+    ptx::pdl_trigger();   // the GEMM that consumes these limbs may start its prologue
     __shared__ __align__(16) uint8_t tile[L][kTR][kPitch];
     const int64_t plane = rows * k_pad;
     const int64_t tiles_r = (rows + kTR - 1) / kTR;
@@ -153,6 +155,7 @@ template <int L, int SCHEME>
 __global__ void __launch_bounds__(256) encode_trans_tma_kernel(const __grid_constant__ CUtensorMap tmX, ModP M,
                                                                int64_t rows, int64_t k_pad,
                                                                int8_t* __restrict__ limbs) {
+    ptx::pdl_trigger();   // the GEMM that consumes these limbs may start its prologue
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int32_t* ring = reinterpret_cast<const int32_t*>(sm);
@@ -283,6 +286,7 @@ __global__ void __launch_bounds__(256) encode_crt_direct_kernel(ModP M, CrtConst
                                                                 int64_t k_pad, const int32_t* __restrict__ X,
                                                                 int64_t ldx, int8_t* __restrict__ planes,
                                                                 int vec_ok) {
+    ptx::pdl_trigger();   // the GEMM that consumes these limbs may start its prologue
     const int64_t groups = k_pad / 16;
     const int64_t plane = rows * k_pad;
     for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
@@ -337,6 +341,7 @@ __global__ void __launch_bounds__(256) encode_crt_direct_kernel(ModP M, CrtConst
 __global__ void __launch_bounds__(256) encode_crt_trans_kernel(ModP M, CrtConsts C, int64_t rows, int64_t k,
                                                                int64_t k_pad, const int32_t* __restrict__ X,
                                                                int64_t ldx, int8_t* __restrict__ planes) {
+    ptx::pdl_trigger();   // the GEMM that consumes these limbs may start its prologue
     __shared__ __align__(16) uint8_t tile[4][kTR][kPitch];
     const int64_t plane = rows * k_pad;
     const int64_t tiles_r = (rows + kTR - 1) / kTR;
@@ -426,6 +431,7 @@ constexpr int kCrtTmaSmem = kCrtStages * kTmaTileBytes + kMaxMod * kTR * kPitch 
 __global__ void __launch_bounds__(256) encode_crt_trans_tma_kernel(const __grid_constant__ CUtensorMap tmX, ModP M,
                                                                    CrtConsts C, int64_t rows, int64_t k_pad,
                                                                    int8_t* __restrict__ planes) {
+    ptx::pdl_trigger();   // the GEMM that consumes these limbs may start its prologue
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int32_t* ring = reinterpret_cast<const int32_t*>(sm);

@@ -151,6 +151,9 @@ __device__ __forceinline__ void for_each_step(const GemmArgs& a, int unit, int n
     }
 }
 
+// programmatic dependent launch of the GEMM after its encoders (FF_NOPDL=1: off)
+const bool g_pdl = getenv("FF_NOPDL") == nullptr;
+
 template <int kPair, bool kTrace>
 __global__ void __launch_bounds__(kThreads, 1)
     ffgemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -223,6 +226,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     const int unit = sh->sched[0], nunits = sh->sched[1], tbase = sh->sched[2], tcount = sh->sched[3];
     const uint32_t tmem_base = sh->tmem_base;
+    // launched programmatically after the encoders: everything above overlapped
+    // them; the limb planes (TMA), C and the scratch are read only from here on
+    ptx::pdl_wait();
 
     if (warp == 0) {
         // ------------------------------------------------ TMA producer (both CTAs)
@@ -706,15 +712,17 @@ int launch_impl(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = K::SMEM;
     cfg.stream = st;
-    cudaLaunchAttribute attr[2];
+    cudaLaunchAttribute attr[3];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = kPair;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
-    attr[1].id = cudaLaunchAttributeCooperative;   // all CTAs co-resident (die-aware registration)
-    attr[1].val.cooperative = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // prologue overlaps the encoders
+    attr[1].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+    attr[2].id = cudaLaunchAttributeCooperative;   // all CTAs co-resident (die-aware registration)
+    attr[2].val.cooperative = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = a.die_map ? 2 : 1;
+    cfg.numAttrs = a.die_map ? 3 : 2;
     const cudaError_t lerr = tracing ? cudaLaunchKernelEx(&cfg, ffgemm_tc_kernel<kPair, true>, mapA, mapB, a)
                                      : cudaLaunchKernelEx(&cfg, ffgemm_tc_kernel<kPair, false>, mapA, mapB, a);
     if (lerr != cudaSuccess) return FF_ERR_CUDA;
