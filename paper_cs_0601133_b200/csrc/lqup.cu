@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cstring>
 #include <vector>
 #include <cstdio>
@@ -961,6 +962,9 @@ int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t* A, int64_t lda, int64_
     } cleanup{ps, ev_ready, ev_panel};
     if (cudaEventRecord(ev_ready, st) != cudaSuccess) return fail_cuda();
     int buf = 0;
+    // FF_LQUP_TIMELINE=1 (development aid): per-panel event timestamps, printed at the end
+    const bool tl = getenv("FF_LQUP_TIMELINE") != nullptr;
+    std::vector<std::array<cudaEvent_t, 4>> tl_ev;
     const int group = [] {
         const char* g = getenv("FF_LQUP_GROUP");                // experiment knob (1 = no deferral)
         const int v = g ? atoi(g) : kGroup;
@@ -990,6 +994,7 @@ int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t* A, int64_t lda, int64_
         pa.win = win; pa.tmp = tmpd; pa.Linv = Linv; pa.Uinv = Uinv; pa.out = dout;
         pa.red = red;
         if (cudaStreamWaitEvent(ps, ev_ready, 0) != cudaSuccess) return fail_cuda();
+        if (tl) { tl_ev.emplace_back(); for (auto& x : tl_ev.back()) cudaEventCreate(&x); cudaEventRecord(tl_ev.back()[0], ps); }
         bool used_pair = false;
         if (Wc == kH && hr == kH && spec_fails < kSpecGiveUp) {
             panel_spec_kernel<<<1, kThr, kSpecSmem, ps>>>(pa);
@@ -1025,8 +1030,10 @@ int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t* A, int64_t lda, int64_
             if (cudaMemcpyAsync(hout.data(), dout, hout.size() * 4, cudaMemcpyDeviceToHost, ps) != cudaSuccess)
                 return fail_cuda();
         }
+        if (tl) cudaEventRecord(tl_ev.back()[1], ps);
         if (cudaEventRecord(ev_panel, ps) != cudaSuccess || cudaStreamSynchronize(ps) != cudaSuccess)
             return fail_cuda();
+        if (tl) cudaEventRecord(tl_ev.back()[2], st);   // host turnaround: GEMM work enqueued from here
         if (cudaStreamWaitEvent(st, ev_panel, 0) != cudaSuccess) return fail_cuda();
         const int64_t kk = hout[0];
         if (getenv("FF_LQUP_TRACE")) {
@@ -1082,27 +1089,32 @@ int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t* A, int64_t lda, int64_
                 if ((e = gemm_plain(p, opts, 'N', 'N', kk, n - c - Wc, kk, 1, Linv, kH, Ar, lda, 0, Ar, lda, gws, st)))
                     return e;
             }
-            if (i0 + kH < m_active) {                // G = X U11^-1 (window columns up to date)
-                int32_t* X = A + (i0 + kH) * lda + c;
-                if ((e = gemm_plain(p, opts, 'N', 'N', m_active - i0 - kH, kk, kk, 1, X, lda, Uinv, kH, 0, X, lda, gws, st)))
-                    return e;
-            }
+            // G = X U11^-1 (window columns up to date): the next panel's rows now, the
+            // rows below it once that panel kernel has been released
+            auto gmul = [&](int64_t ra, int64_t rb) -> int {
+                rb = std::min<int64_t>(rb, m_active);
+                if (rb <= ra) return 0;
+                int32_t* X = A + ra * lda + c;
+                return gemm_plain(p, opts, 'N', 'N', rb - ra, kk, kk, 1, X, lda, Uinv, kH, 0, X, lda, gws, st);
+            };
             if (npend == 0) { pi0 = i0; pc0 = c; }
             ++npend;
-            const int64_t r1 = i0 + kH, c1 = c + kH, K = c1 - pc0;
+            const int64_t r1 = i0 + kH, c1 = c + kH, K = c1 - pc0, rn = std::min<int64_t>(m_active, r1 + kH);
+            if ((e = gmul(r1, rn))) return e;
             if (npend == group || r1 + kH >= m_active || c1 + kH >= n) {
                 // flush: the next panel's rows first (they release its panel kernel), then the rest
-                const int64_t rn = std::min<int64_t>(m_active, r1 + kH);
                 if ((e = upd(r1, rn, c1, n, K, 0))) return e;
                 if (cudaEventRecord(ev_ready, st) != cudaSuccess) return fail_cuda();
+                if ((e = gmul(rn, m_active))) return e;
                 if ((e = upd(rn, m_active, c1, n, K, kReserve))) return e;
                 npend = 0;
             } else {
                 // lookahead: the next panel's rows (all columns), then the next window's
                 // columns of the rows below it
-                if ((e = upd(r1, r1 + kH, c1, n, K, 0))) return e;
+                if ((e = upd(r1, rn, c1, n, K, 0))) return e;
                 if (cudaEventRecord(ev_ready, st) != cudaSuccess) return fail_cuda();
-                if ((e = upd(r1 + kH, m_active, c1, c1 + kH, K, 0))) return e;
+                if ((e = gmul(rn, m_active))) return e;
+                if ((e = upd(rn, m_active, c1, c1 + kH, K, 0))) return e;
             }
             ready_recorded = true;
         } else if (kk > 0) {
@@ -1157,6 +1169,7 @@ int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t* A, int64_t lda, int64_
             m_active -= z;
         }
         if (!ready_recorded && cudaEventRecord(ev_ready, st) != cudaSuccess) return fail_cuda();
+        if (tl) cudaEventRecord(tl_ev.back()[3], st);   // (after the whole iteration's work)
         i0 += kk;
         c += kk;
         r += kk;
@@ -1165,6 +1178,22 @@ int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t* A, int64_t lda, int64_
     if (npend > 0) {                                            // (not reached: the last group flushes)
         if ((e = upd(i0 + kH, m_active, c + kH, n, c - pc0, 0))) return e;
         npend = 0;
+    }
+    if (tl) {
+        cudaStreamSynchronize(st);
+        cudaStreamSynchronize(ps);
+        double sp = 0, sg = 0, sc = 0;
+        for (size_t i = 0; i < tl_ev.size(); ++i) {
+            float a = 0, b = 0, c2 = 0;
+            cudaEventElapsedTime(&a, tl_ev[i][0], tl_ev[i][1]);              // panel kernel
+            cudaEventElapsedTime(&b, tl_ev[i][1], tl_ev[i][2]);              // panel end -> host enqueues
+            if (i + 1 < tl_ev.size()) cudaEventElapsedTime(&c2, tl_ev[i][1], tl_ev[i + 1][0]);   // panel end -> next panel start
+            sp += a; sg += b; sc += c2;
+        }
+        const double np = tl_ev.empty() ? 1.0 : static_cast<double>(tl_ev.size());
+        fprintf(stderr, "[lqup timeline] panels %zu: panel kernel %.1f us, panel end -> host enqueue %.1f us, "
+                "panel end -> next panel start %.1f us (averages)\n", tl_ev.size(), 1e3 * sp / np, 1e3 * sg / np, 1e3 * sc / np);
+        for (auto& e4 : tl_ev) for (auto& x : e4) cudaEventDestroy(x);
     }
     // rows that never got a pivot (c reached n): their U part is already zero
     *rank = r;
