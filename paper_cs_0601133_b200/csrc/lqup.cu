@@ -25,6 +25,7 @@
 
 #include <algorithm>
 #include <array>
+#include <chrono>
 #include <cstring>
 #include <vector>
 #include <cstdio>
@@ -808,12 +809,24 @@ int gemm_plain(uint32_t p, const ff_opts* opts, char tX, char tY, int64_t m, int
                const int32_t* X, int64_t ldx, const int32_t* Y, int64_t ldy, uint32_t beta, int32_t* C, int64_t ldc,
                void* ws, cudaStream_t st, int reserve_sms = 0) {
     if (m == 0 || n == 0) return 0;
+    static const bool host_t = getenv("FF_LQUP_HOSTTIME") != nullptr;   // development aid
+    const auto h0 = std::chrono::steady_clock::now();
     Plan pl;
     int e = make_plan(p, k, opts, &pl);
     if (e) return e;
     set_scalars(&pl, alpha, beta);
     pl.reserve_sms = reserve_sms;
-    return gemm_dev(pl, tX, tY, m, n, k, X, ldx, Y, ldy, C, ldc, ws, st);
+    const auto h1 = std::chrono::steady_clock::now();
+    e = gemm_dev(pl, tX, tY, m, n, k, X, ldx, Y, ldy, C, ldc, ws, st);
+    if (host_t) {
+        const auto h2 = std::chrono::steady_clock::now();
+        static double tp = 0, tg = 0;
+        static long cnt = 0;
+        tp += std::chrono::duration<double, std::micro>(h1 - h0).count();
+        tg += std::chrono::duration<double, std::micro>(h2 - h1).count();
+        if (++cnt % 200 == 0) fprintf(stderr, "[gemm_plain host] %ld calls: plan %.1f us, enqueue %.1f us (avg)\n", cnt, tp / cnt, tg / cnt);
+    }
+    return e;
 }
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -964,7 +977,7 @@ int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t* A, int64_t lda, int64_
     int buf = 0;
     // FF_LQUP_TIMELINE=1 (development aid): per-panel event timestamps, printed at the end
     const bool tl = getenv("FF_LQUP_TIMELINE") != nullptr;
-    std::vector<std::array<cudaEvent_t, 4>> tl_ev;
+    std::vector<std::array<cudaEvent_t, 6>> tl_ev;
     const int group = [] {
         const char* g = getenv("FF_LQUP_GROUP");                // experiment knob (1 = no deferral)
         const int v = g ? atoi(g) : kGroup;
@@ -1089,6 +1102,7 @@ int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t* A, int64_t lda, int64_
                 if ((e = gemm_plain(p, opts, 'N', 'N', kk, n - c - Wc, kk, 1, Linv, kH, Ar, lda, 0, Ar, lda, gws, st)))
                     return e;
             }
+            if (tl) cudaEventRecord(tl_ev.back()[4], st);
             // G = X U11^-1 (window columns up to date): the next panel's rows now, the
             // rows below it once that panel kernel has been released
             auto gmul = [&](int64_t ra, int64_t rb) -> int {
@@ -1101,6 +1115,7 @@ int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t* A, int64_t lda, int64_
             ++npend;
             const int64_t r1 = i0 + kH, c1 = c + kH, K = c1 - pc0, rn = std::min<int64_t>(m_active, r1 + kH);
             if ((e = gmul(r1, rn))) return e;
+            if (tl) cudaEventRecord(tl_ev.back()[5], st);
             if (npend == group || r1 + kH >= m_active || c1 + kH >= n) {
                 // flush: the next panel's rows first (they release its panel kernel), then the rest
                 if ((e = upd(r1, rn, c1, n, K, 0))) return e;
@@ -1182,9 +1197,13 @@ int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t* A, int64_t lda, int64_
     if (tl) {
         cudaStreamSynchronize(st);
         cudaStreamSynchronize(ps);
-        double sp = 0, sg = 0, sc = 0;
+        double sp = 0, sg = 0, sc = 0, su = 0, sgg = 0, si = 0;
         for (size_t i = 0; i < tl_ev.size(); ++i) {
-            float a = 0, b = 0, c2 = 0;
+            float a = 0, b = 0, c2 = 0, u = 0, g = 0, ii = 0;
+            if (cudaEventElapsedTime(&u, tl_ev[i][2], tl_ev[i][4]) != cudaSuccess) { u = 0; cudaGetLastError(); }
+            if (cudaEventElapsedTime(&g, tl_ev[i][4], tl_ev[i][5]) != cudaSuccess) { g = 0; cudaGetLastError(); }
+            if (i + 1 < tl_ev.size() && cudaEventElapsedTime(&ii, tl_ev[i][5], tl_ev[i + 1][0]) != cudaSuccess) { ii = 0; cudaGetLastError(); }
+            su += u; sgg += g; si += ii;
             cudaEventElapsedTime(&a, tl_ev[i][0], tl_ev[i][1]);              // panel kernel
             cudaEventElapsedTime(&b, tl_ev[i][1], tl_ev[i][2]);              // panel end -> host enqueues
             if (i + 1 < tl_ev.size()) cudaEventElapsedTime(&c2, tl_ev[i][1], tl_ev[i + 1][0]);   // panel end -> next panel start
@@ -1192,7 +1211,9 @@ int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t* A, int64_t lda, int64_
         }
         const double np = tl_ev.empty() ? 1.0 : static_cast<double>(tl_ev.size());
         fprintf(stderr, "[lqup timeline] panels %zu: panel kernel %.1f us, panel end -> host enqueue %.1f us, "
-                "panel end -> next panel start %.1f us (averages)\n", tl_ev.size(), 1e3 * sp / np, 1e3 * sg / np, 1e3 * sc / np);
+                "panel end -> next panel start %.1f us (averages); chain: U_rest %.1f us, G(next rows) %.1f us, "
+                "lookahead row update -> next panel start %.1f us\n", tl_ev.size(), 1e3 * sp / np, 1e3 * sg / np,
+                1e3 * sc / np, 1e3 * su / np, 1e3 * sgg / np, 1e3 * si / np);
         for (auto& e4 : tl_ev) for (auto& x : e4) cudaEventDestroy(x);
     }
     // rows that never got a pivot (c reached n): their U part is already zero
