@@ -578,8 +578,72 @@ __device__ __forceinline__ void mm_one(const MmJob J, int lt, int nthr, uint32_t
         }
     }
 }
+// The same job on the tensor cores (warp-level mma.sync m16n8k32 u8 x u8 -> s32),
+// for p < 2^16: residues split into two bytes, x = x0 + 256 x1, so that
+// A B = P00 + 256 (P01 + P10) + 65536 P11 with four byte products, each exact in
+// s32 (K <= 128: K 255^2 < 2^24), recombined in 64 bits and reduced once.  A
+// warp computes a 16 x 8 tile; the fragments are built straight from the u32
+// matrices (A: one 16 B load gives four k of a row; B: four loads down a column)
+// and their bytes gathered with byte permutes.  K is zero-padded to 32.
+__device__ __forceinline__ void imma16832(int (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                          uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+        : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+// bytes 0 (lo) and 1 (hi) of four residues < 2^16, packed in order
+__device__ __forceinline__ void split4(uint32_t x, uint32_t y, uint32_t z, uint32_t w, uint32_t& lo, uint32_t& hi) {
+    const uint32_t t0 = __byte_perm(x, y, 0x5140), t1 = __byte_perm(z, w, 0x5140);   // x0 y0 x1 y1 | z0 w0 z1 w1
+    lo = __byte_perm(t0, t1, 0x5410);
+    hi = __byte_perm(t0, t1, 0x7632);
+}
+__device__ void mm_tc(const MmJob J, int wg, int nw, uint32_t p, unsigned long long mu64) {
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const int tiles_n = J.N / 8, tiles = (J.M / 16) * tiles_n;
+    for (int tile = wg; tile < tiles; tile += nw) {
+        const int r0 = (tile / tiles_n) * 16, c0 = (tile % tiles_n) * 8;
+        int P00[4] = {0, 0, 0, 0}, P01[4] = {0, 0, 0, 0}, P10[4] = {0, 0, 0, 0}, P11[4] = {0, 0, 0, 0};
+        for (int k0 = 0; k0 < J.K; k0 += 32) {
+            uint32_t alo[4], ahi[4], blo[2], bhi[2];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {              // a0: row g, a1: row g+8; a2, a3: k + 16
+                const int row = r0 + g + ((q & 1) ? 8 : 0), k = k0 + ((q & 2) ? 16 : 0) + 4 * t;
+                uint4 v = make_uint4(0u, 0u, 0u, 0u);
+                if (k < J.K) v = *reinterpret_cast<const uint4*>(J.A + row * J.lda + k);
+                split4(v.x, v.y, v.z, v.w, alo[q], ahi[q]);
+            }
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {              // b0: column g, k = 4t..; b1: k + 16
+                const int k = k0 + (q ? 16 : 0) + 4 * t;
+                const uint32_t* bp = J.B + k * J.ldb + c0 + g;
+                uint32_t x = 0, y = 0, z = 0, w = 0;
+                if (k < J.K) { x = bp[0]; y = bp[J.ldb]; z = bp[2 * J.ldb]; w = bp[3 * J.ldb]; }
+                split4(x, y, z, w, blo[q], bhi[q]);
+            }
+            imma16832(P00, alo[0], alo[1], alo[2], alo[3], blo[0], blo[1]);
+            imma16832(P01, alo[0], alo[1], alo[2], alo[3], bhi[0], bhi[1]);
+            imma16832(P10, ahi[0], ahi[1], ahi[2], ahi[3], blo[0], blo[1]);
+            imma16832(P11, ahi[0], ahi[1], ahi[2], ahi[3], bhi[0], bhi[1]);
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {                  // d0, d1: row g, cols 2t, 2t+1; d2, d3: row g+8
+            const unsigned long long S = static_cast<unsigned long long>(static_cast<uint32_t>(P00[e])) +
+                                         (static_cast<unsigned long long>(static_cast<uint32_t>(P01[e]) +
+                                                                          static_cast<uint32_t>(P10[e])) << 8) +
+                                         (static_cast<unsigned long long>(static_cast<uint32_t>(P11[e])) << 16);
+            const uint32_t r = residue_u64(S, mu64, p);
+            uint32_t* c = J.C + (r0 + g + ((e & 2) ? 8 : 0)) * J.ldc + c0 + 2 * t + (e & 1);
+            if (J.mode == 0) *c = r;
+            else if (J.mode == 1) *c = subm_u(*c, r, p);
+            else *c = r ? p - r : 0u;
+        }
+    }
+}
+
 __device__ __forceinline__ void mm_any(bool big, const MmJob& J, int lt, int nthr, uint32_t p, unsigned long long mu64) {
-    if (big) mm_one<true>(J, lt, nthr, p, mu64);
+    if (p < 65536u) mm_tc(J, lt >> 5, nthr >> 5, p, mu64);     // (groups are whole warps)
+    else if (big) mm_one<true>(J, lt, nthr, p, mu64);
     else mm_one<false>(J, lt, nthr, p, mu64);
 }
 
