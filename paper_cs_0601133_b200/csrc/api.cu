@@ -143,10 +143,24 @@ size_t gemm_ws_bytes(const Plan& pl, int64_t m, int64_t n) { return ws_bytes(pl,
 namespace {
 
 // The whole path on device pointers.
+// Small-field latency path (gemm_small.cu) for short K and small problems:
+// FF_SMALL=0 never, FF_SMALL=1 whenever valid (experiments); default by size.
+bool prefer_small(int64_t m, int64_t n, int64_t k) {
+    const char* env = getenv("FF_SMALL");
+    const int mode = env ? atoi(env) : -1;
+    if (mode >= 0) return mode > 0;
+    // measured (p = 65521, alpha = -1, beta = 1): 128^3 19.9 vs 31.5 us, 128 x 8192 x 128
+    // 21.9 vs 33.3 us; but 512^3 40.8 vs 36.4 us, 128 x 8192 x 1024 98 vs 51 us and
+    // 4096^2 x 128 233 vs 90 us -- the tcgen05 path wins beyond short K and ~2M outputs
+    return k <= 256 && m * n <= (int64_t{1} << 21);
+}
+
 int run(const Plan& pl, char transA, char transB, int64_t m, int64_t n, int64_t k, const int32_t* A,
         int64_t lda, const int32_t* B, int64_t ldb, int32_t* C, int64_t ldc, void* ws, cudaStream_t st) {
     if (k == 0 || pl.mp.alpha == 0) return cuda_rc(launch_scale_c(pl.mp, m, n, C, ldc, st));
     if (pl.fp64) return run_f64(pl, is_t(transA), is_t(transB), m, n, k, A, lda, B, ldb, C, ldc, ws, st);
+    if (pl.all_auto && small_path_ok(pl, m, n, k) && prefer_small(m, n, k))
+        return launch_gemm_small(pl, is_t(transA), is_t(transB), m, n, k, A, lda, B, ldb, C, ldc, st);
     int8_t* al = static_cast<int8_t*>(ws);
     int8_t* bl = al + align256(static_cast<size_t>(pl.info.L) * m * pl.info.k_pad);
     int8_t* scratch = bl + align256(static_cast<size_t>(pl.info.L) * n * pl.info.k_pad);

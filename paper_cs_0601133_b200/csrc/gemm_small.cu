@@ -1,0 +1,178 @@
+// gemm_small.cu -- fgemm for small fields (p < 2^16) on the warp-level tensor
+// cores (mma.sync m16n8k32 u8 x u8 -> s32), without encoders: the latency path
+// for short-K and small problems.
+//
+// Every residue x < p < 2^16 is split into two bytes, x = x0 + 256 x1, so that
+// one dot product of length K is
+//     sum_k a_k b_k = P00 + 256 (P01 + P10) + 65536 P11,   P_ij = sum_k a_ki b_kj,
+// four byte products, each exact in s32 while K 255^2 < 2^31 (K <= 32768), and
+// recombined exactly in 64 bits before one modular reduction -- the delayed
+// reduction of PAPER.md Eq. (1) with the whole K in one block.
+// The tcgen05 kernel (gemm_tc.cu) is the throughput path; this one has no
+// encode pass, no TMEM round trips between weight groups and a light epilogue,
+// which is what short-K products (LQUP / ftrsm updates, K = 128 .. 1024) and
+// small matrices are bound by.
+//
+// CTA: 256 threads (8 warps) own a 64 x 64 tile of C; warp w computes rows
+// 16 (w & 3) .. +16 and columns 32 (w >> 2) .. +32 (four m16n8 tiles).  K is
+// staged 32 at a time in shared memory as canonical u32 residues (any int32
+// input is reduced on load, reading R3); fragments are built from them with
+// byte permutes.  The next K slice is loaded into registers while the current
+// one is multiplied (register double buffering).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "internal.h"
+#include "modp.cuh"
+
+namespace ff {
+
+namespace {
+
+constexpr int kSM = 64, kSN = 64, kSK = 32;
+constexpr int kSThreads = 256;
+constexpr int kApitch = kSK + 4;   // u32; 16 B aligned rows
+constexpr int kBpitch = kSN + 4;
+
+struct SmallArgs {
+    ModP M;
+    unsigned long long mu64;       // floor(2^64 / p)
+    const int32_t* A;
+    const int32_t* B;
+    int32_t* C;
+    int64_t lda, ldb, ldc;
+    int32_t m, n, k;
+    int32_t tA, tB;                // 1: op(X) = X^T
+};
+
+__device__ __forceinline__ void imma(int (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                     uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+        : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// bytes 0 (lo) and 1 (hi) of four values < 2^16, in order
+__device__ __forceinline__ void split4(uint32_t x, uint32_t y, uint32_t z, uint32_t w, uint32_t& lo, uint32_t& hi) {
+    const uint32_t t0 = __byte_perm(x, y, 0x5140), t1 = __byte_perm(z, w, 0x5140);
+    lo = __byte_perm(t0, t1, 0x5410);
+    hi = __byte_perm(t0, t1, 0x7632);
+}
+
+__device__ __forceinline__ int32_t ld_a(const SmallArgs& a, int r, int kk) {   // op(A)[r][kk], 0 outside
+    if (r >= a.m || kk >= a.k) return 0;
+    return a.tA ? a.A[static_cast<int64_t>(kk) * a.lda + r] : a.A[static_cast<int64_t>(r) * a.lda + kk];
+}
+__device__ __forceinline__ int32_t ld_b(const SmallArgs& a, int kk, int c) {   // op(B)[kk][c], 0 outside
+    if (kk >= a.k || c >= a.n) return 0;
+    return a.tB ? a.B[static_cast<int64_t>(c) * a.ldb + kk] : a.B[static_cast<int64_t>(kk) * a.ldb + c];
+}
+
+__global__ void __launch_bounds__(kSThreads) small_gemm_kernel(const __grid_constant__ SmallArgs a) {
+    __shared__ __align__(16) uint32_t As[kSM][kApitch];
+    __shared__ __align__(16) uint32_t Bs[kSK][kBpitch];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+    const int wm = warp & 3, wn = warp >> 2;
+    const int m0 = blockIdx.y * kSM, n0 = blockIdx.x * kSN;
+    // staging: 2048 values per operand slice, 8 per thread, mapped so that the
+    // global reads are coalesced along the stored (fastest) dimension
+    int32_t ra[8], rb[8];
+    auto fetch = [&](int k0) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int e = tid + j * kSThreads;
+            if (a.tA) ra[j] = ld_a(a, m0 + e % kSM, k0 + e / kSM);      // A stored [k][m]: along m
+            else ra[j] = ld_a(a, m0 + e / kSK, k0 + e % kSK);           // A stored [m][k]: along k
+            if (a.tB) rb[j] = ld_b(a, k0 + e % kSK, n0 + e / kSK);      // B stored [n][k]: along k
+            else rb[j] = ld_b(a, k0 + e / kSN, n0 + e % kSN);           // B stored [k][n]: along n
+        }
+    };
+    auto stage = [&]() {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int e = tid + j * kSThreads;
+            const uint32_t va = residue_i32(ra[j], a.M), vb = residue_i32(rb[j], a.M);
+            if (a.tA) As[e % kSM][e / kSM] = va; else As[e / kSK][e % kSK] = va;
+            if (a.tB) Bs[e % kSK][e / kSK] = vb; else Bs[e / kSN][e % kSN] = vb;
+        }
+    };
+    int P[4][4][4];                     // [n-tile][byte product 00, 01, 10, 11][fragment]
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) P[i][j][e] = 0;
+    fetch(0);
+    for (int k0 = 0; k0 < a.k; k0 += kSK) {
+        __syncthreads();                // the previous slice is consumed
+        stage();
+        __syncthreads();
+        if (k0 + kSK < a.k) fetch(k0 + kSK);   // in flight during the products
+        uint32_t alo[4], ahi[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {   // a0: row g, a1: row g + 8; a2, a3: k + 16
+            const uint4 v = *reinterpret_cast<const uint4*>(&As[wm * 16 + g + ((q & 1) ? 8 : 0)][((q & 2) ? 16 : 0) + 4 * t]);
+            split4(v.x, v.y, v.z, v.w, alo[q], ahi[q]);
+        }
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+            const int c = wn * 32 + nt * 8 + g;
+            uint32_t blo[2], bhi[2];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int kk = (q ? 16 : 0) + 4 * t;
+                split4(Bs[kk][c], Bs[kk + 1][c], Bs[kk + 2][c], Bs[kk + 3][c], blo[q], bhi[q]);
+            }
+            imma(P[nt][0], alo[0], alo[1], alo[2], alo[3], blo[0], blo[1]);
+            imma(P[nt][1], alo[0], alo[1], alo[2], alo[3], bhi[0], bhi[1]);
+            imma(P[nt][2], ahi[0], ahi[1], ahi[2], ahi[3], blo[0], blo[1]);
+            imma(P[nt][3], ahi[0], ahi[1], ahi[2], ahi[3], bhi[0], bhi[1]);
+        }
+    }
+    // epilogue: R = P00 + 256 (P01 + P10) + 65536 P11 (exact, < 2^48), one
+    // reduction, then alpha R + beta C mod p
+    const uint32_t p = a.M.p;
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int r = m0 + wm * 16 + g + ((e & 2) ? 8 : 0);
+            const int c = n0 + wn * 32 + nt * 8 + 2 * t + (e & 1);
+            if (r >= a.m || c >= a.n) continue;
+            const unsigned long long S =
+                static_cast<unsigned long long>(static_cast<uint32_t>(P[nt][0][e])) +
+                (static_cast<unsigned long long>(static_cast<uint32_t>(P[nt][1][e]) + static_cast<uint32_t>(P[nt][2][e])) << 8) +
+                (static_cast<unsigned long long>(static_cast<uint32_t>(P[nt][3][e])) << 16);
+            uint32_t x = mulmod_shoup(residue_u64(S, a.mu64, p), a.M.alpha, a.M.alpha_sh, p);
+            int32_t* cp = a.C + static_cast<int64_t>(r) * a.ldc + c;
+            if (a.M.beta) x = addmod(x, mulmod_shoup(residue_i32(*cp, a.M), a.M.beta, a.M.beta_sh, p), p);
+            *cp = static_cast<int32_t>(x);
+        }
+}
+
+}  // namespace
+
+bool small_path_ok(const Plan& pl, int64_t m, int64_t n, int64_t k) {
+    return pl.mp.p < 65536u && k > 0 && k <= 32768 && m > 0 && n > 0 && m < (1ll << 30) && n < (1ll << 30);
+}
+
+int launch_gemm_small(const Plan& pl, bool tA, bool tB, int64_t m, int64_t n, int64_t k, const int32_t* A, int64_t lda,
+                      const int32_t* B, int64_t ldb, int32_t* C, int64_t ldc, cudaStream_t st) {
+    if (!small_path_ok(pl, m, n, k)) return FF_ERR_INTERNAL;
+    SmallArgs a;
+    a.M = pl.mp;
+    a.mu64 = static_cast<unsigned long long>((static_cast<unsigned __int128>(1) << 64) / pl.mp.p);
+    a.A = A; a.B = B; a.C = C;
+    a.lda = lda; a.ldb = ldb; a.ldc = ldc;
+    a.m = static_cast<int32_t>(m); a.n = static_cast<int32_t>(n); a.k = static_cast<int32_t>(k);
+    a.tA = tA ? 1 : 0; a.tB = tB ? 1 : 0;
+    const dim3 grid(static_cast<unsigned>((n + kSN - 1) / kSN), static_cast<unsigned>((m + kSM - 1) / kSM));
+    if (grid.y > 65535u) return FF_ERR_INTERNAL;
+    small_gemm_kernel<<<grid, kSThreads, 0, st>>>(a);
+    return cudaGetLastError() == cudaSuccess ? 0 : FF_ERR_CUDA;
+}
+
+}  // namespace ff

@@ -70,6 +70,7 @@ struct Plan {
     bool korder_auto;                // k-outer chosen by default (no option, no kb_override):
                                      // the launch may fall back to group-outer for L2-sized operands
     uint32_t kinv, kinv_sh;          // 256^-(G-1) mod p and its Shoup constant (k-outer carry)
+    bool all_auto;                   // no option forced: the planner may route to the small-field path
 };
 
 constexpr int64_t kKbLocalityBytes = 8192;  // L * kb per row-slice in k-outer order (swept on c4, c5)
@@ -86,6 +87,11 @@ cudaError_t launch_encode(const Plan& pl, int kmajor_src, int64_t rows, int64_t 
 size_t crt_scratch_bytes(const Plan& pl);
 cudaError_t launch_scale_c(const ModP& mp, int64_t m, int64_t n, int32_t* C, int64_t ldc,
                            cudaStream_t st);
+
+// gemm_small.cu: p < 2^16 on warp-level tensor cores, no encoders (latency path)
+bool small_path_ok(const Plan& pl, int64_t m, int64_t n, int64_t k);
+int launch_gemm_small(const Plan& pl, bool tA, bool tB, int64_t m, int64_t n, int64_t k, const int32_t* A, int64_t lda,
+                      const int32_t* B, int64_t ldb, int32_t* C, int64_t ldc, cudaStream_t st);
 
 // gemm_tc.cu
 struct OutSpec {          // C <- (a * A B + b * C) mod p for one output block
