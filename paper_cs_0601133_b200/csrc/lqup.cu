@@ -1121,6 +1121,9 @@ int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t* A, int64_t lda, int64_
         }
         if (hout[1]) {                       // a row without pivot in the window: widen and redo
             W = std::min<int64_t>(n, 4 * Wc);
+            // the wider window reaches columns whose update was queued after the
+            // release of this panel: wait for all of it
+            if (cudaEventRecord(ev_ready, st) != cudaSuccess) return fail_cuda();
             continue;
         }
         buf ^= 1;
@@ -1161,39 +1164,40 @@ int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t* A, int64_t lda, int64_
             npend = 0;
         }
         if (generic) {
-            if (c + Wc < n) {                        // U_rest = L11^-1 A_rest (rows up to date)
-                int32_t* Ar = A + i0 * lda + c + Wc;
-                if ((e = gemm_plain(p, opts, 'N', 'N', kk, n - c - Wc, kk, 1, Linv, kH, Ar, lda, 0, Ar, lda, gws, st)))
-                    return e;
-            }
-            if (tl) cudaEventRecord(tl_ev.back()[4], st);
-            // G = X U11^-1 (window columns up to date): the next panel's rows now, the
-            // rows below it once that panel kernel has been released
-            auto gmul = [&](int64_t ra, int64_t rb) -> int {
+            // The next panel kernel needs only its own 128 x 128 window up to date, so the
+            // chain that releases it is three 128-column products (U_rest's first window,
+            // G of the next panel's rows, the window's update); everything wider runs
+            // while that panel kernel does.
+            const int64_t r1 = i0 + kH, c1 = c + kH, rn = std::min<int64_t>(m_active, r1 + kH);
+            const int64_t cw = std::min<int64_t>(n, c1 + kH);                     // end of the next window
+            auto urest = [&](int64_t ca, int64_t cb) -> int {                     // U_rest = L11^-1 A_rest
+                if (cb <= ca) return 0;
+                int32_t* Ar = A + i0 * lda + ca;
+                return gemm_plain(p, opts, 'N', 'N', kk, cb - ca, kk, 1, Linv, kH, Ar, lda, 0, Ar, lda, gws, st);
+            };
+            auto gmul = [&](int64_t ra, int64_t rb) -> int {                      // G = X U11^-1
                 rb = std::min<int64_t>(rb, m_active);
                 if (rb <= ra) return 0;
                 int32_t* X = A + ra * lda + c;
                 return gemm_plain(p, opts, 'N', 'N', rb - ra, kk, kk, 1, X, lda, Uinv, kH, 0, X, lda, gws, st);
             };
+            if ((e = urest(c1, cw))) return e;
+            if (tl) cudaEventRecord(tl_ev.back()[4], st);
             if (npend == 0) { pi0 = i0; pc0 = c; }
             ++npend;
-            const int64_t r1 = i0 + kH, c1 = c + kH, K = c1 - pc0, rn = std::min<int64_t>(m_active, r1 + kH);
+            const int64_t K = c1 - pc0;
             if ((e = gmul(r1, rn))) return e;
             if (tl) cudaEventRecord(tl_ev.back()[5], st);
+            if ((e = upd(r1, rn, c1, cw, K, 0))) return e;                      // the next window
+            if (cudaEventRecord(ev_ready, st) != cudaSuccess) return fail_cuda();
+            if ((e = urest(cw, n))) return e;
+            if ((e = upd(r1, rn, cw, n, K, 0))) return e;                        // the rest of its rows
+            if ((e = gmul(rn, m_active))) return e;
             if (npend == group || r1 + kH >= m_active || c1 + kH >= n) {
-                // flush: the next panel's rows first (they release its panel kernel), then the rest
-                if ((e = upd(r1, rn, c1, n, K, 0))) return e;
-                if (cudaEventRecord(ev_ready, st) != cudaSuccess) return fail_cuda();
-                if ((e = gmul(rn, m_active))) return e;
-                if ((e = upd(rn, m_active, c1, n, K, kReserve))) return e;
+                if ((e = upd(rn, m_active, c1, n, K, kReserve))) return e;      // flush the group
                 npend = 0;
-            } else {
-                // lookahead: the next panel's rows (all columns), then the next window's
-                // columns of the rows below it
-                if ((e = upd(r1, rn, c1, n, K, 0))) return e;
-                if (cudaEventRecord(ev_ready, st) != cudaSuccess) return fail_cuda();
-                if ((e = gmul(rn, m_active))) return e;
-                if ((e = upd(rn, m_active, c1, c1 + kH, K, 0))) return e;
+            } else if ((e = upd(rn, m_active, c1, cw, K, 0))) {                 // the next window's columns below
+                return e;
             }
             ready_recorded = true;
         } else if (kk > 0) {
