@@ -127,8 +127,7 @@ __global__ void __launch_bounds__(kThr) panel_kernel(PanelArgs P) {
     // copy in (canonical residues)
     for (int64_t r = ty; r < hr; r += 32)
         for (int64_t cc = tx; cc < W; cc += 32) {
-            const int64_t v = static_cast<int64_t>(P.A[(P.i0 + r) * P.lda + P.c + cc]) % static_cast<int64_t>(p);
-            w[r * W + cc] = static_cast<uint32_t>(v < 0 ? v + p : v);
+            w[r * W + cc] = residue_i32_64(P.A[(P.i0 + r) * P.lda + P.c + cc], P.mu64, p);
         }
     // E = I (kH x kH): the same row operations turn it into S L^-1 (see below)
     for (int e = tid; e < kH * kH; e += kThr) E[e] = ((e / kH) == (e % kH)) ? 1u : 0u;
@@ -316,8 +315,7 @@ __global__ void __launch_bounds__(kThr) panel2_kernel(PanelArgs P) {
         const int r = e / kHalf, cl = e % kHalf;
         uint32_t v = 0;
         if (r < hr) {
-            const int64_t x = static_cast<int64_t>(P.A[(P.i0 + r) * P.lda + P.c + c0 + cl]) % static_cast<int64_t>(p);
-            v = static_cast<uint32_t>(x < 0 ? x + p : x);
+            v = residue_i32_64(P.A[(P.i0 + r) * P.lda + P.c + c0 + cl], P.mu64, p);
         }
         w[e] = v;
         E[e] = (r == c0 + cl) ? 1u : 0u;

@@ -92,6 +92,13 @@ __device__ __forceinline__ uint32_t residue_u64(unsigned long long x, unsigned l
     return static_cast<uint32_t>(r >= p ? r - p : r);
 }
 
+// Any int32 -> its Euclidean residue in [0, p), with mu64 = floor(2^64 / p):
+// x + p 2^31 > 0 and < 2^62, one Barrett step.
+__device__ __forceinline__ uint32_t residue_i32_64(int32_t x, unsigned long long mu64, uint32_t p) {
+    return residue_u64(static_cast<unsigned long long>(static_cast<long long>(x) + (static_cast<long long>(p) << 31)),
+                       mu64, p);
+}
+
 __device__ __forceinline__ uint32_t addmod(uint32_t a, uint32_t b, uint32_t p) {
     const uint32_t s = a + b;  // < 2p < 2^32
     return s >= p ? s - p : s;

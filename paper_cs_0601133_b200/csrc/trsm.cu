@@ -78,8 +78,7 @@ __global__ void __launch_bounds__(kInvThreads) trsm_diag_inv_kernel(InvArgs a) {
         if (i < db && j < db) {
             const bool inside = a.upper ? (j >= i) : (j <= i);
             if (inside) {
-                const int64_t x = static_cast<int64_t>(a.A[(r0 + i) * a.lda + r0 + j]) % static_cast<int64_t>(p);
-                v = static_cast<uint32_t>(x < 0 ? x + p : x);
+                v = residue_i32_64(a.A[(r0 + i) * a.lda + r0 + j], a.mu64, p);
             }
         }
         D[e] = v;
@@ -138,14 +137,14 @@ struct MatDesc {
     int64_t row0_step;   // absolute row offset of batch b = b * row0_step (for the limits)
     int64_t col0_step;
     int32_t reduce;      // 1: reduce raw int32 mod p on load
+    unsigned long long mu64;   // floor(2^64 / p) (for reduce)
 };
 
 __device__ __forceinline__ uint32_t load_md(const MatDesc& d, int64_t b, int64_t i, int64_t j, uint32_t p) {
     if (b * d.row0_step + i >= d.rows_lim || b * d.col0_step + j >= d.cols_lim) return 0u;
     const int32_t x = d.ptr[b * d.bstride + i * d.ld + j];
     if (!d.reduce) return static_cast<uint32_t>(x);
-    const int64_t r = static_cast<int64_t>(x) % static_cast<int64_t>(p);
-    return static_cast<uint32_t>(r < 0 ? r + p : r);
+    return residue_i32_64(x, d.mu64, p);
 }
 
 // C[b] = (neg ? -1 : 1) * X[b] Y[b] mod p, all n x n (zero outside the limits);
@@ -181,6 +180,70 @@ __global__ void __launch_bounds__(256) batched_modmul_kernel(MatDesc X, MatDesc 
         const int i = i0 + ty + 8 * q, j = j0 + tx;
         if (i < n && j < n) {
             const uint32_t v = static_cast<uint32_t>(acc[q]);
+            C[b * c_bstride + static_cast<int64_t>(i) * ldc + j] = static_cast<int32_t>(neg && v ? p - v : v);
+        }
+    }
+}
+
+// The same on the warp-level tensor cores for p < 2^16 (as gemm_small.cu):
+// residues split into two bytes, four mma.sync m16n8k32 u8 products per 32-wide
+// k slice, recombined exactly in 64 bits (n <= kLeaf: each byte product stays
+// below n 255^2 < 2^31) and reduced once.  8 warps, one m16n8 tile each.
+__device__ __forceinline__ void imma_t(int (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                       uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+        : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void split4_t(uint32_t x, uint32_t y, uint32_t z, uint32_t w, uint32_t& lo, uint32_t& hi) {
+    const uint32_t t0 = __byte_perm(x, y, 0x5140), t1 = __byte_perm(z, w, 0x5140);
+    lo = __byte_perm(t0, t1, 0x5410);
+    hi = __byte_perm(t0, t1, 0x7632);
+}
+__global__ void __launch_bounds__(256) batched_modmul_tc_kernel(MatDesc X, MatDesc Y, int32_t* C, int64_t c_bstride,
+                                                                int64_t ldc, int n, int neg, uint32_t p,
+                                                                unsigned long long mu64) {
+    __shared__ uint32_t xs[32][36], ys[32][40];
+    const int64_t b = blockIdx.z;
+    const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
+    const int warp = ty, g = tx >> 2, t = tx & 3;
+    const int wm = warp & 1, wn = warp >> 1;                 // 2 x 4 tiles of 16 x 8
+    const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
+    int P[4][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}, {0, 0, 0, 0}, {0, 0, 0, 0}};
+    for (int k0 = 0; k0 < n; k0 += 32) {
+        for (int r = ty; r < 32; r += 8) {
+            xs[r][tx] = (i0 + r < n && k0 + tx < n) ? load_md(X, b, i0 + r, k0 + tx, p) : 0u;
+            ys[r][tx] = (k0 + r < n && j0 + tx < n) ? load_md(Y, b, k0 + r, j0 + tx, p) : 0u;
+        }
+        __syncthreads();
+        uint32_t alo[4], ahi[4], blo[2], bhi[2];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int r = wm * 16 + g + ((q & 1) ? 8 : 0), k = ((q & 2) ? 16 : 0) + 4 * t;
+            const uint4 v = *reinterpret_cast<const uint4*>(&xs[r][k]);
+            split4_t(v.x, v.y, v.z, v.w, alo[q], ahi[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int k = (q ? 16 : 0) + 4 * t, c = wn * 8 + g;
+            split4_t(ys[k][c], ys[k + 1][c], ys[k + 2][c], ys[k + 3][c], blo[q], bhi[q]);
+        }
+        imma_t(P[0], alo[0], alo[1], alo[2], alo[3], blo[0], blo[1]);
+        imma_t(P[1], alo[0], alo[1], alo[2], alo[3], bhi[0], bhi[1]);
+        imma_t(P[2], ahi[0], ahi[1], ahi[2], ahi[3], blo[0], blo[1]);
+        imma_t(P[3], ahi[0], ahi[1], ahi[2], ahi[3], bhi[0], bhi[1]);
+        __syncthreads();
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const int i = i0 + wm * 16 + g + ((e & 2) ? 8 : 0), j = j0 + wn * 8 + 2 * t + (e & 1);
+        if (i < n && j < n) {
+            const unsigned long long S =
+                static_cast<unsigned long long>(static_cast<uint32_t>(P[0][e])) +
+                (static_cast<unsigned long long>(static_cast<uint32_t>(P[1][e]) + static_cast<uint32_t>(P[2][e])) << 8) +
+                (static_cast<unsigned long long>(static_cast<uint32_t>(P[3][e])) << 16);
+            const uint32_t v = residue_u64(S, mu64, p);
             C[b * c_bstride + static_cast<int64_t>(i) * ldc + j] = static_cast<int32_t>(neg && v ? p - v : v);
         }
     }
@@ -444,19 +507,24 @@ int ff_trsm_ex(uint32_t p, char side, char uplo, char transA, char diag, int64_t
         int32_t* Ws = reinterpret_cast<int32_t*>(ws + w.lvl_off[l]);
         assemble_kernel<<<dim3(64, static_cast<unsigned>(nb_s)), 256, 0, st>>>(Wh, nb_h, Ws, sz, upper ? 1 : 0);
         const int64_t big = INT64_MAX / 4;
-        MatDesc W1 = {Wh, 2LL * h * h, h, big, big, 0, 0, 0};
-        MatDesc W3 = {Wh + static_cast<int64_t>(h) * h, 2LL * h * h, h, (nb_h - 1) * h, big, sz, 0, 0};
-        MatDesc Tm = {T, static_cast<int64_t>(h) * h, h, big, big, 0, 0, 0};
+        MatDesc W1 = {Wh, 2LL * h * h, h, big, big, 0, 0, 0, ia.mu64};
+        MatDesc W3 = {Wh + static_cast<int64_t>(h) * h, 2LL * h * h, h, (nb_h - 1) * h, big, sz, 0, 0, ia.mu64};
+        MatDesc Tm = {T, static_cast<int64_t>(h) * h, h, big, big, 0, 0, 0, ia.mu64};
         const dim3 g(h / 32, h / 32, static_cast<unsigned>(nb_s));
+        auto modmul = [&](dim3 gg, cudaStream_t ss, MatDesc X, MatDesc Y, int32_t* Cc, int64_t cb, int64_t ldcc,
+                          int nn, int ng, uint32_t pp, unsigned long long mu) {
+            if (pp < 65536u) batched_modmul_tc_kernel<<<gg, 256, 0, ss>>>(X, Y, Cc, cb, ldcc, nn, ng, pp, mu);
+            else batched_modmul_kernel<<<gg, 256, 0, ss>>>(X, Y, Cc, cb, ldcc, nn, ng, pp, mu);
+        };
         if (upper) {
-            MatDesc A12 = {A + h, sz * lda + sz, lda, d, d - h, sz, sz, 1};      // A[r0 + i][r0 + h + j]
-            batched_modmul_kernel<<<g, 256, 0, st>>>(W1, A12, T, static_cast<int64_t>(h) * h, h, h, 0, p, ia.mu64);
-            batched_modmul_kernel<<<g, 256, 0, st>>>(Tm, W3, Ws + h, static_cast<int64_t>(sz) * sz, sz, h, 1, p,
+            MatDesc A12 = {A + h, sz * lda + sz, lda, d, d - h, sz, sz, 1, ia.mu64};      // A[r0 + i][r0 + h + j]
+            modmul(g, st, W1, A12, T, static_cast<int64_t>(h) * h, h, h, 0, p, ia.mu64);
+            modmul(g, st, Tm, W3, Ws + h, static_cast<int64_t>(sz) * sz, sz, h, 1, p,
                                                      ia.mu64);
         } else {
-            MatDesc A21 = {A + h * lda, sz * lda + sz, lda, d - h, d, sz, sz, 1};  // A[r0 + h + i][r0 + j]
-            batched_modmul_kernel<<<g, 256, 0, st>>>(A21, W1, T, static_cast<int64_t>(h) * h, h, h, 0, p, ia.mu64);
-            batched_modmul_kernel<<<g, 256, 0, st>>>(W3, Tm, Ws + static_cast<int64_t>(h) * sz,
+            MatDesc A21 = {A + h * lda, sz * lda + sz, lda, d - h, d, sz, sz, 1, ia.mu64};  // A[r0 + h + i][r0 + j]
+            modmul(g, st, A21, W1, T, static_cast<int64_t>(h) * h, h, h, 0, p, ia.mu64);
+            modmul(g, st, W3, Tm, Ws + static_cast<int64_t>(h) * sz,
                                                      static_cast<int64_t>(sz) * sz, sz, h, 1, p, ia.mu64);
         }
         if (cudaGetLastError() != cudaSuccess) return FF_ERR_CUDA;
