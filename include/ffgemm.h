@@ -101,7 +101,11 @@ typedef struct ff_opts {
     int32_t debug_unchecked_kb; /* test builds only: accept a kb_override above the safe
                                bound (to show that the bound is needed); results are then
                                not guaranteed */
-    int32_t reserved[3];
+    int32_t inputs_canonical; /* 1: the caller guarantees every element of op(A), op(B) is a
+                               canonical residue in [0, p) (C may still be any int32): for
+                               p < 2^16 short-K products may then stream A and B raw
+                               (DESIGN.md §4.10).  Results are undefined if violated. */
+    int32_t reserved[2];
 } ff_opts;
 
 /* The plan the library derives from (p, k, opts): host-only, no GPU needed. */

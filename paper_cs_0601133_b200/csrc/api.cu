@@ -155,10 +155,24 @@ bool prefer_small(int64_t m, int64_t n, int64_t k) {
     return k <= 256 && m * n <= (int64_t{1} << 21);
 }
 
+// The cp.async variant for canonical operands (internal callers): FF_SMALL as above.
+bool prefer_small_canon(int64_t m, int64_t n, int64_t k) {
+    const char* env = getenv("FF_SMALL");
+    const int mode = env ? atoi(env) : -1;
+    if (mode >= 0) return mode > 0;
+    // measured against the tcgen05 path (p = 65521, alpha = -1, beta = 1): 512^3 21 vs
+    // 36 us, 128 x 8192 x 128 20 vs 33 us, 128 x 8192 x 1024 51 vs 51 us, 1024^3
+    // 51 vs 41 us, 4096^2 x 128 146 vs 90 us
+    return k <= 1024 && m * n <= (int64_t{1} << 21) && m * n * k < (int64_t{1} << 30);
+}
+
 int run(const Plan& pl, char transA, char transB, int64_t m, int64_t n, int64_t k, const int32_t* A,
         int64_t lda, const int32_t* B, int64_t ldb, int32_t* C, int64_t ldc, void* ws, cudaStream_t st) {
     if (k == 0 || pl.mp.alpha == 0) return cuda_rc(launch_scale_c(pl.mp, m, n, C, ldc, st));
     if (pl.fp64) return run_f64(pl, is_t(transA), is_t(transB), m, n, k, A, lda, B, ldb, C, ldc, ws, st);
+    if (pl.all_auto && small_canon_ok(pl, is_t(transA), is_t(transB), m, n, k, A, lda, B, ldb) &&
+        prefer_small_canon(m, n, k))
+        return launch_gemm_small_canon(pl, m, n, k, A, lda, B, ldb, C, ldc, st);
     if (pl.all_auto && small_path_ok(pl, m, n, k) && prefer_small(m, n, k))
         return launch_gemm_small(pl, is_t(transA), is_t(transB), m, n, k, A, lda, B, ldb, C, ldc, st);
     int8_t* al = static_cast<int8_t*>(ws);

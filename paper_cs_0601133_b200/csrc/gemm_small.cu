@@ -153,7 +153,137 @@ __global__ void __launch_bounds__(kSThreads) small_gemm_kernel(const __grid_cons
         }
 }
 
+// Variant for internal callers whose A and B are canonical residues (LQUP's
+// panel chain: outputs of earlier products), both not transposed, rows 16 B
+// aligned: the slices are copied raw with cp.async into a 4-deep ring, so the
+// whole K streams with several slices in flight (the register-staged kernel
+// above waits one load latency per slice).
+constexpr int kCStages = 4;
+constexpr int kCApitch = kSK + 4, kCBpitch = kSN + 4;
+constexpr int kCSmem = kCStages * (kSM * kCApitch + kSK * kCBpitch) * 4;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int bytes) {
+    const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(bytes) : "memory");
+}
+
+__global__ void __launch_bounds__(kSThreads) small_gemm_canon_kernel(const __grid_constant__ SmallArgs a) {
+    extern __shared__ __align__(16) uint32_t csm[];
+    uint32_t* As = csm;                                  // [kCStages][kSM][kCApitch]
+    uint32_t* Bs = csm + kCStages * kSM * kCApitch;      // [kCStages][kSK][kCBpitch]
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+    const int wm = warp & 3, wn = warp >> 2;
+    const int m0 = blockIdx.y * kSM, n0 = blockIdx.x * kSN;
+    const int nsl = (a.k + kSK - 1) / kSK;
+    auto issue = [&](int sl) {
+        if (sl < nsl) {
+            const int st = sl % kCStages, k0 = sl * kSK;
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {                // A: 64 rows x 8 chunks of 4
+                const int e = tid + j * kSThreads, r = e >> 3, kc = (e & 7) * 4;
+                const int row = m0 + r, kk = k0 + kc;
+                const int nb = (row < a.m && kk < a.k) ? 4 * min(4, a.k - kk) : 0;
+                const int32_t* src = nb ? a.A + static_cast<int64_t>(row) * a.lda + kk : a.A;
+                cp_async16(As + (st * kSM + r) * kCApitch + kc, src, nb);
+            }
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {                // B: 32 rows x 16 chunks of 4
+                const int e = tid + j * kSThreads, r = e >> 4, cc = (e & 15) * 4;
+                const int kk = k0 + r, col = n0 + cc;
+                const int nb = (kk < a.k && col < a.n) ? 4 * min(4, a.n - col) : 0;
+                const int32_t* src = nb ? a.B + static_cast<int64_t>(kk) * a.ldb + col : a.B;
+                cp_async16(Bs + (st * kSK + r) * kCBpitch + cc, src, nb);
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    int P[4][4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) P[i][j][e] = 0;
+    for (int s = 0; s < kCStages - 1; ++s) issue(s);
+    for (int sl = 0; sl < nsl; ++sl) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(kCStages - 2) : "memory");
+        __syncthreads();                                 // slice sl visible; slice sl-1's stage is free
+        issue(sl + kCStages - 1);
+        const uint32_t* A_ = As + (sl % kCStages) * kSM * kCApitch;
+        const uint32_t* B_ = Bs + (sl % kCStages) * kSK * kCBpitch;
+        uint32_t alo[4], ahi[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint4 v = *reinterpret_cast<const uint4*>(A_ + (wm * 16 + g + ((q & 1) ? 8 : 0)) * kCApitch +
+                                                            ((q & 2) ? 16 : 0) + 4 * t);
+            split4(v.x, v.y, v.z, v.w, alo[q], ahi[q]);
+        }
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+            const int c = wn * 32 + nt * 8 + g;
+            uint32_t blo[2], bhi[2];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int kk = (q ? 16 : 0) + 4 * t;
+                split4(B_[kk * kCBpitch + c], B_[(kk + 1) * kCBpitch + c], B_[(kk + 2) * kCBpitch + c],
+                       B_[(kk + 3) * kCBpitch + c], blo[q], bhi[q]);
+            }
+            imma(P[nt][0], alo[0], alo[1], alo[2], alo[3], blo[0], blo[1]);
+            imma(P[nt][1], alo[0], alo[1], alo[2], alo[3], bhi[0], bhi[1]);
+            imma(P[nt][2], ahi[0], ahi[1], ahi[2], ahi[3], blo[0], blo[1]);
+            imma(P[nt][3], ahi[0], ahi[1], ahi[2], ahi[3], bhi[0], bhi[1]);
+        }
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    const uint32_t p = a.M.p;
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int r = m0 + wm * 16 + g + ((e & 2) ? 8 : 0);
+            const int c = n0 + wn * 32 + nt * 8 + 2 * t + (e & 1);
+            if (r >= a.m || c >= a.n) continue;
+            const unsigned long long S =
+                static_cast<unsigned long long>(static_cast<uint32_t>(P[nt][0][e])) +
+                (static_cast<unsigned long long>(static_cast<uint32_t>(P[nt][1][e]) + static_cast<uint32_t>(P[nt][2][e])) << 8) +
+                (static_cast<unsigned long long>(static_cast<uint32_t>(P[nt][3][e])) << 16);
+            uint32_t x = mulmod_shoup(residue_u64(S, a.mu64, p), a.M.alpha, a.M.alpha_sh, p);
+            int32_t* cp = a.C + static_cast<int64_t>(r) * a.ldc + c;
+            if (a.M.beta) x = addmod(x, mulmod_shoup(residue_i32(*cp, a.M), a.M.beta, a.M.beta_sh, p), p);
+            *cp = static_cast<int32_t>(x);
+        }
+}
+
 }  // namespace
+
+bool small_canon_ok(const Plan& pl, bool tA, bool tB, int64_t m, int64_t n, int64_t k, const int32_t* A, int64_t lda,
+                    const int32_t* B, int64_t ldb) {
+    return pl.canonical_ab && !tA && !tB && pl.mp.p < 65536u && k > 0 && k <= 32768 && m > 0 && n > 0 &&
+           m < (1ll << 30) && n < (1ll << 30) && (lda % 4) == 0 && (ldb % 4) == 0 &&
+           (reinterpret_cast<uintptr_t>(A) & 15) == 0 && (reinterpret_cast<uintptr_t>(B) & 15) == 0;
+}
+
+int launch_gemm_small_canon(const Plan& pl, int64_t m, int64_t n, int64_t k, const int32_t* A, int64_t lda,
+                            const int32_t* B, int64_t ldb, int32_t* C, int64_t ldc, cudaStream_t st) {
+    SmallArgs a;
+    a.M = pl.mp;
+    a.mu64 = static_cast<unsigned long long>((static_cast<unsigned __int128>(1) << 64) / pl.mp.p);
+    a.A = A; a.B = B; a.C = C;
+    a.lda = lda; a.ldb = ldb; a.ldc = ldc;
+    a.m = static_cast<int32_t>(m); a.n = static_cast<int32_t>(n); a.k = static_cast<int32_t>(k);
+    a.tA = 0; a.tB = 0;
+    const dim3 grid(static_cast<unsigned>((n + kSN - 1) / kSN), static_cast<unsigned>((m + kSM - 1) / kSM));
+    if (grid.y > 65535u) return FF_ERR_INTERNAL;
+    static bool attr = false;
+    if (!attr) {
+        if (cudaFuncSetAttribute(small_gemm_canon_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kCSmem) !=
+            cudaSuccess)
+            return FF_ERR_CUDA;
+        attr = true;
+    }
+    small_gemm_canon_kernel<<<grid, kSThreads, kCSmem, st>>>(a);
+    return cudaGetLastError() == cudaSuccess ? 0 : FF_ERR_CUDA;
+}
 
 bool small_path_ok(const Plan& pl, int64_t m, int64_t n, int64_t k) {
     return pl.mp.p < 65536u && k > 0 && k <= 32768 && m > 0 && n > 0 && m < (1ll << 30) && n < (1ll << 30);

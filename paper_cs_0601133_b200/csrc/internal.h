@@ -71,6 +71,7 @@ struct Plan {
                                      // the launch may fall back to group-outer for L2-sized operands
     uint32_t kinv, kinv_sh;          // 256^-(G-1) mod p and its Shoup constant (k-outer carry)
     bool all_auto;                   // no option forced: the planner may route to the small-field path
+    bool canonical_ab;               // (internal callers) A, B hold canonical residues in [0, p)
 };
 
 constexpr int64_t kKbLocalityBytes = 8192;  // L * kb per row-slice in k-outer order (swept on c4, c5)
@@ -92,6 +93,11 @@ cudaError_t launch_scale_c(const ModP& mp, int64_t m, int64_t n, int32_t* C, int
 bool small_path_ok(const Plan& pl, int64_t m, int64_t n, int64_t k);
 int launch_gemm_small(const Plan& pl, bool tA, bool tB, int64_t m, int64_t n, int64_t k, const int32_t* A, int64_t lda,
                       const int32_t* B, int64_t ldb, int32_t* C, int64_t ldc, cudaStream_t st);
+
+bool small_canon_ok(const Plan& pl, bool tA, bool tB, int64_t m, int64_t n, int64_t k, const int32_t* A, int64_t lda,
+                    const int32_t* B, int64_t ldb);
+int launch_gemm_small_canon(const Plan& pl, int64_t m, int64_t n, int64_t k, const int32_t* A, int64_t lda,
+                            const int32_t* B, int64_t ldb, int32_t* C, int64_t ldc, cudaStream_t st);
 
 // gemm_tc.cu
 struct OutSpec {          // C <- (a * A B + b * C) mod p for one output block

@@ -869,7 +869,7 @@ __global__ void zero_kernel(int32_t* A, int64_t lda, int64_t r0, int64_t r1, int
 
 int gemm_plain(uint32_t p, const ff_opts* opts, char tX, char tY, int64_t m, int64_t n, int64_t k, uint32_t alpha,
                const int32_t* X, int64_t ldx, const int32_t* Y, int64_t ldy, uint32_t beta, int32_t* C, int64_t ldc,
-               void* ws, cudaStream_t st, int reserve_sms = 0) {
+               void* ws, cudaStream_t st, int reserve_sms = 0, bool canon = false) {
     if (m == 0 || n == 0) return 0;
     static const bool host_t = getenv("FF_LQUP_HOSTTIME") != nullptr;   // development aid
     const auto h0 = std::chrono::steady_clock::now();
@@ -878,6 +878,7 @@ int gemm_plain(uint32_t p, const ff_opts* opts, char tX, char tY, int64_t m, int
     if (e) return e;
     set_scalars(&pl, alpha, beta);
     pl.reserve_sms = reserve_sms;
+    pl.canonical_ab = canon;         // the caller guarantees X, Y canonical (products of earlier steps)
     const auto h1 = std::chrono::steady_clock::now();
     e = gemm_dev(pl, tX, tY, m, n, k, X, ldx, Y, ldy, C, ldc, ws, st);
     if (host_t) {
@@ -1053,7 +1054,7 @@ int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t* A, int64_t lda, int64_
         cb = std::min<int64_t>(cb, n);
         if (rb <= ra || cb <= ca || K <= 0) return 0;
         return gemm_plain(p, opts, 'N', 'N', rb - ra, cb - ca, K, neg1, A + ra * lda + pc0, lda, A + pi0 * lda + ca, lda,
-                          1, A + ra * lda + ca, lda, gws, st, reserve);
+                          1, A + ra * lda + ca, lda, gws, st, reserve, true);   // L and U entries: canonical
     };
     while (i0 < m_active && c < n) {
         int32_t* Linv = Linv2 + static_cast<size_t>(buf) * kH * kH;
@@ -1170,14 +1171,14 @@ int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t* A, int64_t lda, int64_
             const int64_t cw = std::min<int64_t>(n, c1 + kH);                     // end of the next window
             auto urest = [&](int64_t ca, int64_t cb) -> int {                     // U_rest = L11^-1 A_rest
                 if (cb <= ca) return 0;
-                int32_t* Ar = A + i0 * lda + ca;
-                return gemm_plain(p, opts, 'N', 'N', kk, cb - ca, kk, 1, Linv, kH, Ar, lda, 0, Ar, lda, gws, st);
+                int32_t* Ar = A + i0 * lda + ca;    // (canonical once an earlier panel has updated these rows)
+                return gemm_plain(p, opts, 'N', 'N', kk, cb - ca, kk, 1, Linv, kH, Ar, lda, 0, Ar, lda, gws, st, 0, i0 > 0);
             };
             auto gmul = [&](int64_t ra, int64_t rb) -> int {                      // G = X U11^-1
                 rb = std::min<int64_t>(rb, m_active);
                 if (rb <= ra) return 0;
                 int32_t* X = A + ra * lda + c;
-                return gemm_plain(p, opts, 'N', 'N', rb - ra, kk, kk, 1, X, lda, Uinv, kH, 0, X, lda, gws, st);
+                return gemm_plain(p, opts, 'N', 'N', rb - ra, kk, kk, 1, X, lda, Uinv, kH, 0, X, lda, gws, st, 0, i0 > 0);
             };
             if ((e = urest(c1, cw))) return e;
             if (tl) cudaEventRecord(tl_ev.back()[4], st);

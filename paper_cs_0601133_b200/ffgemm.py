@@ -32,7 +32,8 @@ _p, _ch, _sz = ctypes.c_void_p, ctypes.c_char, ctypes.c_size_t
 class ff_opts(ctypes.Structure):
     _fields_ = [("winograd", _i32), ("scheme", _i32), ("kb_override", _i64),
                 ("debug_saturate", _i32), ("cta_group", _i32), ("host_block", _i32),
-                ("korder", _i32), ("debug_unchecked_kb", _i32), ("reserved", _i32 * 3)]
+                ("korder", _i32), ("debug_unchecked_kb", _i32), ("inputs_canonical", _i32),
+                ("reserved", _i32 * 2)]
 
 
 class ff_plan_info(ctypes.Structure):

@@ -63,3 +63,34 @@ def test_small_path_k_at_the_s32_bound(env, monkeypatch):
     ff.ff_gemm_ex(p, "N", "N", m, n, k, 1, dA, k, dB, n, 0, dC, n)
     torch.cuda.synchronize()
     np.testing.assert_array_equal(dC.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("p", [2, 251, 65521])
+def test_small_path_canonical_inputs(env, p, monkeypatch):
+    """inputs_canonical = 1 (A, B already in [0, p)): the cp.async variant
+    streams them raw; ragged K and n exercise its partial (zero-filled) 16-byte
+    chunks, transposed operands fall back to the reducing kernel.  C stays any
+    int32.  Bit-exact vs the oracle, forced on and under the default rule."""
+    torch, ff = env
+    rng = np.random.default_rng(p * 3 + 1)
+    for (m, n, k, tA, tB) in [(5, 3, 7, "N", "N"), (64, 64, 32, "N", "N"), (65, 63, 33, "N", "N"),
+                              (128, 301, 130, "N", "N"), (200, 70, 1000, "N", "N"), (17, 129, 4101, "N", "N"),
+                              (128, 128, 1024, "N", "N"), (40, 50, 60, "T", "N"), (40, 50, 60, "N", "T")]:
+        ar, ac = (m, k) if tA == "N" else (k, m)
+        br, bc = (k, n) if tB == "N" else (n, k)
+        la, lb = (ac + 3) // 4 * 4 + 4, (bc + 3) // 4 * 4     # leading dimensions: multiples of 4
+        A = rng.integers(0, p, size=(ar, la), dtype=np.int64).astype(np.int32)
+        B = rng.integers(0, p, size=(br, lb), dtype=np.int64).astype(np.int32)
+        C = rng.integers(-2 ** 31, 2 ** 31, size=(m, n), dtype=np.int64).astype(np.int32)
+        alpha, beta = p - 1, 1
+        want = oracle.fgemm(p, tA, tB, alpha, A[:, :ac], B[:, :bc], beta, C, m=m, n=n, k=k)
+        for mode in ("1", None):
+            if mode is None:
+                monkeypatch.delenv("FF_SMALL", raising=False)
+            else:
+                monkeypatch.setenv("FF_SMALL", mode)
+            dA, dB, dC = (torch.from_numpy(x).cuda() for x in (A, B, C))
+            ff.ff_gemm_ex(p, tA, tB, m, n, k, alpha, dA, la, dB, lb, beta, dC, n, {"inputs_canonical": 1})
+            torch.cuda.synchronize()
+            np.testing.assert_array_equal(dC.cpu().numpy(), want, err_msg="m=%d n=%d k=%d %s%s FF_SMALL=%s" % (
+                m, n, k, tA, tB, mode))
