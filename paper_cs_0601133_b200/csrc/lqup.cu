@@ -512,10 +512,6 @@ static_assert(kB == 16 || kB == 32, "block size");
 __device__ __forceinline__ uint32_t mulm_b(uint32_t a, uint32_t b, uint32_t p, unsigned long long mu64) {
     return residue_u64(static_cast<unsigned long long>(a) * b, mu64, p);
 }
-__device__ __forceinline__ uint32_t ffma_b(uint32_t a, uint32_t x, uint32_t b, uint32_t y, uint32_t p,
-                                           unsigned long long mu64) {   // (a x + b y) mod p
-    return residue_u64(static_cast<unsigned long long>(a) * x + static_cast<unsigned long long>(b) * y, mu64, p);
-}
 
 // C = A B (mode 0), C - A B (mode 1) or -(A B) (mode 2) mod p on shared-memory
 // residue matrices; M multiple of 4, N and K of 32; rows of A 16-byte aligned.
@@ -645,6 +641,41 @@ __device__ __forceinline__ void mm_any(bool big, const MmJob& J, int lt, int nth
     else mm_one<false>(J, lt, nthr, p, mu64);
 }
 
+// Block row b of L11^-1 and block column b of U11^-1 once blocks 0..b are final
+// (left-looking):
+//   Li[b][j] = -Li[b][b] (sum_{k=j}^{b-1} L[b][k] Li[k][j]),
+//   Ui[j][b] = -(sum_{k=j}^{b-1} Ui[j][k] U[k][b]) Ui[b][b],   j < b,
+// two dependent products over the thread group [g0, g0 + gn) (whole warps),
+// synchronised by `bar` (a named barrier for the group, or the CTA barrier).
+template <class Bar>
+__device__ __forceinline__ void inv_block(int b, const uint32_t* W, uint32_t* Li, uint32_t* Ui, uint32_t* T, int gtid,
+                                          int gn, bool big, uint32_t p, unsigned long long mu, Bar bar) {
+    if (b == 0) return;
+    const int n = 2 * b, gw = gn / 32, wpj = gw / n;
+    const int q = (gtid >> 5) / wpj, lt = gtid - q * wpj * 32;
+    const bool on = q < n;
+    const int j = q >> 1;
+    uint32_t* Tq = T + q * kB * kB;
+    if (on) {
+        if ((q & 1) == 0)       // T_L = [L[b][j] .. L[b][b-1]] [Li[j][j] ; .. ; Li[b-1][j]]
+            mm_any(big, mm_job(Tq, kB, W + b * kB * kH + j * kB, kH, Li + j * kB * kH + j * kB, kH, kB, kB, (b - j) * kB, 0),
+                   lt, wpj * 32, p, mu);
+        else                    // T_U = [Ui[j][j] .. Ui[j][b-1]] [U[j][b] ; .. ; U[b-1][b]]
+            mm_any(big, mm_job(Tq, kB, Ui + j * kB * kH + j * kB, kH, W + j * kB * kH + b * kB, kH, kB, kB, (b - j) * kB, 0),
+                   lt, wpj * 32, p, mu);
+    }
+    bar();
+    if (on) {
+        if ((q & 1) == 0)
+            mm_any(big, mm_job(Li + b * kB * kH + j * kB, kH, Li + b * kB * kH + b * kB, kH, Tq, kB, kB, kB, kB, 2),
+                   lt, wpj * 32, p, mu);
+        else
+            mm_any(big, mm_job(Ui + j * kB * kH + b * kB, kH, Tq, kB, Ui + b * kB * kH + b * kB, kH, kB, kB, kB, 2),
+                   lt, wpj * 32, p, mu);
+    }
+    bar();
+}
+
 __global__ void __launch_bounds__(kThr) panel_spec_kernel(PanelArgs P) {
     extern __shared__ __align__(16) uint32_t dyn3[];
     uint32_t* W = dyn3;                       // [kH][kH] the window -> L (strict lower) and U
@@ -688,7 +719,11 @@ __global__ void __launch_bounds__(kThr) panel_spec_kernel(PanelArgs P) {
         uint32_t* El = Li + o * kH + o;        // E_L, then L_D^-1
         uint32_t* Eu = Ui + o * kH + o;        // E_U, then U_D^-1
         uint32_t x = 0u, el = 0u, eu = 0u;
-        if (elim) {
+        if (!elim) {
+            // the other 24 warps: block kb - 1's row of L11^-1 / column of U11^-1 meanwhile
+            inv_block(kb - 1, W, Li, Ui, T, tid - kB * kB, kThr - kB * kB, big, p, mu,
+                      [] { ptx::named_bar_sync(2, kThr - kB * kB); });
+        } else {
             x = D[er * kH + ec];
             if (ec == 0) ash[0][er] = shoup_c(x, p, mu);
             if (er == 0) bsh[0][ec] = shoup_c(x, p, mu);
@@ -788,34 +823,9 @@ __global__ void __launch_bounds__(kThr) panel_spec_kernel(PanelArgs P) {
     }
     long long t_1 = clock64(), t_2 = 0;
     if (!fail) {
-        // full inverses by block waves d = j - i (block units), a warp group per block:
-        //   Li_ij = -Li_ii (sum_{k=j}^{i-1} L_ik Li_kj),  Ui_ij = -Ui_ii (sum_{k=i+1}^{j} U_ik Ui_kj)
-        constexpr int nb = kNb;
-        for (int d = 1; d < nb; ++d) {
-            const int n = 2 * (nb - d);                  // jobs: (L, U) per block pair; <= 2 (kNb - 1) scratch blocks
-            const int wpj = 32 / n, q = ty / wpj, lt = tid - q * wpj * 32;
-            const bool on = q < n;
-            const int i = d + q / 2;
-            uint32_t* Tq = T + q * kB * kB;
-            if (on) {
-                if ((q & 1) == 0)
-                    mm_any(big, mm_job(Tq, kB, W + i * kB * kH + (i - d) * kB, kH, Li + (i - d) * kB * kH + (i - d) * kB, kH,
-                                       kB, kB, d * kB, 0), lt, wpj * 32, p, mu);
-                else
-                    mm_any(big, mm_job(Tq, kB, W + (i - d) * kB * kH + (i - d + 1) * kB, kH,
-                                       Ui + (i - d + 1) * kB * kH + i * kB, kH, kB, kB, d * kB, 0), lt, wpj * 32, p, mu);
-            }
-            __syncthreads();
-            if (on) {
-                if ((q & 1) == 0)
-                    mm_any(big, mm_job(Li + i * kB * kH + (i - d) * kB, kH, Li + i * kB * kH + i * kB, kH, Tq, kB, kB, kB, kB, 2),
-                           lt, wpj * 32, p, mu);
-                else
-                    mm_any(big, mm_job(Ui + (i - d) * kB * kH + i * kB, kH, Ui + (i - d) * kB * kH + (i - d) * kB, kH, Tq, kB,
-                                       kB, kB, kB, 2), lt, wpj * 32, p, mu);
-            }
-            __syncthreads();
-        }
+        // the last block's row of L11^-1 / column of U11^-1 (the earlier ones ran
+        // beside the eliminations)
+        inv_block(kNb - 1, W, Li, Ui, T, tid, kThr, big, p, mu, [] { __syncthreads(); });
         t_2 = clock64();
         for (int e = tid; e < kH * kH; e += kThr) {
             const int r = e / kH, c = e % kH;
