@@ -761,58 +761,69 @@ __global__ void __launch_bounds__(kThr) panel_spec_kernel(PanelArgs P) {
                     eu = subm_u(shoup_m(eu, pk, pk_sh, p), shoup_m(h, D[t * kH + ec], bsh[par][ec], p), p);
                     Eu[er * kH + ec] = eu;
                 }
+                if (er == t && ec == t) { El[t * kH + t] = S; Eu[t * kH + t] = S; }   // the implicit diagonals S_t
                 S = shoup_m(S, pk, pk_sh, p);
                 ptx::named_bar_sync(1, kB * kB);
-            }
-            // (2) prefix P_t and suffix Q_t products of the pivots, one inverse of
-            // P_{kB-1}: 1/S_t = inv Q_t, 1/pk_t = (1/S_{t+1}) P_{t-1}, 1/u_tt = S_t / pk_t
-            if (!fail && ty == 0) {
-                const bool on = tx < kB;
-                const uint32_t v = on ? D[tx * kH + tx] : 1u;
-                uint32_t pre = v, suf = v;
-#pragma unroll
-                for (int d = 1; d < kB; d <<= 1) {
-                    const uint32_t y = __shfl_up_sync(0xffffffffu, pre, d);
-                    const uint32_t z = __shfl_down_sync(0xffffffffu, suf, d);
-                    if (tx >= d) pre = mulm_b(pre, y, p, mu);
-                    if (tx + d < kB) suf = mulm_b(suf, z, p, mu);
-                }
-                const uint32_t total = __shfl_sync(0xffffffffu, pre, kB - 1);
-                const uint32_t inv = inv_dev(total, p);
-                const uint32_t is = mulm_b(inv, suf, p, mu);              // 1 / S_tx
-                uint32_t is_next = __shfl_down_sync(0xffffffffu, is, 1);  // 1 / S_{tx+1} = 1 / P_tx
-                if (tx == kB - 1) is_next = inv;
-                uint32_t pprev = __shfl_up_sync(0xffffffffu, pre, 1);    // P_{tx-1} = S_tx
-                if (tx == 0) pprev = 1u % p;
-                const uint32_t ip = mulm_b(is_next, pprev, p, mu);
-                if (on) {
-                    isc[o + tx] = is;
-                    ipk[o + tx] = ip;
-                    iu[o + tx] = mulm_b(pprev, ip, p, mu);
-                }
             }
         }
         __syncthreads();
         fail = s_fail != 0;
         if (fail) break;
+        // (2) warp 0: prefix P_t and suffix Q_t products of the pivots, one inverse of
+        // P_{kB-1}: 1/S_t = inv Q_t, 1/pk_t = (1/S_{t+1}) P_{t-1}, 1/u_tt = S_t / pk_t.
+        // Meanwhile warps 1..31 form the raw products E_L A12 and A21 E_U (E_L = S L_D^-1,
+        // E_U = U_D^-1-ish with column scales S_c), scaled to U12 and L21 once the
+        // inverses are known: U12 = diag(1/S_r) (E_L A12), L21 = (A21 E_U) diag(1/pk_c).
+        const int R = kH - o - kB;
+        uint32_t* T1 = T;
+        uint32_t* T2 = T + kB * R;
+        if (ty == 0) {
+            const uint32_t v = tx < kB ? D[tx * kH + tx] : 1u;
+            uint32_t pre = v, suf = v;
+#pragma unroll
+            for (int d = 1; d < kB; d <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, pre, d);
+                const uint32_t z = __shfl_down_sync(0xffffffffu, suf, d);
+                if (tx >= d) pre = mulm_b(pre, y, p, mu);
+                if (tx + d < kB) suf = mulm_b(suf, z, p, mu);
+            }
+            const uint32_t total = __shfl_sync(0xffffffffu, pre, kB - 1);
+            const uint32_t inv = inv_dev(total, p);
+            const uint32_t is = mulm_b(inv, suf, p, mu);              // 1 / S_tx
+            uint32_t is_next = __shfl_down_sync(0xffffffffu, is, 1);  // 1 / S_{tx+1} = 1 / P_tx
+            if (tx == kB - 1) is_next = inv;
+            uint32_t pprev = __shfl_up_sync(0xffffffffu, pre, 1);    // P_{tx-1} = S_tx
+            if (tx == 0) pprev = 1u % p;
+            const uint32_t ip = mulm_b(is_next, pprev, p, mu);
+            if (tx < kB) {
+                isc[o + tx] = is;
+                ipk[o + tx] = ip;
+                iu[o + tx] = mulm_b(pprev, ip, p, mu);
+            }
+        } else if (R > 0) {
+            const int gw = 31, w1 = 15;                                  // warps 1..15 | 16..31
+            const int wi = ty - 1;
+            if (wi < w1) mm_any(big, mm_job(T1, R, El, kH, W + o * kH + o + kB, kH, kB, R, kB, 0), wi * 32 + tx, w1 * 32, p, mu);
+            else mm_any(big, mm_job(T2, kB, W + (o + kB) * kH + o, kH, Eu, kH, R, kB, kB, 0), (wi - w1) * 32 + tx,
+                        (gw - w1) * 32, p, mu);
+        }
+        __syncthreads();
         // true L_D (a / pk_c), U_D (row / S_r); L_D^-1 = E_L / S_r (unit diagonal);
-        // U_D^-1 = E_U / pk_c (E_U col c = S_c U'^-1 col c, U_D^-1 = U'^-1 diag(S_c / pk_c))
+        // U_D^-1 = E_U / pk_c (E_U col c = S_c U'^-1 col c, U_D^-1 = U'^-1 diag(S_c / pk_c));
+        // U12 rows and L21 columns scaled alike
         if (elim) {
             D[er * kH + ec] = mulm_b(x, er > ec ? ipk[o + ec] : isc[o + er], p, mu);
             El[er * kH + ec] = ec < er ? mulm_b(el, isc[o + er], p, mu) : (ec == er ? 1u : 0u);
             Eu[er * kH + ec] = er < ec ? mulm_b(eu, ipk[o + ec], p, mu) : (ec == er ? iu[o + ec] : 0u);
+        } else if (R > 0) {
+            for (int e = tid - kB * kB; e < kB * R; e += kThr - kB * kB) {
+                T1[e] = mulm_b(T1[e], isc[o + e / R], p, mu);
+                T2[e] = mulm_b(T2[e], ipk[o + e % kB], p, mu);
+            }
         }
         __syncthreads();
-        // (3) U12 = L_D^-1 A12 (T1, kB x R) and L21 = A21 U_D^-1 (T2, R x kB), then
-        // A22 -= L21 U12 while T1, T2 are copied into the window
-        const int R = kH - o - kB;
+        // (3) A22 -= L21 U12 while U12 (T1, kB x R) and L21 (T2, R x kB) are copied into the window
         if (R > 0) {
-            uint32_t* T1 = T;
-            uint32_t* T2 = T + kB * R;
-            const int half = kThr / 2, g = tid / half, lt = tid % half;
-            if (g == 0) mm_any(big, mm_job(T1, R, El, kH, W + o * kH + o + kB, kH, kB, R, kB, 0), lt, half, p, mu);
-            else mm_any(big, mm_job(T2, kB, W + (o + kB) * kH + o, kH, Eu, kH, R, kB, kB, 0), lt, half, p, mu);
-            __syncthreads();
             mm_any(big, mm_job(W + (o + kB) * kH + o + kB, kH, T2, kB, T1, R, R, R, kB, 1), tid, kThr, p, mu);
             for (int e = tid; e < kB * R; e += kThr) {
                 W[(o + e / R) * kH + o + kB + e % R] = T1[e];
