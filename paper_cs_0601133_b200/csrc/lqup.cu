@@ -744,22 +744,26 @@ __global__ void __launch_bounds__(kThr) panel_spec_kernel(PanelArgs P) {
                 const uint32_t pk = D[t * kH + t];
                 if (pk == 0u) { fail = true; if (tid == 0) s_fail = 1; break; }   // uniform: speculation failed
                 const uint32_t pk_sh = ash[par][t];
-                if (er > t) {
-                    const uint32_t a = D[er * kH + t], a_sh = ash[par][er];
-                    if (ec > t) {
-                        x = subm_u(shoup_m(x, pk, pk_sh, p), shoup_m(D[t * kH + ec], a, a_sh, p), p);
-                        D[er * kH + ec] = x;
-                        if (ec == t + 1) ash[par ^ 1][er] = shoup_c(x, p, mu);
-                        if (er == t + 1) bsh[par ^ 1][ec] = shoup_c(x, p, mu);
-                    } else {
-                        const uint32_t g = (ec == t) ? S : El[t * kH + ec];
-                        el = subm_u(shoup_m(el, pk, pk_sh, p), shoup_m(g, a, a_sh, p), p);
-                        El[er * kH + ec] = el;
+                // one update per thread, v <- pk v - X Y, without divergence: all
+                // operands are loaded and the role (D, E_L or E_U cell) selects them
+                const uint32_t a = D[er * kH + t], a_sh = ash[par][er];          // D[r][t] and its constant
+                const uint32_t u = D[t * kH + ec], u_sh = bsh[par][ec];          // D[t][c] and its constant
+                const uint32_t elt = El[t * kH + ec], eut = Eu[er * kH + t];
+                const bool rowop = er > t, colgt = ec > t;
+                const uint32_t v = rowop ? (colgt ? x : el) : eu;
+                const uint32_t X = rowop ? (colgt ? u : (ec == t ? S : elt)) : (er == t ? S : eut);
+                const uint32_t Y = rowop ? a : u, Ysh = rowop ? a_sh : u_sh;
+                const uint32_t nv = subm_u(shoup_m(v, pk, pk_sh, p), shoup_m(X, Y, Ysh, p), p);
+                if (rowop || colgt) {
+                    uint32_t* dst = rowop ? (colgt ? D : El) : Eu;
+                    dst[er * kH + ec] = nv;
+                    if (rowop && colgt) x = nv;
+                    else if (rowop) el = nv;
+                    else eu = nv;
+                    if (rowop && colgt) {
+                        if (ec == t + 1) ash[par ^ 1][er] = shoup_c(nv, p, mu);
+                        if (er == t + 1) bsh[par ^ 1][ec] = shoup_c(nv, p, mu);
                     }
-                } else if (ec > t) {
-                    const uint32_t h = (er == t) ? S : Eu[er * kH + t];
-                    eu = subm_u(shoup_m(eu, pk, pk_sh, p), shoup_m(h, D[t * kH + ec], bsh[par][ec], p), p);
-                    Eu[er * kH + ec] = eu;
                 }
                 if (er == t && ec == t) { El[t * kH + t] = S; Eu[t * kH + t] = S; }   // the implicit diagonals S_t
                 S = shoup_m(S, pk, pk_sh, p);
