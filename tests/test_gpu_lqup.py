@@ -179,3 +179,27 @@ def test_lqup_deferred_updates_match_immediate(env, dep_row, monkeypatch):
     np.testing.assert_array_equal(P1, P2)
     np.testing.assert_array_equal(F1, F2)
     _check_valid(p, A, F1, Q1, P1, r1)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_lqup_random_sweep(env, seed):
+    """Seeded random shapes, ranks and primes (incl. tiny fields where the
+    speculative panel fails and the pivoting panels take over): rank and
+    determinant against the oracle, the factorization valid."""
+    torch, ff = env
+    rng = np.random.default_rng(777 + seed)
+    primes = [2, 3, 7, 251, 4099, 65521, 8388593, 2 ** 31 - 1]
+    for _ in range(3):
+        p = int(rng.choice(primes))
+        m, n = (int(x) for x in rng.integers(1, 700, size=2))
+        if rng.random() < 0.5:
+            r = int(rng.integers(0, min(m, n) + 1))
+            A = _low_rank(rng, p, m, n, r)
+        else:
+            A = rng.integers(-2 ** 31, 2 ** 31, size=(m, n), dtype=np.int64).astype(np.int32)
+        F, Q, P, rk = _factor(torch, ff, p, A)
+        want_r, want_d = oracle.rank_det(p, A)
+        assert rk == want_r, (p, m, n)
+        _check_valid(p, A, F, Q, P, rk)
+        if m == n:
+            assert ff.rank_det(p, torch.from_numpy(A).cuda())[1] == want_d
