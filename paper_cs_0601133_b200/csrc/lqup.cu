@@ -59,6 +59,8 @@ struct PanelArgs {
     uint32_t p;
     unsigned long long mu64;     // floor(2^64 / p)
     int32_t red;                 // panel_spec_kernel: reduce 64-bit sums every red products
+    volatile int32_t* note;      // panel_spec_kernel: host-mapped [seq, fail] written last (or null)
+    int32_t seq;
     double* win;                 // workspace hr x W (ld W): the window, residues as exact doubles
     int32_t* Linv;               // kH x kH
     int32_t* Uinv;               // kH x kH
@@ -856,6 +858,11 @@ __global__ void __launch_bounds__(kThr) panel_spec_kernel(PanelArgs P) {
         P.out[1] = fail ? 1 : 0;
         P.out[2] = 0;
         P.out[3] = 0;
+        if (P.note) {                 // the host polls this instead of synchronising the stream
+            P.note[1] = fail ? 1 : 0;
+            __threadfence_system();
+            P.note[0] = P.seq;
+        }
     }
 }
 
@@ -1063,6 +1070,21 @@ int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t* A, int64_t lda, int64_
     } cleanup{ps, ev_ready, ev_panel};
     if (cudaEventRecord(ev_ready, st) != cudaSuccess) return fail_cuda();
     int buf = 0;
+    // host-mapped note for the speculative panel's outcome (one per process)
+    static volatile int32_t* note_h = nullptr;
+    static int32_t* note_d = nullptr;
+    static int32_t note_seq = 0;
+    if (!note_h) {
+        void* hp_ = nullptr;
+        if (cudaHostAlloc(&hp_, 64, cudaHostAllocMapped | cudaHostAllocPortable) == cudaSuccess &&
+            cudaHostGetDevicePointer(reinterpret_cast<void**>(&note_d), hp_, 0) == cudaSuccess) {
+            note_h = static_cast<volatile int32_t*>(hp_);
+            note_h[0] = 0;
+        } else {
+            cudaGetLastError();
+            note_d = nullptr;
+        }
+    }
     // FF_LQUP_TIMELINE=1 (development aid): per-panel event timestamps, printed at the end
     const bool tl = getenv("FF_LQUP_TIMELINE") != nullptr;
     std::vector<std::array<cudaEvent_t, 6>> tl_ev;
@@ -1088,6 +1110,8 @@ int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t* A, int64_t lda, int64_
         const int64_t hr = std::min<int64_t>(kH, m_active - i0);
         const int64_t Wc = std::min<int64_t>(W, n - c);
         PanelArgs pa;
+        pa.note = nullptr;
+        pa.seq = 0;
         pa.A = A; pa.lda = lda; pa.i0 = i0; pa.hr = hr; pa.c = c; pa.W = Wc;
         pa.full = (c + Wc == n) ? 1 : 0;
         pa.p = p;
@@ -1097,12 +1121,33 @@ int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t* A, int64_t lda, int64_
         if (cudaStreamWaitEvent(ps, ev_ready, 0) != cudaSuccess) return fail_cuda();
         if (tl) { tl_ev.emplace_back(); for (auto& x : tl_ev.back()) cudaEventCreate(&x); cudaEventRecord(tl_ev.back()[0], ps); }
         bool used_pair = false;
+        bool waited = false;
         if (Wc == kH && hr == kH && spec_fails < kSpecGiveUp) {
+            pa.note = note_d;
+            pa.seq = ++note_seq;
             panel_spec_kernel<<<1, kThr, kSpecSmem, ps>>>(pa);
-            if (cudaGetLastError() != cudaSuccess ||
-                cudaMemcpyAsync(hout.data(), dout, hout.size() * 4, cudaMemcpyDeviceToHost, ps) != cudaSuccess ||
-                cudaStreamSynchronize(ps) != cudaSuccess)
+            pa.note = nullptr;
+            if (cudaGetLastError() != cudaSuccess) return fail_cuda();
+            if (note_h) {
+                // poll the host-mapped note (lower latency than a stream synchronisation
+                // plus a copy); the stream is queried now and then for errors
+                if (tl) cudaEventRecord(tl_ev.back()[1], ps);
+                if (cudaEventRecord(ev_panel, ps) != cudaSuccess) return fail_cuda();
+                for (long spins = 1; note_h[0] != pa.seq; ++spins) {
+                    if ((spins & 4095) == 0) {
+                        const cudaError_t q = cudaStreamQuery(ps);
+                        if (q == cudaSuccess && note_h[0] != pa.seq) return FF_ERR_INTERNAL;
+                        if (q != cudaSuccess && q != cudaErrorNotReady) return fail_cuda();
+                    }
+                }
+                hout[1] = note_h[1];
+                hout[0] = hout[1] ? 0 : kH;
+                hout[2] = hout[3] = 0;
+                waited = !hout[1];
+            } else if (cudaMemcpyAsync(hout.data(), dout, hout.size() * 4, cudaMemcpyDeviceToHost, ps) != cudaSuccess ||
+                       cudaStreamSynchronize(ps) != cudaSuccess) {
                 return fail_cuda();
+            }
             used_pair = !hout[1];
             if (hout[1]) ++spec_fails;
         }
@@ -1131,9 +1176,11 @@ int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t* A, int64_t lda, int64_
             if (cudaMemcpyAsync(hout.data(), dout, hout.size() * 4, cudaMemcpyDeviceToHost, ps) != cudaSuccess)
                 return fail_cuda();
         }
-        if (tl) cudaEventRecord(tl_ev.back()[1], ps);
-        if (cudaEventRecord(ev_panel, ps) != cudaSuccess || cudaStreamSynchronize(ps) != cudaSuccess)
-            return fail_cuda();
+        if (!waited) {
+            if (tl) cudaEventRecord(tl_ev.back()[1], ps);
+            if (cudaEventRecord(ev_panel, ps) != cudaSuccess || cudaStreamSynchronize(ps) != cudaSuccess)
+                return fail_cuda();
+        }
         if (tl) cudaEventRecord(tl_ev.back()[2], st);   // host turnaround: GEMM work enqueued from here
         if (cudaStreamWaitEvent(st, ev_panel, 0) != cudaSuccess) return fail_cuda();
         const int64_t kk = hout[0];
