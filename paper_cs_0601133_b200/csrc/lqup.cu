@@ -693,19 +693,39 @@ __global__ void __launch_bounds__(kThr) panel_spec_kernel(PanelArgs P) {
     const bool big = P.red < kB;
     long long t_0 = clock64();
     {
-        constexpr int kPer = kH * kH / kThr;      // all loads in flight before any use
-        int32_t v[kPer];
+        const int32_t* src = P.A + P.i0 * P.lda + P.c;
+        const bool vec = (P.lda % 4) == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0;
+        if (vec) {                                // 16-byte rows: 4 loads per thread, all in flight
+            int4 v[4];
 #pragma unroll
-        for (int q = 0; q < kPer; ++q) {
-            const int e = tid + q * kThr;
-            v[q] = P.A[(P.i0 + e / kH) * P.lda + P.c + e % kH];
-        }
+            for (int q = 0; q < 4; ++q) {
+                const int e = (tid + q * kThr) * 4;
+                v[q] = *reinterpret_cast<const int4*>(src + static_cast<int64_t>(e / kH) * P.lda + e % kH);
+            }
 #pragma unroll
-        for (int q = 0; q < kPer; ++q) {
-            const int e = tid + q * kThr;
-            W[e] = residue_u64(static_cast<unsigned long long>(static_cast<long long>(v[q]) + (static_cast<long long>(p) << 31)), mu, p);
-            Li[e] = 0u;
-            Ui[e] = 0u;
+            for (int q = 0; q < 4; ++q) {
+                const int e = (tid + q * kThr) * 4;
+                *reinterpret_cast<uint4*>(W + e) =
+                    make_uint4(residue_i32_64(v[q].x, mu, p), residue_i32_64(v[q].y, mu, p), residue_i32_64(v[q].z, mu, p),
+                               residue_i32_64(v[q].w, mu, p));
+                *reinterpret_cast<uint4*>(Li + e) = make_uint4(0u, 0u, 0u, 0u);
+                *reinterpret_cast<uint4*>(Ui + e) = make_uint4(0u, 0u, 0u, 0u);
+            }
+        } else {
+            constexpr int kPer = kH * kH / kThr;  // all loads in flight before any use
+            int32_t v[kPer];
+#pragma unroll
+            for (int q = 0; q < kPer; ++q) {
+                const int e = tid + q * kThr;
+                v[q] = src[static_cast<int64_t>(e / kH) * P.lda + e % kH];
+            }
+#pragma unroll
+            for (int q = 0; q < kPer; ++q) {
+                const int e = tid + q * kThr;
+                W[e] = residue_i32_64(v[q], mu, p);
+                Li[e] = 0u;
+                Ui[e] = 0u;
+            }
         }
     }
     if (tid == 0) s_fail = 0;
@@ -844,11 +864,19 @@ __global__ void __launch_bounds__(kThr) panel_spec_kernel(PanelArgs P) {
         // beside the eliminations)
         inv_block(kNb - 1, W, Li, Ui, T, tid, kThr, big, p, mu, [] { __syncthreads(); });
         t_2 = clock64();
-        for (int e = tid; e < kH * kH; e += kThr) {
-            const int r = e / kH, c = e % kH;
-            P.A[(P.i0 + r) * P.lda + P.c + c] = static_cast<int32_t>(W[e]);
-            P.Linv[e] = static_cast<int32_t>(Li[e]);
-            P.Uinv[e] = static_cast<int32_t>(Ui[e]);
+        int32_t* dst = P.A + P.i0 * P.lda + P.c;
+        if ((P.lda % 4) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+            for (int e = tid * 4; e < kH * kH; e += kThr * 4) {
+                *reinterpret_cast<uint4*>(dst + static_cast<int64_t>(e / kH) * P.lda + e % kH) = *reinterpret_cast<const uint4*>(W + e);
+                *reinterpret_cast<uint4*>(P.Linv + e) = *reinterpret_cast<const uint4*>(Li + e);
+                *reinterpret_cast<uint4*>(P.Uinv + e) = *reinterpret_cast<const uint4*>(Ui + e);
+            }
+        } else {
+            for (int e = tid; e < kH * kH; e += kThr) {
+                dst[static_cast<int64_t>(e / kH) * P.lda + e % kH] = static_cast<int32_t>(W[e]);
+                P.Linv[e] = static_cast<int32_t>(Li[e]);
+                P.Uinv[e] = static_cast<int32_t>(Ui[e]);
+            }
         }
     }
     if (tid == 0) {
