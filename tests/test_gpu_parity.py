@@ -513,3 +513,31 @@ def test_baseline_config_winograd_sampled_rows(env, name):
     rows = [0, 1, m // 2 - 1, m // 2, m - 1]
     want = oracle.fgemm_rows(p, tA, tB, alpha, Ah, Bh, beta, Cinh[rows], rows, m, n, k)
     np.testing.assert_array_equal(out[rows], want)
+
+
+@pytest.mark.parametrize("p,opts", [(65521, None), (65521, {"scheme": 3}), (2 ** 31 - 1, None), (251, None)])
+def test_huge_k_sampled_rows_and_freivalds(env, p, opts):
+    """k = 2^20 + 37 (ragged last k-tile; dozens of delayed-reduction k-blocks
+    per weight group for the large primes): sampled rows against the oracle
+    and Freivalds' test on the whole output, adversarial inputs (every entry
+    p - 1, the largest centred magnitude) in half of A."""
+    torch, ff = env
+    m, n, k = 300, 200, (1 << 20) + 37
+    rng = np.random.default_rng(p % 1000 + (3 if opts else 0))
+    A = rng.integers(0, p, size=(m, k), dtype=np.int64).astype(np.int32)
+    A[: m // 2] = p - 1
+    B = rng.integers(0, p, size=(k, n), dtype=np.int64).astype(np.int32)
+    C = rng.integers(0, p, size=(m, n), dtype=np.int64).astype(np.int32)
+    alpha, beta = p - 1, 1
+    dA, dB, dC = (torch.from_numpy(x).cuda() for x in (A, B, C))
+    ff.ff_gemm_ex(p, "N", "N", m, n, k, alpha, dA, k, dB, n, beta, dC, n, opts)
+    torch.cuda.synchronize()
+    out = dC.cpu().numpy()
+    rows = [0, 1, m // 2 - 1, m // 2, m - 1]
+    np.testing.assert_array_equal(out[rows], oracle.fgemm_rows(p, "N", "N", alpha, A, B, beta, C[rows], rows, m, n, k))
+    for t in range(2):
+        x = ffgen.uniform_vector(p, 99, 40 + t, n)
+        lhs = oracle.matvec(p, "N", out, x).astype(np.int64)
+        rhs = ((alpha % p) * oracle.matvec(p, "N", A, oracle.matvec(p, "N", B, x)).astype(np.int64)
+               + beta * oracle.matvec(p, "N", C, x).astype(np.int64)) % p
+        np.testing.assert_array_equal(lhs, rhs)
