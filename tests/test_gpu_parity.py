@@ -541,3 +541,30 @@ def test_huge_k_sampled_rows_and_freivalds(env, p, opts):
         rhs = ((alpha % p) * oracle.matvec(p, "N", A, oracle.matvec(p, "N", B, x)).astype(np.int64)
                + beta * oracle.matvec(p, "N", C, x).astype(np.int64)) % p
         np.testing.assert_array_equal(lhs, rhs)
+
+
+def test_more_than_2_31_elements_sampled_rows(env):
+    """m = 3 * 2^26 rows, n = 16, k = 16: A and C hold 3 * 2^30 elements each
+    (12 GiB; the limb planes, k padded to 128, 48 GiB), so every row past 2^27
+    is addressed beyond 2^31 elements.  A comes from the
+    device twin of the seeded generator; the sampled rows (around the 2^31-
+    element boundary and at the end) are regenerated on the host by ffgen and
+    checked against the oracle."""
+    torch, ff = env
+    p, m, n, k, seed = 65521, 3 << 26, 16, 16, 5
+    A = torch.empty((m, k), dtype=torch.int32, device="cuda")
+    ff.ff_fill_uniform(A, m, k, k, p, seed, 0)
+    B = torch.from_numpy(ffgen.uniform_matrix(p, seed, 1, k, n)).cuda()
+    C = torch.empty((m, n), dtype=torch.int32, device="cuda")
+    ff.fgemm(p, A, B, C, 3, 0)
+    torch.cuda.synchronize()
+    edge = (1 << 31) // n
+    rows = [0, edge - 1, edge, edge + 1, m - 2, m - 1]
+    got = C[rows].cpu().numpy()
+    Bh = B.cpu().numpy()
+    for i, r in enumerate(rows):
+        Ar = ffgen.uniform_matrix(p, seed, 0, m, k, row0=r, nrows=1)
+        want = oracle.fgemm(p, "N", "N", 3, Ar, Bh, 0, None, m=1, n=n, k=k)
+        np.testing.assert_array_equal(got[i:i + 1], want, err_msg="row %d" % r)
+    del A, C
+    torch.cuda.empty_cache()
