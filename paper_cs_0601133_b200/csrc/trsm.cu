@@ -63,6 +63,16 @@ constexpr int kInvSmem = (2 * kNb * kNb + kNb) * 4;
 // (the multipliers use the original D: eliminating columns to the right of k
 // never changes column k); then W_k = E_k / D_kk.  Lower D mirrors it.  One
 // barrier per phase; the dependent chain per phase is a single product.
+// Shoup's constant floor(w 2^32 / p) for w < p < 2^31 from mu64 = floor(2^64 / p)
+// ((w mu64) >> 32 is the floor or one less; one 64-bit check makes it exact)
+__device__ __forceinline__ uint32_t shoup_mu(uint32_t w, uint32_t p, unsigned long long mu64) {
+    const unsigned long long lo = static_cast<unsigned long long>(w) * static_cast<uint32_t>(mu64);
+    const unsigned long long hi = static_cast<unsigned long long>(w) * static_cast<uint32_t>(mu64 >> 32);
+    unsigned long long c = hi + (lo >> 32);
+    if ((c + 1) * p <= (static_cast<unsigned long long>(w) << 32)) ++c;
+    return static_cast<uint32_t>(c);
+}
+
 __global__ void __launch_bounds__(kInvThreads) trsm_diag_inv_kernel(InvArgs a) {
     extern __shared__ uint32_t sm[];
     uint32_t* D = sm;                    // [kNb][kNb]
@@ -93,8 +103,9 @@ __global__ void __launch_bounds__(kInvThreads) trsm_diag_inv_kernel(InvArgs a) {
                 const uint32_t d = D[r * kNb + k];
                 if (d == 0u) continue;
                 const uint32_t mlt = residue_u64(static_cast<unsigned long long>(d) * dinv[k], a.mu64, p);
+                const uint32_t mlt_sh = shoup_mu(mlt, p, a.mu64);     // per-row Shoup constant
                 for (int c = k + tx; c < db; c += 32) {
-                    const uint32_t t = residue_u64(static_cast<unsigned long long>(mlt) * E[k * kNb + c], a.mu64, p);
+                    const uint32_t t = mulmod_shoup(E[k * kNb + c], mlt, mlt_sh, p);
                     const uint32_t x = E[r * kNb + c];
                     E[r * kNb + c] = x >= t ? x - t : x + p - t;
                 }
@@ -107,8 +118,9 @@ __global__ void __launch_bounds__(kInvThreads) trsm_diag_inv_kernel(InvArgs a) {
                 const uint32_t d = D[r * kNb + k];
                 if (d == 0u) continue;
                 const uint32_t mlt = residue_u64(static_cast<unsigned long long>(d) * dinv[k], a.mu64, p);
+                const uint32_t mlt_sh = shoup_mu(mlt, p, a.mu64);
                 for (int c = tx; c <= k; c += 32) {
-                    const uint32_t t = residue_u64(static_cast<unsigned long long>(mlt) * E[k * kNb + c], a.mu64, p);
+                    const uint32_t t = mulmod_shoup(E[k * kNb + c], mlt, mlt_sh, p);
                     const uint32_t x = E[r * kNb + c];
                     E[r * kNb + c] = x >= t ? x - t : x + p - t;
                 }
