@@ -31,8 +31,8 @@ namespace ff {
 
 namespace {
 
-constexpr int kNb = 128;            // diagonal block size inverted by trsm_diag_inv_kernel
-constexpr int kLeaf = 512;          // leaf size of the recursion: inverses doubled 128 -> 256 -> 512
+constexpr int kNb = 64;             // diagonal block size inverted by trsm_diag_inv_kernel
+constexpr int kLeaf = 512;          // leaf size of the recursion: inverses doubled 64 -> 128 -> 256 -> 512
 
 struct InvArgs {
     const int32_t* A;
