@@ -166,6 +166,14 @@ bool prefer_small_canon(int64_t m, int64_t n, int64_t k) {
     return k <= 1024 && m * n <= (int64_t{1} << 21) && m * n * k < (int64_t{1} << 30);
 }
 
+// The same for 2^16 <= p < 2^31 (3-4 bytes per residue): FF_SMALL as above.
+bool prefer_small_wide(int64_t m, int64_t n, int64_t k) {
+    const char* env = getenv("FF_SMALL");
+    const int mode = env ? atoi(env) : -1;
+    if (mode >= 0) return mode > 0;
+    return k <= 1024 && m * n <= (int64_t{1} << 21) && m * n * k < (int64_t{1} << 29);
+}
+
 int run(const Plan& pl, char transA, char transB, int64_t m, int64_t n, int64_t k, const int32_t* A,
         int64_t lda, const int32_t* B, int64_t ldb, int32_t* C, int64_t ldc, void* ws, cudaStream_t st) {
     if (k == 0 || pl.mp.alpha == 0) return cuda_rc(launch_scale_c(pl.mp, m, n, C, ldc, st));
@@ -173,6 +181,9 @@ int run(const Plan& pl, char transA, char transB, int64_t m, int64_t n, int64_t 
     if (pl.all_auto && small_canon_ok(pl, is_t(transA), is_t(transB), m, n, k, A, lda, B, ldb) &&
         prefer_small_canon(m, n, k))
         return launch_gemm_small_canon(pl, m, n, k, A, lda, B, ldb, C, ldc, st);
+    if (pl.all_auto && small_wide_ok(pl, is_t(transA), is_t(transB), m, n, k, A, lda, B, ldb) &&
+        prefer_small_wide(m, n, k))
+        return launch_gemm_small_wide(pl, m, n, k, A, lda, B, ldb, C, ldc, st);
     if (pl.all_auto && small_path_ok(pl, m, n, k) && prefer_small(m, n, k))
         return launch_gemm_small(pl, is_t(transA), is_t(transB), m, n, k, A, lda, B, ldb, C, ldc, st);
     int8_t* al = static_cast<int8_t*>(ws);

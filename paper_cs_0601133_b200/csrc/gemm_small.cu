@@ -254,7 +254,148 @@ __global__ void __launch_bounds__(kSThreads) small_gemm_canon_kernel(const __gri
         }
 }
 
+// Wider fields (2^16 <= p < 2^31), canonical operands: L = 3 or 4 bytes per
+// residue and all L^2 byte products per K slice (each exact in s32 for K <= 33025),
+// recombined at the end as sum_{i,j} (P_ij mod p) (256^(i+j) mod p) mod p.  The
+// L^2 accumulators need a narrower tile: 64 x 16 per CTA, one m16n8 tile per warp.
+constexpr int kWN = 16;
+constexpr int kWBpitch = kWN + 4;
+constexpr int kWSmem = kCStages * (kSM * kCApitch + kSK * kWBpitch) * 4;
+
+__device__ __forceinline__ uint32_t pack_byte(uint32_t x, uint32_t y, uint32_t z, uint32_t w, int b) {
+    const uint32_t s = static_cast<uint32_t>(b) | (static_cast<uint32_t>(4 + b) << 4);
+    return __byte_perm(__byte_perm(x, y, s), __byte_perm(z, w, s), 0x5410);
+}
+
+template <int L>
+__global__ void __launch_bounds__(kSThreads) small_gemm_wide_kernel(const __grid_constant__ SmallArgs a) {
+    extern __shared__ __align__(16) uint32_t wsm[];
+    uint32_t* As = wsm;                                  // [kCStages][kSM][kCApitch]
+    uint32_t* Bs = wsm + kCStages * kSM * kCApitch;      // [kCStages][kSK][kWBpitch]
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+    const int wm = warp & 3, wn = warp >> 2;
+    const int m0 = blockIdx.y * kSM, n0 = blockIdx.x * kWN;
+    const int nsl = (a.k + kSK - 1) / kSK;
+    auto issue = [&](int sl) {
+        if (sl < nsl) {
+            const int st = sl % kCStages, k0 = sl * kSK;
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {                // A: 64 rows x 8 chunks of 4
+                const int e = tid + j * kSThreads, r = e >> 3, kc = (e & 7) * 4;
+                const int row = m0 + r, kk = k0 + kc;
+                const int nb = (row < a.m && kk < a.k) ? 4 * min(4, a.k - kk) : 0;
+                const int32_t* src = nb ? a.A + static_cast<int64_t>(row) * a.lda + kk : a.A;
+                cp_async16(As + (st * kSM + r) * kCApitch + kc, src, nb);
+            }
+            if (tid < kSK * kWN / 4) {                  // B: 32 rows x 4 chunks of 4
+                const int r = tid >> 2, cc = (tid & 3) * 4;
+                const int kk = k0 + r, col = n0 + cc;
+                const int nb = (kk < a.k && col < a.n) ? 4 * min(4, a.n - col) : 0;
+                const int32_t* src = nb ? a.B + static_cast<int64_t>(kk) * a.ldb + col : a.B;
+                cp_async16(Bs + (st * kSK + r) * kWBpitch + cc, src, nb);
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    int P[L * L][4];
+#pragma unroll
+    for (int q = 0; q < L * L; ++q)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) P[q][e] = 0;
+    for (int s = 0; s < kCStages - 1; ++s) issue(s);
+    for (int sl = 0; sl < nsl; ++sl) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(kCStages - 2) : "memory");
+        __syncthreads();
+        issue(sl + kCStages - 1);
+        const uint32_t* A_ = As + (sl % kCStages) * kSM * kCApitch;
+        const uint32_t* B_ = Bs + (sl % kCStages) * kSK * kWBpitch;
+        uint32_t av[4][4], bv[2][4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint4 v = *reinterpret_cast<const uint4*>(A_ + (wm * 16 + g + ((q & 1) ? 8 : 0)) * kCApitch +
+                                                            ((q & 2) ? 16 : 0) + 4 * t);
+            av[q][0] = v.x; av[q][1] = v.y; av[q][2] = v.z; av[q][3] = v.w;
+        }
+        const int c = wn * 8 + g;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int kk = (q ? 16 : 0) + 4 * t;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) bv[q][i] = B_[(kk + i) * kWBpitch + c];
+        }
+#pragma unroll
+        for (int i = 0; i < L; ++i) {
+            const uint32_t a0 = pack_byte(av[0][0], av[0][1], av[0][2], av[0][3], i);
+            const uint32_t a1 = pack_byte(av[1][0], av[1][1], av[1][2], av[1][3], i);
+            const uint32_t a2 = pack_byte(av[2][0], av[2][1], av[2][2], av[2][3], i);
+            const uint32_t a3 = pack_byte(av[3][0], av[3][1], av[3][2], av[3][3], i);
+#pragma unroll
+            for (int j = 0; j < L; ++j) {
+                const uint32_t b0 = pack_byte(bv[0][0], bv[0][1], bv[0][2], bv[0][3], j);
+                const uint32_t b1 = pack_byte(bv[1][0], bv[1][1], bv[1][2], bv[1][3], j);
+                imma(P[i * L + j], a0, a1, a2, a3, b0, b1);
+            }
+        }
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    const uint32_t p = a.M.p;
+    uint32_t w[2 * L - 1];                               // 256^s mod p
+    w[0] = 1u % p;
+#pragma unroll
+    for (int q = 1; q < 2 * L - 1; ++q) w[q] = residue_u64(static_cast<unsigned long long>(w[q - 1]) * 256u, a.mu64, p);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const int r = m0 + wm * 16 + g + ((e & 2) ? 8 : 0);
+        const int cc = n0 + wn * 8 + 2 * t + (e & 1);
+        if (r >= a.m || cc >= a.n) continue;
+        uint32_t S = 0u;
+#pragma unroll
+        for (int i = 0; i < L; ++i)
+#pragma unroll
+            for (int j = 0; j < L; ++j)
+                S = residue_u64(static_cast<unsigned long long>(S) +
+                                    static_cast<unsigned long long>(static_cast<uint32_t>(P[i * L + j][e])) * w[i + j],
+                                a.mu64, p);
+        uint32_t x = mulmod_shoup(S, a.M.alpha, a.M.alpha_sh, p);
+        int32_t* cp = a.C + static_cast<int64_t>(r) * a.ldc + cc;
+        if (a.M.beta) x = addmod(x, mulmod_shoup(residue_i32(*cp, a.M), a.M.beta, a.M.beta_sh, p), p);
+        *cp = static_cast<int32_t>(x);
+    }
+}
+
 }  // namespace
+
+bool small_wide_ok(const Plan& pl, bool tA, bool tB, int64_t m, int64_t n, int64_t k, const int32_t* A, int64_t lda,
+                   const int32_t* B, int64_t ldb) {
+    return pl.canonical_ab && !tA && !tB && pl.mp.p >= 65536u && k > 0 && k <= 32768 && m > 0 && n > 0 &&
+           m < (1ll << 30) && n < (1ll << 30) && (lda % 4) == 0 && (ldb % 4) == 0 &&
+           (reinterpret_cast<uintptr_t>(A) & 15) == 0 && (reinterpret_cast<uintptr_t>(B) & 15) == 0;
+}
+
+int launch_gemm_small_wide(const Plan& pl, int64_t m, int64_t n, int64_t k, const int32_t* A, int64_t lda,
+                           const int32_t* B, int64_t ldb, int32_t* C, int64_t ldc, cudaStream_t st) {
+    SmallArgs a;
+    a.M = pl.mp;
+    a.mu64 = static_cast<unsigned long long>((static_cast<unsigned __int128>(1) << 64) / pl.mp.p);
+    a.A = A; a.B = B; a.C = C;
+    a.lda = lda; a.ldb = ldb; a.ldc = ldc;
+    a.m = static_cast<int32_t>(m); a.n = static_cast<int32_t>(n); a.k = static_cast<int32_t>(k);
+    a.tA = 0; a.tB = 0;
+    const dim3 grid(static_cast<unsigned>((n + kWN - 1) / kWN), static_cast<unsigned>((m + kSM - 1) / kSM));
+    if (grid.y > 65535u) return FF_ERR_INTERNAL;
+    static bool attr = false;
+    if (!attr) {
+        if (cudaFuncSetAttribute(small_gemm_wide_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kWSmem) !=
+                cudaSuccess ||
+            cudaFuncSetAttribute(small_gemm_wide_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kWSmem) !=
+                cudaSuccess)
+            return FF_ERR_CUDA;
+        attr = true;
+    }
+    if (pl.mp.p < (1u << 24)) small_gemm_wide_kernel<3><<<grid, kSThreads, kWSmem, st>>>(a);
+    else small_gemm_wide_kernel<4><<<grid, kSThreads, kWSmem, st>>>(a);
+    return cudaGetLastError() == cudaSuccess ? 0 : FF_ERR_CUDA;
+}
 
 bool small_canon_ok(const Plan& pl, bool tA, bool tB, int64_t m, int64_t n, int64_t k, const int32_t* A, int64_t lda,
                     const int32_t* B, int64_t ldb) {

@@ -65,10 +65,11 @@ def test_small_path_k_at_the_s32_bound(env, monkeypatch):
     np.testing.assert_array_equal(dC.cpu().numpy(), want)
 
 
-@pytest.mark.parametrize("p", [2, 251, 65521])
+@pytest.mark.parametrize("p", [2, 251, 65521, 65537, 8388593, 16777259, 67108859, 2 ** 31 - 1])
 def test_small_path_canonical_inputs(env, p, monkeypatch):
-    """inputs_canonical = 1 (A, B already in [0, p)): the cp.async variant
-    streams them raw; ragged K and n exercise its partial (zero-filled) 16-byte
+    """inputs_canonical = 1 (A, B already in [0, p)): the cp.async variants
+    stream them raw (p < 2^16: two bytes, four byte products; larger p: three
+    or four bytes, 9 or 16 byte products); ragged K and n exercise its partial (zero-filled) 16-byte
     chunks, transposed operands fall back to the reducing kernel.  C stays any
     int32.  Bit-exact vs the oracle, forced on and under the default rule."""
     torch, ff = env
