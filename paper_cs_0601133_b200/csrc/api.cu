@@ -1,3 +1,4 @@
+#include <utility>
 // api.cu -- the C ABI (include/ffgemm.h): argument checking, quick returns,
 // workspace management and the launch sequence encode(A), encode(B), gemm_tc.
 #include <cuda_runtime.h>
@@ -178,13 +179,29 @@ int run(const Plan& pl, char transA, char transB, int64_t m, int64_t n, int64_t 
         int64_t lda, const int32_t* B, int64_t ldb, int32_t* C, int64_t ldc, void* ws, cudaStream_t st) {
     if (k == 0 || pl.mp.alpha == 0) return cuda_rc(launch_scale_c(pl.mp, m, n, C, ldc, st));
     if (pl.fp64) return run_f64(pl, is_t(transA), is_t(transB), m, n, k, A, lda, B, ldb, C, ldc, ws, st);
+    // The small paths read A and B while other CTAs write C, so C must not overlap
+    // them (an in-place product, e.g. LQUP's U_rest = L11^-1 A_rest, takes the
+    // tcgen05 path, which reads only the encoded planes).  Conservative span test.
+    auto span = [](const int32_t* X, int64_t rows, int64_t cols, int64_t ld) {
+        const uintptr_t lo = reinterpret_cast<uintptr_t>(X);
+        return std::make_pair(lo, lo + static_cast<uintptr_t>(((rows - 1) * ld + cols) * 4));
+    };
+    const auto sa = is_t(transA) ? span(A, k, m, lda) : span(A, m, k, lda);
+    const auto sb = is_t(transB) ? span(B, n, k, ldb) : span(B, k, n, ldb);
+    const auto sc = span(C, m, n, ldc);
+    const bool c_disjoint = (sc.second <= sa.first || sa.second <= sc.first) &&
+                            (sc.second <= sb.first || sb.second <= sc.first);
+    // (the canonical-input variants handle overlap with a grid barrier instead)
     if (pl.all_auto && small_canon_ok(pl, is_t(transA), is_t(transB), m, n, k, A, lda, B, ldb) &&
-        prefer_small_canon(m, n, k))
-        return launch_gemm_small_canon(pl, m, n, k, A, lda, B, ldb, C, ldc, st);
-    if (pl.all_auto && small_wide_ok(pl, is_t(transA), is_t(transB), m, n, k, A, lda, B, ldb) &&
-        prefer_small_wide(m, n, k))
-        return launch_gemm_small_wide(pl, m, n, k, A, lda, B, ldb, C, ldc, st);
-    if (pl.all_auto && small_path_ok(pl, m, n, k) && prefer_small(m, n, k))
+        prefer_small_canon(m, n, k)) {
+        const int e = launch_gemm_small_canon(pl, m, n, k, A, lda, B, ldb, C, ldc, !c_disjoint, st);
+        if (e != FF_ERR_INTERNAL) return e;
+    } else if (pl.all_auto && small_wide_ok(pl, is_t(transA), is_t(transB), m, n, k, A, lda, B, ldb) &&
+               prefer_small_wide(m, n, k)) {
+        const int e = launch_gemm_small_wide(pl, m, n, k, A, lda, B, ldb, C, ldc, !c_disjoint, st);
+        if (e != FF_ERR_INTERNAL) return e;
+    }
+    if (pl.all_auto && c_disjoint && small_path_ok(pl, m, n, k) && prefer_small(m, n, k))
         return launch_gemm_small(pl, is_t(transA), is_t(transB), m, n, k, A, lda, B, ldb, C, ldc, st);
     int8_t* al = static_cast<int8_t*>(ws);
     int8_t* bl = al + align256(static_cast<size_t>(pl.info.L) * m * pl.info.k_pad);

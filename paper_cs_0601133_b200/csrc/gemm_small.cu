@@ -19,6 +19,7 @@
 // input is reduced on load, reading R3); fragments are built from them with
 // byte permutes.  The next K slice is loaded into registers while the current
 // one is multiplied (register double buffering).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -44,6 +45,7 @@ struct SmallArgs {
     int64_t lda, ldb, ldc;
     int32_t m, n, k;
     int32_t tA, tB;                // 1: op(X) = X^T
+    int32_t alias;                 // 1: C overlaps A or B: grid-wide barrier between reads and writes
 };
 
 __device__ __forceinline__ void imma(int (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
@@ -235,6 +237,7 @@ __global__ void __launch_bounds__(kSThreads) small_gemm_canon_kernel(const __gri
         }
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
+    if (a.alias) cooperative_groups::this_grid().sync();   // every CTA has read its A, B before C is written
     const uint32_t p = a.M.p;
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt)
@@ -338,6 +341,7 @@ __global__ void __launch_bounds__(kSThreads) small_gemm_wide_kernel(const __grid
         }
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
+    if (a.alias) cooperative_groups::this_grid().sync();   // every CTA has read its A, B before C is written
     const uint32_t p = a.M.p;
     uint32_t w[2 * L - 1];                               // 256^s mod p
     w[0] = 1u % p;
@@ -365,6 +369,39 @@ __global__ void __launch_bounds__(kSThreads) small_gemm_wide_kernel(const __grid
 
 }  // namespace
 
+// Plain launch, or (alias) a cooperative one with every CTA co-resident for the
+// grid barrier; FF_ERR_INTERNAL if the grid cannot be co-resident (the caller
+// then takes the tcgen05 path).
+int launch_small(const void* fn, dim3 grid, int smem, SmallArgs& a, bool alias, cudaStream_t st) {
+    static const void* done[4] = {nullptr, nullptr, nullptr, nullptr};   // attribute set once per kernel
+    bool seen = false;
+    for (const void* d : done) seen = seen || d == fn;
+    if (!seen) {
+        if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return FF_ERR_CUDA;
+        for (auto& d : done)
+            if (!d) { d = fn; break; }
+    }
+    void* args[] = {&a};
+    if (!alias) {
+        if (cudaLaunchKernel(fn, grid, dim3(kSThreads), args, static_cast<size_t>(smem), st) != cudaSuccess) {
+            cudaGetLastError();
+            return FF_ERR_CUDA;
+        }
+        return 0;
+    }
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kSThreads, static_cast<size_t>(smem)) != cudaSuccess) {
+        cudaGetLastError();
+        return FF_ERR_INTERNAL;
+    }
+    if (static_cast<int64_t>(per_sm) * num_sms() < static_cast<int64_t>(grid.x) * grid.y) return FF_ERR_INTERNAL;
+    if (cudaLaunchCooperativeKernel(fn, grid, dim3(kSThreads), args, static_cast<size_t>(smem), st) != cudaSuccess) {
+        cudaGetLastError();
+        return FF_ERR_CUDA;
+    }
+    return 0;
+}
+
 bool small_wide_ok(const Plan& pl, bool tA, bool tB, int64_t m, int64_t n, int64_t k, const int32_t* A, int64_t lda,
                    const int32_t* B, int64_t ldb) {
     return pl.canonical_ab && !tA && !tB && pl.mp.p >= 65536u && k > 0 && k <= 32768 && m > 0 && n > 0 &&
@@ -373,7 +410,7 @@ bool small_wide_ok(const Plan& pl, bool tA, bool tB, int64_t m, int64_t n, int64
 }
 
 int launch_gemm_small_wide(const Plan& pl, int64_t m, int64_t n, int64_t k, const int32_t* A, int64_t lda,
-                           const int32_t* B, int64_t ldb, int32_t* C, int64_t ldc, cudaStream_t st) {
+                           const int32_t* B, int64_t ldb, int32_t* C, int64_t ldc, bool alias, cudaStream_t st) {
     SmallArgs a;
     a.M = pl.mp;
     a.mu64 = static_cast<unsigned long long>((static_cast<unsigned __int128>(1) << 64) / pl.mp.p);
@@ -383,18 +420,10 @@ int launch_gemm_small_wide(const Plan& pl, int64_t m, int64_t n, int64_t k, cons
     a.tA = 0; a.tB = 0;
     const dim3 grid(static_cast<unsigned>((n + kWN - 1) / kWN), static_cast<unsigned>((m + kSM - 1) / kSM));
     if (grid.y > 65535u) return FF_ERR_INTERNAL;
-    static bool attr = false;
-    if (!attr) {
-        if (cudaFuncSetAttribute(small_gemm_wide_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kWSmem) !=
-                cudaSuccess ||
-            cudaFuncSetAttribute(small_gemm_wide_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kWSmem) !=
-                cudaSuccess)
-            return FF_ERR_CUDA;
-        attr = true;
-    }
-    if (pl.mp.p < (1u << 24)) small_gemm_wide_kernel<3><<<grid, kSThreads, kWSmem, st>>>(a);
-    else small_gemm_wide_kernel<4><<<grid, kSThreads, kWSmem, st>>>(a);
-    return cudaGetLastError() == cudaSuccess ? 0 : FF_ERR_CUDA;
+    a.alias = alias ? 1 : 0;
+    const void* fn = pl.mp.p < (1u << 24) ? reinterpret_cast<const void*>(small_gemm_wide_kernel<3>)
+                                          : reinterpret_cast<const void*>(small_gemm_wide_kernel<4>);
+    return launch_small(fn, grid, kWSmem, a, alias, st);
 }
 
 bool small_canon_ok(const Plan& pl, bool tA, bool tB, int64_t m, int64_t n, int64_t k, const int32_t* A, int64_t lda,
@@ -405,7 +434,7 @@ bool small_canon_ok(const Plan& pl, bool tA, bool tB, int64_t m, int64_t n, int6
 }
 
 int launch_gemm_small_canon(const Plan& pl, int64_t m, int64_t n, int64_t k, const int32_t* A, int64_t lda,
-                            const int32_t* B, int64_t ldb, int32_t* C, int64_t ldc, cudaStream_t st) {
+                            const int32_t* B, int64_t ldb, int32_t* C, int64_t ldc, bool alias, cudaStream_t st) {
     SmallArgs a;
     a.M = pl.mp;
     a.mu64 = static_cast<unsigned long long>((static_cast<unsigned __int128>(1) << 64) / pl.mp.p);
@@ -415,15 +444,8 @@ int launch_gemm_small_canon(const Plan& pl, int64_t m, int64_t n, int64_t k, con
     a.tA = 0; a.tB = 0;
     const dim3 grid(static_cast<unsigned>((n + kSN - 1) / kSN), static_cast<unsigned>((m + kSM - 1) / kSM));
     if (grid.y > 65535u) return FF_ERR_INTERNAL;
-    static bool attr = false;
-    if (!attr) {
-        if (cudaFuncSetAttribute(small_gemm_canon_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kCSmem) !=
-            cudaSuccess)
-            return FF_ERR_CUDA;
-        attr = true;
-    }
-    small_gemm_canon_kernel<<<grid, kSThreads, kCSmem, st>>>(a);
-    return cudaGetLastError() == cudaSuccess ? 0 : FF_ERR_CUDA;
+    a.alias = alias ? 1 : 0;
+    return launch_small(reinterpret_cast<const void*>(small_gemm_canon_kernel), grid, kCSmem, a, alias, st);
 }
 
 bool small_path_ok(const Plan& pl, int64_t m, int64_t n, int64_t k) {
@@ -440,6 +462,7 @@ int launch_gemm_small(const Plan& pl, bool tA, bool tB, int64_t m, int64_t n, in
     a.lda = lda; a.ldb = ldb; a.ldc = ldc;
     a.m = static_cast<int32_t>(m); a.n = static_cast<int32_t>(n); a.k = static_cast<int32_t>(k);
     a.tA = tA ? 1 : 0; a.tB = tB ? 1 : 0;
+    a.alias = 0;
     const dim3 grid(static_cast<unsigned>((n + kSN - 1) / kSN), static_cast<unsigned>((m + kSM - 1) / kSM));
     if (grid.y > 65535u) return FF_ERR_INTERNAL;
     small_gemm_kernel<<<grid, kSThreads, 0, st>>>(a);

@@ -96,12 +96,14 @@ int launch_gemm_small(const Plan& pl, bool tA, bool tB, int64_t m, int64_t n, in
 
 bool small_canon_ok(const Plan& pl, bool tA, bool tB, int64_t m, int64_t n, int64_t k, const int32_t* A, int64_t lda,
                     const int32_t* B, int64_t ldb);
+// alias: C overlaps A or B (in-place products): a cooperative launch with a grid barrier between the
+// reads and the writes; FF_ERR_INTERNAL if the grid cannot be co-resident
 int launch_gemm_small_canon(const Plan& pl, int64_t m, int64_t n, int64_t k, const int32_t* A, int64_t lda,
-                            const int32_t* B, int64_t ldb, int32_t* C, int64_t ldc, cudaStream_t st);
+                            const int32_t* B, int64_t ldb, int32_t* C, int64_t ldc, bool alias, cudaStream_t st);
 bool small_wide_ok(const Plan& pl, bool tA, bool tB, int64_t m, int64_t n, int64_t k, const int32_t* A, int64_t lda,
                    const int32_t* B, int64_t ldb);
 int launch_gemm_small_wide(const Plan& pl, int64_t m, int64_t n, int64_t k, const int32_t* A, int64_t lda,
-                           const int32_t* B, int64_t ldb, int32_t* C, int64_t ldc, cudaStream_t st);
+                           const int32_t* B, int64_t ldb, int32_t* C, int64_t ldc, bool alias, cudaStream_t st);
 
 // gemm_tc.cu
 struct OutSpec {          // C <- (a * A B + b * C) mod p for one output block

@@ -95,3 +95,36 @@ def test_small_path_canonical_inputs(env, p, monkeypatch):
             torch.cuda.synchronize()
             np.testing.assert_array_equal(dC.cpu().numpy(), want, err_msg="m=%d n=%d k=%d %s%s FF_SMALL=%s" % (
                 m, n, k, tA, tB, mode))
+
+
+@pytest.mark.parametrize("p", [65521, 8388593])
+@pytest.mark.parametrize("canonical", [0, 1])
+def test_in_place_products(env, p, canonical, monkeypatch):
+    """C aliasing B (X <- W X) or A (X <- X W), as LQUP's U_rest / G products
+    do: the small paths read A and B while other CTAs write C, so an overlap
+    must either take the grid-barrier variant (canonical inputs) or the
+    tcgen05 path (which reads only its encoded planes).  Forced small paths
+    (FF_SMALL=1) included; results bit-exact."""
+    torch, ff = env
+    rng = np.random.default_rng(p + canonical)
+    for mode in ("1", None):
+        if mode is None:
+            monkeypatch.delenv("FF_SMALL", raising=False)
+        else:
+            monkeypatch.setenv("FF_SMALL", mode)
+        for (r, c) in [(128, 1000), (300, 128), (128, 128)]:
+            k = r if c >= r else c
+            W = rng.integers(0, p, size=(k, k), dtype=np.int64).astype(np.int32)
+            X = rng.integers(0, p, size=(r, c), dtype=np.int64).astype(np.int32)
+            opts = {"inputs_canonical": canonical}
+            dW = torch.from_numpy(W).cuda()
+            if c >= r:      # X <- W X  (C = B)
+                dX = torch.from_numpy(X).cuda()
+                ff.ff_gemm_ex(p, "N", "N", r, c, r, 1, dW, k, dX, c, 0, dX, c, opts)
+                want = oracle.fgemm(p, "N", "N", 1, W, X, 0, None, m=r, n=c, k=r)
+            else:           # X <- X W  (C = A)
+                dX = torch.from_numpy(X).cuda()
+                ff.ff_gemm_ex(p, "N", "N", r, c, c, 1, dX, c, dW, k, 0, dX, c, opts)
+                want = oracle.fgemm(p, "N", "N", 1, X, W, 0, None, m=r, n=c, k=c)
+            torch.cuda.synchronize()
+            np.testing.assert_array_equal(dX.cpu().numpy(), want, err_msg="%dx%d FF_SMALL=%s" % (r, c, mode))
