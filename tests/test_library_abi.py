@@ -204,3 +204,29 @@ def test_f64_plan_is_paper_eq2(ff):
         ff.ff_plan_query(2 ** 27 - 39, 10, {"scheme": 4})       # lambda < 4: beyond the paper's 2^26 bound
     with pytest.raises(ff.FFError):
         ff.ff_plan_query(65521, 10, {"scheme": 4, "kb_override": 2 ** 23})
+
+
+def test_struct_layouts_match_the_header(ff, tmp_path):
+    """The ctypes mirrors of ff_opts and ff_plan_info (the Python binding) have
+    the header's size and field offsets: compiled and measured with the host C
+    compiler from include/ffgemm.h itself."""
+    import subprocess
+    from paper_cs_0601133_b200 import ffgemm as binding
+    structs = {"ff_opts": binding.ff_opts, "ff_plan_info": binding.ff_plan_info}
+    lines = ['#include <stddef.h>', '#include <stdio.h>', '#include "ffgemm.h"', "int main(void) {"]
+    for name, cls in structs.items():
+        lines.append('printf("%s sizeof %%zu\\n", sizeof(%s));' % (name, name))
+        for fname, _ in cls._fields_:
+            lines.append('printf("%s %s %%zu\\n", offsetof(%s, %s));' % (name, fname, name, fname))
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines) + "\n")
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), "-I", "/usr/local/cuda/include", str(src),
+                    "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.split("\n")
+    got = {tuple(l.split()[:2]): int(l.split()[2]) for l in out if l.strip()}
+    for name, cls in structs.items():
+        assert got[(name, "sizeof")] == ctypes.sizeof(cls), name
+        for fname, _ in cls._fields_:
+            assert got[(name, fname)] == getattr(cls, fname).offset, (name, fname)
