@@ -955,8 +955,8 @@ int gemm_plain(uint32_t p, const ff_opts* opts, char tX, char tY, int64_t m, int
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct LqupWs {
-    size_t win, linv, uinv, out, pairs, gemm;
-    size_t total() const { return win + linv + uinv + out + pairs + gemm; }
+    size_t win, linv, uinv, out, pairs, gemm, obuf;
+    size_t total() const { return win + linv + uinv + out + pairs + gemm + obuf; }
 };
 
 int lqup_ws(uint32_t p, int64_t m, int64_t n, const ff_opts* opts, LqupWs* w) {
@@ -978,6 +978,8 @@ int lqup_ws(uint32_t p, int64_t m, int64_t n, const ff_opts* opts, LqupWs* w) {
         }
     }
     w->gemm = align256(g);
+    // out-of-place destination of the wide U_rest / G products (copied back)
+    w->obuf = align256(static_cast<size_t>(kH) * std::max<int64_t>(std::max<int64_t>(m, n), 1) * 4);
     return 0;
 }
 
@@ -1054,6 +1056,7 @@ int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t* A, int64_t lda, int64_
     const size_t out_stride = ((4 + 4 * kMaxSwaps) * 4 + 64) / 4;
     int64_t* dpairs = reinterpret_cast<int64_t*>(ws + w.win + w.linv + w.uinv + w.out);
     void* gws = ws + w.win + w.linv + w.uinv + w.out + w.pairs;
+    int32_t* obuf = reinterpret_cast<int32_t*>(ws + w.win + w.linv + w.uinv + w.out + w.pairs + w.gemm);
     std::vector<int32_t> hout(4 + 4 * kMaxSwaps);
     std::vector<int64_t> hp(4 * kMaxSwaps);
     const uint32_t neg1 = p - 1;
@@ -1289,9 +1292,30 @@ int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t* A, int64_t lda, int64_
             if (tl) cudaEventRecord(tl_ev.back()[5], st);
             if ((e = upd(r1, rn, c1, cw, K, 0))) return e;                      // the next window
             if (cudaEventRecord(ev_ready, st) != cudaSuccess) return fail_cuda();
-            if ((e = urest(cw, n))) return e;
+            // the wide U_rest and G products: out of place (a small-field product may not
+            // run in place without a grid barrier, which these grids are too large for),
+            // then copied back
+            if (i0 > 0 && cw < n) {
+                if ((e = gemm_plain(p, opts, 'N', 'N', kk, n - cw, kk, 1, Linv, kH, A + i0 * lda + cw, lda, 0, obuf, n - cw,
+                                    gws, st, 0, true)))
+                    return e;
+                if (cudaMemcpy2DAsync(A + i0 * lda + cw, lda * 4, obuf, (n - cw) * 4, (n - cw) * 4, kk,
+                                      cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+                    return fail_cuda();
+            } else if ((e = urest(cw, n))) {
+                return e;
+            }
             if ((e = upd(r1, rn, cw, n, K, 0))) return e;                        // the rest of its rows
-            if ((e = gmul(rn, m_active))) return e;
+            if (i0 > 0 && rn < m_active) {
+                if ((e = gemm_plain(p, opts, 'N', 'N', m_active - rn, kk, kk, 1, A + rn * lda + c, lda, Uinv, kH, 0, obuf, kk,
+                                    gws, st, 0, true)))
+                    return e;
+                if (cudaMemcpy2DAsync(A + rn * lda + c, lda * 4, obuf, kk * 4, kk * 4, m_active - rn,
+                                      cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+                    return fail_cuda();
+            } else if ((e = gmul(rn, m_active))) {
+                return e;
+            }
             if (npend == group || r1 + kH >= m_active || c1 + kH >= n) {
                 if ((e = upd(rn, m_active, c1, n, K, kReserve))) return e;      // flush the group
                 npend = 0;
