@@ -13,12 +13,20 @@
 // which is what short-K products (LQUP / ftrsm updates, K = 128 .. 1024) and
 // small matrices are bound by.
 //
-// CTA: 256 threads (8 warps) own a 64 x 64 tile of C; warp w computes rows
-// 16 (w & 3) .. +16 and columns 32 (w >> 2) .. +32 (four m16n8 tiles).  K is
-// staged 32 at a time in shared memory as canonical u32 residues (any int32
-// input is reduced on load, reading R3); fragments are built from them with
-// byte permutes.  The next K slice is loaded into registers while the current
-// one is multiplied (register double buffering).
+// Three kernels:
+//  * small_gemm_kernel: any int32 inputs (reduced on load, reading R3), any
+//    transposes; CTA of 256 threads (8 warps) owns a 64 x 64 tile of C, warp w
+//    computes rows 16 (w & 3) .. +16 and columns 32 (w >> 2) .. +32 (four
+//    m16n8 tiles); K staged 32 at a time in shared memory as canonical u32
+//    residues, the next slice loaded into registers meanwhile;
+//  * small_gemm_canon_kernel: canonical, non-transposed operands streamed raw by
+//    cp.async through a 4-deep ring (same tile);
+//  * small_gemm_wide_kernel<L>: the same for 2^16 <= p < 2^31 with L = 3 or 4
+//    bytes per residue (64 x 16 tiles for the L^2 accumulators).
+// Fragments are built from the u32 residues with byte permutes.  None of them
+// may run with C overlapping A or B unless launched with `alias` (the two
+// canonical kernels only): a cooperative launch whose grid barrier separates
+// every CTA's reads from the first write.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
