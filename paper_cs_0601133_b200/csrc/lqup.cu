@@ -1229,6 +1229,14 @@ int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t* A, int64_t lda, int64_
             continue;
         }
         buf ^= 1;
+        const bool generic = group > 1 && kk == kH && hr == kH && Wc == kH;
+        // A non-generic panel first brings the pending region up to date -- before its
+        // column swaps, which may reach beyond the 128-column window (widened window)
+        // and would otherwise exchange pending and up-to-date columns.
+        if (npend > 0 && !generic) {
+            if ((e = upd(i0 + kH, m_active, c + kH, n, c - pc0, 0))) return e;
+            npend = 0;
+        }
         const int ncol = hout[2], nrow = hout[3];
         // column swaps (window coordinates) on all rows outside the panel + bookkeeping
         if (ncol > 0) {
@@ -1260,11 +1268,6 @@ int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t* A, int64_t lda, int64_
         // reduction), not by K, so this divides the dominant cost by the group size.
         // Invariant while npend > 0: the pending panels (rows [pi0, i0), L columns
         // [pc0, c)) have not yet updated rows >= i0 + kH at columns >= c + kH.
-        const bool generic = group > 1 && kk == kH && hr == kH && Wc == kH;
-        if (npend > 0 && !generic) {                 // bring everything up to date first
-            if ((e = upd(i0 + kH, m_active, c + kH, n, c - pc0, 0))) return e;
-            npend = 0;
-        }
         if (generic) {
             // The next panel kernel needs only its own 128 x 128 window up to date, so the
             // chain that releases it is three 128-column products (U_rest's first window,
