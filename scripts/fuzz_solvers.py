@@ -16,7 +16,7 @@ from test_gpu_trsm import _tri  # noqa: E402
 
 torch.cuda.set_device(0)
 n_cases = int(sys.argv[1]) if len(sys.argv) > 1 else 40
-rng = np.random.default_rng(4242)
+rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 4242)
 bad = 0
 for case in range(n_cases):
     p = _random_prime(rng)
@@ -35,11 +35,20 @@ for case in range(n_cases):
         print("TRSM MISMATCH p=%d %s%s%s%s m=%d n=%d" % (p, side, uplo, trans, diag, m, n), flush=True)
 for case in range(n_cases):
     p = _random_prime(rng)
-    m, n = (int(x) for x in rng.integers(1, 900, size=2))
-    if rng.random() < 0.5:
+    m, n = (int(x) for x in rng.integers(1, int(os.environ.get("FUZZ_MAXN", 900)), size=2))
+    if rng.random() < 0.4:
         A = _low_rank(rng, p, m, n, int(rng.integers(0, min(m, n) + 1)))
     else:
         A = rng.integers(-2 ** 31, 2 ** 31, size=(m, n), dtype=np.int64).astype(np.int32)
+    if rng.random() < 0.5:                               # structure: zero / repeated rows and columns
+        for _ in range(int(rng.integers(1, 6))):
+            kind = int(rng.integers(0, 4))
+            i, j = int(rng.integers(0, m)), int(rng.integers(0, m))
+            c0 = int(rng.integers(0, n))
+            if kind == 0: A[i] = 0
+            elif kind == 1: A[i] = A[j]
+            elif kind == 2: A[:, c0:c0 + int(rng.integers(1, 200))] = 0
+            else: A[i:i + int(rng.integers(1, 200)), :] = A[j]
     dA = torch.from_numpy(np.ascontiguousarray(A)).cuda()
     Q, P, rk = ff.lqup(p, dA)
     torch.cuda.synchronize()

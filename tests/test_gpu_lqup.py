@@ -197,6 +197,11 @@ def test_lqup_random_sweep(env, seed):
             A = _low_rank(rng, p, m, n, r)
         else:
             A = rng.integers(-2 ** 31, 2 ** 31, size=(m, n), dtype=np.int64).astype(np.int32)
+        if rng.random() < 0.5:                       # structure: zero / repeated rows, zero columns
+            i, j, c0 = int(rng.integers(0, m)), int(rng.integers(0, m)), int(rng.integers(0, n))
+            A[i] = A[j]
+            A[:, c0:c0 + int(rng.integers(1, 150))] = 0
+            A[j] = 0
         F, Q, P, rk = _factor(torch, ff, p, A)
         want_r, want_d = oracle.rank_det(p, A)
         assert rk == want_r, (p, m, n)
