@@ -82,7 +82,8 @@ extern "C" {
  * a NULL pointer means all defaults. */
 typedef struct ff_opts {
     int32_t winograd;       /* 0 auto, 1 one Winograd level (Table 2; needs even
-                               m, n, k, else FF_ERR_OPTS), -1 never */
+                               m, n, k with m, n >= 512 and k >= 256, else FF_ERR_OPTS),
+                               -1 never */
     int32_t scheme;         /* FF_SCHEME_*; AUTO picks the fewest int8 products: limbs
                                (S on ties) unless CRT needs clearly fewer */
     int64_t kb_override;    /* 0: planner k-block; else k-block length in elements,
