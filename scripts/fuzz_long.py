@@ -19,7 +19,7 @@ for block in range(100, 100 + nblocks):
     rng = np.random.default_rng(20261019 + block)
     for case in range(40):
         p = _random_prime(rng)
-        m, n, k = (int(x) for x in rng.choice([1, 2, 7, 31, 64, 127, 128, 129, 200, 255, 256, 300, 383, 513, 1000], size=3))
+        m, n, k = (int(x) for x in rng.choice([1, 2, 7, 31, 64, 127, 128, 129, 200, 255, 256, 300, 383, 513, 1000] + ([1024, 1536, 2047, 2304] if os.environ.get("FUZZ_BIG") else []), size=3))
         tA, tB = str(rng.choice(["N", "T"])), str(rng.choice(["N", "T"]))
         opts = {}
         r = rng.random()
