@@ -196,6 +196,11 @@ int run(const Plan& pl, char transA, char transB, int64_t m, int64_t n, int64_t 
         prefer_small_canon(m, n, k)) {
         const int e = launch_gemm_small_canon(pl, m, n, k, A, lda, B, ldb, C, ldc, !c_disjoint, st);
         if (e != FF_ERR_INTERNAL) return e;
+    } else if (pl.all_auto && small_stream_ok(pl, is_t(transA), is_t(transB), m, n, k, A, lda, B, ldb) &&
+               prefer_small_canon(m, n, k)) {
+        // raw inputs, not transposed: the same streaming kernel reduces each slice in shared memory
+        const int e = launch_gemm_small_canon(pl, m, n, k, A, lda, B, ldb, C, ldc, !c_disjoint, st, true);
+        if (e != FF_ERR_INTERNAL) return e;
     } else if (pl.all_auto && small_wide_ok(pl, is_t(transA), is_t(transB), m, n, k, A, lda, B, ldb) &&
                prefer_small_wide(m, n, k)) {
         const int e = launch_gemm_small_wide(pl, m, n, k, A, lda, B, ldb, C, ldc, !c_disjoint, st);

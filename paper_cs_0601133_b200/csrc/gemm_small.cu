@@ -54,6 +54,7 @@ struct SmallArgs {
     int32_t m, n, k;
     int32_t tA, tB;                // 1: op(X) = X^T
     int32_t alias;                 // 1: C overlaps A or B: grid-wide barrier between reads and writes
+    int32_t reduce;                // small_gemm_canon_kernel: 1: A, B raw int32, reduced in shared memory
 };
 
 __device__ __forceinline__ void imma(int (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
@@ -217,6 +218,22 @@ __global__ void __launch_bounds__(kSThreads) small_gemm_canon_kernel(const __gri
     for (int s = 0; s < kCStages - 1; ++s) issue(s);
     for (int sl = 0; sl < nsl; ++sl) {
         asm volatile("cp.async.wait_group %0;" ::"n"(kCStages - 2) : "memory");
+        if (a.reduce) {                                  // raw int32 inputs: this thread's own chunks of
+            const int st = sl % kCStages;                // slice sl have landed -> residues (R3)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int e = tid + j * kSThreads;
+                uint4* qa = reinterpret_cast<uint4*>(As + (st * kSM + (e >> 3)) * kCApitch + (e & 7) * 4);
+                uint4* qb = reinterpret_cast<uint4*>(Bs + (st * kSK + (e >> 4)) * kCBpitch + (e & 15) * 4);
+                uint4 va = *qa, vb = *qb;
+                va.x = residue_i32(static_cast<int32_t>(va.x), a.M); va.y = residue_i32(static_cast<int32_t>(va.y), a.M);
+                va.z = residue_i32(static_cast<int32_t>(va.z), a.M); va.w = residue_i32(static_cast<int32_t>(va.w), a.M);
+                vb.x = residue_i32(static_cast<int32_t>(vb.x), a.M); vb.y = residue_i32(static_cast<int32_t>(vb.y), a.M);
+                vb.z = residue_i32(static_cast<int32_t>(vb.z), a.M); vb.w = residue_i32(static_cast<int32_t>(vb.w), a.M);
+                *qa = va;
+                *qb = vb;
+            }
+        }
         __syncthreads();                                 // slice sl visible; slice sl-1's stage is free
         issue(sl + kCStages - 1);
         const uint32_t* A_ = As + (sl % kCStages) * kSM * kCApitch;
@@ -429,6 +446,7 @@ int launch_gemm_small_wide(const Plan& pl, int64_t m, int64_t n, int64_t k, cons
     const dim3 grid(static_cast<unsigned>((n + kWN - 1) / kWN), static_cast<unsigned>((m + kSM - 1) / kSM));
     if (grid.y > 65535u) return FF_ERR_INTERNAL;
     a.alias = alias ? 1 : 0;
+    a.reduce = 0;
     const void* fn = pl.mp.p < (1u << 24) ? reinterpret_cast<const void*>(small_gemm_wide_kernel<3>)
                                           : reinterpret_cast<const void*>(small_gemm_wide_kernel<4>);
     return launch_small(fn, grid, kWSmem, a, alias, st);
@@ -442,7 +460,8 @@ bool small_canon_ok(const Plan& pl, bool tA, bool tB, int64_t m, int64_t n, int6
 }
 
 int launch_gemm_small_canon(const Plan& pl, int64_t m, int64_t n, int64_t k, const int32_t* A, int64_t lda,
-                            const int32_t* B, int64_t ldb, int32_t* C, int64_t ldc, bool alias, cudaStream_t st) {
+                            const int32_t* B, int64_t ldb, int32_t* C, int64_t ldc, bool alias, cudaStream_t st,
+                            bool reduce) {
     SmallArgs a;
     a.M = pl.mp;
     a.mu64 = static_cast<unsigned long long>((static_cast<unsigned __int128>(1) << 64) / pl.mp.p);
@@ -453,7 +472,15 @@ int launch_gemm_small_canon(const Plan& pl, int64_t m, int64_t n, int64_t k, con
     const dim3 grid(static_cast<unsigned>((n + kSN - 1) / kSN), static_cast<unsigned>((m + kSM - 1) / kSM));
     if (grid.y > 65535u) return FF_ERR_INTERNAL;
     a.alias = alias ? 1 : 0;
+    a.reduce = reduce ? 1 : 0;
     return launch_small(reinterpret_cast<const void*>(small_gemm_canon_kernel), grid, kCSmem, a, alias, st);
+}
+
+bool small_stream_ok(const Plan& pl, bool tA, bool tB, int64_t m, int64_t n, int64_t k, const int32_t* A, int64_t lda,
+                     const int32_t* B, int64_t ldb) {
+    return !tA && !tB && pl.mp.p < 65536u && k > 0 && k <= 32768 && m > 0 && n > 0 && m < (1ll << 30) &&
+           n < (1ll << 30) && (lda % 4) == 0 && (ldb % 4) == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0 &&
+           (reinterpret_cast<uintptr_t>(B) & 15) == 0;
 }
 
 bool small_path_ok(const Plan& pl, int64_t m, int64_t n, int64_t k) {
@@ -471,6 +498,7 @@ int launch_gemm_small(const Plan& pl, bool tA, bool tB, int64_t m, int64_t n, in
     a.m = static_cast<int32_t>(m); a.n = static_cast<int32_t>(n); a.k = static_cast<int32_t>(k);
     a.tA = tA ? 1 : 0; a.tB = tB ? 1 : 0;
     a.alias = 0;
+    a.reduce = 0;
     const dim3 grid(static_cast<unsigned>((n + kSN - 1) / kSN), static_cast<unsigned>((m + kSM - 1) / kSM));
     if (grid.y > 65535u) return FF_ERR_INTERNAL;
     small_gemm_kernel<<<grid, kSThreads, 0, st>>>(a);

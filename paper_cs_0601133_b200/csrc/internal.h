@@ -98,8 +98,12 @@ bool small_canon_ok(const Plan& pl, bool tA, bool tB, int64_t m, int64_t n, int6
                     const int32_t* B, int64_t ldb);
 // alias: C overlaps A or B (in-place products): a cooperative launch with a grid barrier between the
 // reads and the writes; FF_ERR_INTERNAL if the grid cannot be co-resident
+// reduce: A, B are raw int32 (any value), reduced per slice in shared memory (small_stream_ok)
 int launch_gemm_small_canon(const Plan& pl, int64_t m, int64_t n, int64_t k, const int32_t* A, int64_t lda,
-                            const int32_t* B, int64_t ldb, int32_t* C, int64_t ldc, bool alias, cudaStream_t st);
+                            const int32_t* B, int64_t ldb, int32_t* C, int64_t ldc, bool alias, cudaStream_t st,
+                            bool reduce = false);
+bool small_stream_ok(const Plan& pl, bool tA, bool tB, int64_t m, int64_t n, int64_t k, const int32_t* A, int64_t lda,
+                     const int32_t* B, int64_t ldb);
 bool small_wide_ok(const Plan& pl, bool tA, bool tB, int64_t m, int64_t n, int64_t k, const int32_t* A, int64_t lda,
                    const int32_t* B, int64_t ldb);
 int launch_gemm_small_wide(const Plan& pl, int64_t m, int64_t n, int64_t k, const int32_t* A, int64_t lda,
