@@ -106,7 +106,9 @@ typedef struct ff_opts {
                                canonical residue in [0, p) (C may still be any int32): for
                                p < 2^16 short-K products may then stream A and B raw
                                (DESIGN.md §4.10).  Results are undefined if violated. */
-    int32_t reserved[2];
+    int32_t small_path;     /* small-field latency kernels: 0 by the size
+                               rule, 1 whenever they apply, -1 never (results are identical) */
+    int32_t reserved[1];
 } ff_opts;
 
 /* The plan the library derives from (p, k, opts): host-only, no GPU needed. */
@@ -268,6 +270,32 @@ int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t *A, int64_t lda, int64_
  * -5 lda, -6 rank, -7 det requested for m != n. */
 int ff_rank_det(uint32_t p, int64_t m, int64_t n, const int32_t *A, int64_t lda, int64_t *rank,
                 uint32_t *det);
+
+/* ---- kernel timing for benchmarks (host) -----------------------------------
+ * ff_prof_start(capacity): from now on every GEMM-kernel launch of the library
+ * (tcgen05 limb/CRT, small-field, fp64 -- on the current device, any stream) is
+ * bracketed by two CUDA events recorded on that launch's own stream, for the
+ * first `capacity` launches, and every kernel launch of the fgemm path
+ * (encoders, pre-additions, GEMMs, scaling) is counted.  Returns 0, -1
+ * (capacity outside [0, 2^20]) or FF_ERR_CUDA.
+ * ff_prof_stop(gemm_ms, cap, launches): stops recording, waits for the
+ * recorded events, writes min(cap, recorded) per-launch durations in ms to
+ * gemm_ms (host, may be NULL), stores the number of kernel launches counted
+ * since ff_prof_start in *launches (may be NULL) and returns the number of
+ * GEMM launches recorded (or -FF_ERR_CUDA).  Process-wide state: not for
+ * concurrent use by several host threads. */
+int ff_prof_start(int32_t capacity);
+int ff_prof_stop(float *gemm_ms, int32_t cap, int64_t *launches);
+
+/* The int8 tensor-core ceiling of the current device, measured: the hot
+ * kernel's instruction (tcgen05.mma.cta_group::2.kind::i8, 256 x 256 x 32,
+ * s32 in TMEM) issued back to back from SMEM-resident operands by every CTA
+ * pair, no data movement, no epilogue; `iters` x 4 MMAs per pair, best of 3
+ * timed launches on the legacy default stream (synchronous).  *tops receives
+ * int8 tera-ops/s (2 per multiply-add).  The analogue of the paper's dgemm
+ * yardstick for fgemm.  Codes: -1 iters <= 0 or tops
+ * NULL; FF_ERR_ARCH / FF_ERR_CUDA. */
+int ff_mma_ceiling(int32_t iters, double *tops);
 
 /* ---- synthetic inputs (device twin of ffgen/__init__.py) -----------------
  * X[r*ld + c] = v[index0 + r*cols + c] for r < rows, c < cols, where v is the

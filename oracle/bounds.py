@@ -103,3 +103,35 @@ def t_update(p: int, gamma: int = 53) -> int:
     """Largest t with (t+1)(p-1)^2 < 2^gamma, capped at 2^31 - 1 - p."""
     t = (2 ** gamma - 1) // ((p - 1) ** 2) - 1
     return min(t, 2 ** 31 - 1 - p)
+
+
+# ---------------------------------------------------------------- Thm 3.1 / Cor 3.4
+
+def winograd_v(M: int, m: int, l: int) -> int:
+    """v_l of Appendix A.1: v_l = (1+3^l)/2 M + (1-3^l)/2 m
+    (both halves are integers since 3^l is odd)."""
+    return (1 + 3 ** l) // 2 * M + (1 - 3 ** l) // 2 * m
+
+
+def thm31_bound(MA: int, mA: int, MB: int, mB: int, k: int, l: int) -> int:
+    """Theorem 3.1: every intermediate value z of A x B with
+    l >= 1 recursive Winograd levels has |z| <= v_l^A v_l^B floor(k / 2^l)."""
+    return winograd_v(MA, mA, l) * winograd_v(MB, mB, l) * (k // 2 ** l)
+
+
+def k_winograd_exact(p: int, gamma: int, l: int, balanced: bool = False) -> int:
+    """The exact form of Corollary 3.4 (reading R21): the smallest k for
+    which Theorem 3.1's bound reaches 2^gamma, so l levels are safe iff k < it.
+
+    With X = 2^gamma / v_l^2 (= the paper's 2^(gamma+2)/((1+3^l)(p-1))^2, or
+    2^(gamma+2)/(3^l (p-1))^2 balanced), floor(k/2^l) v_l^2 < 2^gamma holds iff
+    floor(k/2^l) < X iff k < ceil(X) 2^l.  The paper's (X + 1) 2^l (floored)
+    agrees only when 0 < frac(X) 2^l < 1; otherwise it admits up to 2^l values
+    of k whose bound reaches 2^gamma (p = 65521, l = 1, balanced: 1865047 by
+    the printed formula vs 1865046)."""
+    if balanced:
+        h = (p - 1) // 2 if p % 2 else p // 2
+        v = winograd_v(h, -h, l)
+    else:
+        v = winograd_v(p - 1, 0, l)
+    return -(-(2 ** gamma) // (v * v)) * 2 ** l

@@ -85,3 +85,94 @@ def schedule_table2(alpha, A, B, beta, C, step16_operand="A22"):
     top = [r1 + r2 for r1, r2 in zip(C11, C12)]
     bot = [r1 + r2 for r1, r2 in zip(C21, C22)]
     return top + bot
+
+
+# ---------------------------------------------------------------- Thm 3.1 traced
+
+def witness(l: int, MA: int, mA: int, MB: int, mB: int):
+    """Appendix A.6: the square matrices A_l, B_l of order
+    2^l on which l recursive Winograd levels reach Theorem 3.1's bound:
+        A_1 = [[mA, 0], [MA, MA]],  B_1 = [[MB, mB], [0, MB]],
+        A_{l+1} = [[conj(A_l), 0], [A_l, A_l]],  B_{l+1} = [[B_l, conj(B_l)], [0, B_l]],
+    conj(x) = M + m - x."""
+    A = [[mA, 0], [MA, MA]]
+    B = [[MB, mB], [0, MB]]
+    for _ in range(l - 1):
+        n = len(A)
+        Ab = [[MA + mA - x for x in r] for r in A]
+        Bb = [[MB + mB - x for x in r] for r in B]
+        A = [Ab[i] + [0] * n for i in range(n)] + [A[i] + A[i] for i in range(n)]
+        B = [B[i] + Bb[i] for i in range(n)] + [[0] * n + B[i] for i in range(n)]
+    return A, B
+
+
+def _sub(X, Y):
+    return _add(X, Y, -1)
+
+
+def winograd_traced(A, B, l: int):
+    """A x B over Z with l recursive levels of Winograd's algorithm in the form of
+    Appendix A.2, classical products at the leaves.
+
+    Returns (product, max |z|) where z runs over EVERY intermediate value: the
+    pre-additions S1..S4 / T1..T4 (and the partial sums inside them), the seven
+    recursive products P1..P7, the post-additions U1..U7, and the partial sums
+    of every leaf dot product (in order of the inner index).  No reduction
+    anywhere: this is the quantity Theorem 3.1 bounds.  Dimensions of A (m x k)
+    and B (k x n) must be divisible by 2^l."""
+    peak = [0]
+
+    def note(X):
+        for r in X:
+            for x in r:
+                if abs(x) > peak[0]:
+                    peak[0] = abs(x)
+        return X
+
+    def classic(X, Y):
+        k = len(Y)
+        out = []
+        for i in range(len(X)):
+            row = []
+            for j in range(len(Y[0])):
+                s = 0
+                for t in range(k):
+                    s += X[i][t] * Y[t][j]
+                    if abs(s) > peak[0]:
+                        peak[0] = abs(s)
+                row.append(s)
+            out.append(row)
+        return out
+
+    def rec(X, Y, j):
+        if j == 0:
+            return classic(X, Y)
+        A11, A12, A21, A22 = _quad(X, 0, 0), _quad(X, 0, 1), _quad(X, 1, 0), _quad(X, 1, 1)
+        B11, B12, B21, B22 = _quad(Y, 0, 0), _quad(Y, 0, 1), _quad(Y, 1, 0), _quad(Y, 1, 1)
+        S1 = note(_add(A21, A22))
+        S2 = note(_sub(S1, A11))
+        S3 = note(_sub(A11, A21))
+        S4 = note(_sub(A12, S2))
+        T1 = note(_sub(B12, B11))
+        T2 = note(_sub(B22, T1))
+        T3 = note(_sub(B22, B12))
+        T4 = note(_sub(T2, B21))
+        P1 = note(rec(A11, B11, j - 1))
+        P2 = note(rec(A12, B21, j - 1))
+        P3 = note(rec(S4, B22, j - 1))
+        P4 = note(rec(A22, T4, j - 1))
+        P5 = note(rec(S1, T1, j - 1))
+        P6 = note(rec(S2, T2, j - 1))
+        P7 = note(rec(S3, T3, j - 1))
+        U1 = note(_add(P1, P2))
+        U2 = note(_add(P1, P6))
+        U3 = note(_add(U2, P7))
+        U4 = note(_add(U2, P5))
+        U5 = note(_add(U4, P3))
+        U6 = note(_sub(U3, P4))
+        U7 = note(_add(U3, P5))
+        top = [r1 + r2 for r1, r2 in zip(U1, U5)]
+        bot = [r1 + r2 for r1, r2 in zip(U6, U7)]
+        return top + bot
+
+    return rec(A, B, l), peak[0]

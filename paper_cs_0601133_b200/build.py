@@ -41,30 +41,43 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def _compile(src, obj, verbose):
+    cmd = [NVCC] + NVCC_FLAGS + ["-c", src, "-o", obj]
+    if src.endswith(".cpp"):
+        cmd = ["g++", "-std=c++17", "-O2", "-fPIC", "-Wall", "-I", os.path.join(ROOT, "include"),
+               "-I", "/usr/local/cuda/include", "-c", src, "-o", obj]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("nvcc failed on %s" % src)
+    if verbose:
+        sys.stderr.write(r.stderr)
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every source in parallel (objects kept in lib/obj/, rebuilt when a
+    source or any header is newer) and link lib/libffgemm.so."""
     if not force and not _stale():
         return LIB
-    os.makedirs(LIBDIR, exist_ok=True)
-    objs = []
+    from concurrent.futures import ThreadPoolExecutor
+    objdir = os.path.join(LIBDIR, "obj")
+    os.makedirs(objdir, exist_ok=True)
+    hdrs = glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh"))
+    hdrs.append(os.path.join(ROOT, "include", "ffgemm.h"))
+    newest_hdr = max(os.path.getmtime(h) for h in hdrs)
+    jobs, objs = [], []
     for src in sources():
-        obj = os.path.join(LIBDIR, os.path.basename(src) + ".o")
-        cmd = [NVCC] + NVCC_FLAGS + ["-c", src, "-o", obj]
-        if src.endswith(".cpp"):
-            cmd = ["g++", "-std=c++17", "-O2", "-fPIC", "-Wall", "-I", os.path.join(ROOT, "include"), "-I", "/usr/local/cuda/include",
-                   "-c", src, "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        if r.returncode != 0:
-            sys.stderr.write(r.stdout + r.stderr)
-            raise RuntimeError("nvcc failed on %s" % src)
-        if verbose:
-            sys.stderr.write(r.stderr)
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
         objs.append(obj)
+        if force or not os.path.exists(obj) or os.path.getmtime(obj) < max(os.path.getmtime(src), newest_hdr):
+            jobs.append((src, obj))
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 4))) as ex:
+        for f in [ex.submit(_compile, s, o, verbose) for s, o in jobs]:
+            f.result()
     tmp = LIB + ".tmp%d" % os.getpid()
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp] + objs
     subprocess.check_call(cmd)
     os.replace(tmp, LIB)
-    for o in objs:
-        os.remove(o)
     return LIB
 
 

@@ -6,7 +6,10 @@
 #include <cstdint>
 #include <cstring>
 #include <algorithm>
+#include <atomic>
+#include <cstdlib>
 #include <mutex>
+#include <set>
 #include <vector>
 
 #include "internal.h"
@@ -146,9 +149,8 @@ namespace {
 // The whole path on device pointers.
 // Small-field latency path (gemm_small.cu) for short K and small problems:
 // FF_SMALL=0 never, FF_SMALL=1 whenever valid (experiments); default by size.
-bool prefer_small(int64_t m, int64_t n, int64_t k) {
-    const char* env = getenv("FF_SMALL");
-    const int mode = env ? atoi(env) : -1;
+bool prefer_small(const Plan& pl, int64_t m, int64_t n, int64_t k) {
+    const int mode = pl.small_mode;
     if (mode >= 0) return mode > 0;
     // measured (p = 65521, alpha = -1, beta = 1): 128^3 19.9 vs 31.5 us, 128 x 8192 x 128
     // 21.9 vs 33.3 us; but 512^3 40.8 vs 36.4 us, 128 x 8192 x 1024 98 vs 51 us and
@@ -157,9 +159,8 @@ bool prefer_small(int64_t m, int64_t n, int64_t k) {
 }
 
 // The cp.async variant for canonical operands (internal callers): FF_SMALL as above.
-bool prefer_small_canon(int64_t m, int64_t n, int64_t k) {
-    const char* env = getenv("FF_SMALL");
-    const int mode = env ? atoi(env) : -1;
+bool prefer_small_canon(const Plan& pl, int64_t m, int64_t n, int64_t k) {
+    const int mode = pl.small_mode;
     if (mode >= 0) return mode > 0;
     // measured against the tcgen05 path (p = 65521, alpha = -1, beta = 1): 512^3 21 vs
     // 36 us, 128 x 8192 x 128 20 vs 33 us, 128 x 8192 x 1024 51 vs 51 us, 1024^3
@@ -168,9 +169,8 @@ bool prefer_small_canon(int64_t m, int64_t n, int64_t k) {
 }
 
 // The same for 2^16 <= p < 2^31 (3-4 bytes per residue): FF_SMALL as above.
-bool prefer_small_wide(int64_t m, int64_t n, int64_t k) {
-    const char* env = getenv("FF_SMALL");
-    const int mode = env ? atoi(env) : -1;
+bool prefer_small_wide(const Plan& pl, int64_t m, int64_t n, int64_t k) {
+    const int mode = pl.small_mode;
     if (mode >= 0) return mode > 0;
     return k <= 1024 && m * n <= (int64_t{1} << 21) && m * n * k < (int64_t{1} << 29);
 }
@@ -193,20 +193,20 @@ int run(const Plan& pl, char transA, char transB, int64_t m, int64_t n, int64_t 
                             (sc.second <= sb.first || sb.second <= sc.first);
     // (the canonical-input variants handle overlap with a grid barrier instead)
     if (pl.all_auto && small_canon_ok(pl, is_t(transA), is_t(transB), m, n, k, A, lda, B, ldb) &&
-        prefer_small_canon(m, n, k)) {
+        prefer_small_canon(pl, m, n, k)) {
         const int e = launch_gemm_small_canon(pl, m, n, k, A, lda, B, ldb, C, ldc, !c_disjoint, st);
         if (e != FF_ERR_INTERNAL) return e;
     } else if (pl.all_auto && small_stream_ok(pl, is_t(transA), is_t(transB), m, n, k, A, lda, B, ldb) &&
-               prefer_small_canon(m, n, k)) {
+               prefer_small_canon(pl, m, n, k)) {
         // raw inputs, not transposed: the same streaming kernel reduces each slice in shared memory
         const int e = launch_gemm_small_canon(pl, m, n, k, A, lda, B, ldb, C, ldc, !c_disjoint, st, true);
         if (e != FF_ERR_INTERNAL) return e;
     } else if (pl.all_auto && small_wide_ok(pl, is_t(transA), is_t(transB), m, n, k, A, lda, B, ldb) &&
-               prefer_small_wide(m, n, k)) {
+               prefer_small_wide(pl, m, n, k)) {
         const int e = launch_gemm_small_wide(pl, m, n, k, A, lda, B, ldb, C, ldc, !c_disjoint, st);
         if (e != FF_ERR_INTERNAL) return e;
     }
-    if (pl.all_auto && c_disjoint && small_path_ok(pl, m, n, k) && prefer_small(m, n, k))
+    if (pl.all_auto && c_disjoint && small_path_ok(pl, m, n, k) && prefer_small(pl, m, n, k))
         return launch_gemm_small(pl, is_t(transA), is_t(transB), m, n, k, A, lda, B, ldb, C, ldc, st);
     int8_t* al = static_cast<int8_t*>(ws);
     int8_t* bl = al + align256(static_cast<size_t>(pl.info.L) * m * pl.info.k_pad);
@@ -226,6 +226,78 @@ int gemm_dev(const Plan& pl, char transA, char transB, int64_t m, int64_t n, int
 }
 
 int check_device() { return arch_check(cur_dev()); }
+
+cudaError_t set_smem_attr(const void* fn, int bytes) {
+    static std::mutex mu;
+    static std::set<std::pair<int, const void*>> done;
+    const int dev = cur_dev();
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.count({dev, fn})) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done.insert({dev, fn});
+    return e;
+}
+
+namespace {
+struct Prof {
+    std::mutex mu;
+    std::atomic<bool> on{false};
+    std::atomic<long long> launches{0};
+    int dev = -1;
+    std::vector<cudaEvent_t> ev;   // 2 per GEMM launch
+    int used = 0, cap = 0;
+};
+Prof g_prof;
+}  // namespace
+
+void note_launch(int n) {
+    if (g_prof.on.load(std::memory_order_relaxed)) g_prof.launches.fetch_add(n, std::memory_order_relaxed);
+}
+
+void prof_gemm_begin(cudaStream_t st) {
+    if (!g_prof.on.load(std::memory_order_relaxed)) return;
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    if (g_prof.used >= g_prof.cap || cur_dev() != g_prof.dev) return;
+    cudaEventRecord(g_prof.ev[2 * g_prof.used], st);
+}
+
+void prof_gemm_end(cudaStream_t st) {
+    if (!g_prof.on.load(std::memory_order_relaxed)) return;
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    if (g_prof.used >= g_prof.cap || cur_dev() != g_prof.dev) return;
+    cudaEventRecord(g_prof.ev[2 * g_prof.used + 1], st);
+    ++g_prof.used;
+}
+
+namespace {
+int env_int(const char* name, int dflt) {
+    const char* e = getenv(name);
+    return e ? atoi(e) : dflt;
+}
+}  // namespace
+
+const Knobs& knobs() {
+    static const Knobs k = [] {
+        Knobs v;
+        v.small = env_int("FF_SMALL", -1);
+        v.pdl = getenv("FF_NOPDL") == nullptr;
+        v.trace = getenv("FF_TRACE") != nullptr;
+        v.raster = env_int("FF_RASTER", 0);
+        v.hints = env_int("FF_HINTS", -1);
+        v.korder = env_int("FF_KORDER", 0);
+        v.kbloc = getenv("FF_KBLOC") ? atoll(getenv("FF_KBLOC")) : 0;
+        v.enc_notma = getenv("FF_ENC_NOTMA") != nullptr;
+#ifdef FF_EXPERIMENTS
+        v.throttle = env_int("FF_THROTTLE", 0);
+        v.die_aware = getenv("FF_DIE_AWARE") != nullptr && getenv("FF_NO_DIE_AWARE") == nullptr;
+#else
+        v.throttle = 0;
+        v.die_aware = false;
+#endif
+        return v;
+    }();
+    return k;
+}
 
 int num_sms() {
     const int d = cur_dev();
@@ -562,6 +634,41 @@ int ff_fill_uniform(int32_t* X, int64_t rows, int64_t cols, int64_t ld, uint32_t
     if (e) return e;
     return cuda_rc(launch_fill_uniform(X, rows, cols, ld, p, seed, stream_id, index0,
                                        static_cast<cudaStream_t>(stream)));
+}
+
+int ff_prof_start(int32_t capacity) {
+    if (capacity < 0 || capacity > (1 << 20)) return -1;
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    const int dev = cur_dev();
+    if (g_prof.dev != dev) {
+        for (cudaEvent_t e : g_prof.ev) cudaEventDestroy(e);
+        g_prof.ev.clear();
+        g_prof.dev = dev;
+    }
+    while (static_cast<int>(g_prof.ev.size()) < 2 * capacity) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return FF_ERR_CUDA;
+        g_prof.ev.push_back(e);
+    }
+    g_prof.cap = capacity;
+    g_prof.used = 0;
+    g_prof.launches.store(0);
+    g_prof.on.store(true);
+    return 0;
+}
+
+int ff_prof_stop(float* gemm_ms, int32_t cap, int64_t* launches) {
+    g_prof.on.store(false);
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    if (launches) *launches = g_prof.launches.load();
+    const int n = g_prof.used;
+    for (int i = 0; i < n && i < cap && gemm_ms; ++i) {
+        if (cudaEventSynchronize(g_prof.ev[2 * i + 1]) != cudaSuccess ||
+            cudaEventElapsedTime(&gemm_ms[i], g_prof.ev[2 * i], g_prof.ev[2 * i + 1]) != cudaSuccess)
+            return -FF_ERR_CUDA;
+    }
+    g_prof.used = 0;
+    return n;
 }
 
 }  // extern "C"

@@ -67,7 +67,7 @@ void calibrate(int dev, DieInfo& D) {
     D.done = true;
     // Off unless requested: measured 4-6% slower than the plain raster on c4/c5
     // (DESIGN.md §4.8), kept as an experiment.
-    if (!getenv("FF_DIE_AWARE") || getenv("FF_NO_DIE_AWARE")) return;
+    if (!knobs().die_aware) return;
     const int nsm = num_sms();
     std::vector<int> h(512 * 64 * kGran);
     for (int g = 0; g < kGran; ++g)

@@ -561,25 +561,22 @@ void launch_encode_t(const Plan& pl, int kmajor_src, int64_t rows, int64_t k, in
         if (gy > 65535) gy = 65535;
         if (gy < 1) gy = 1;
         const int vec_ok = ((ldx % 4) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0) ? 1 : 0;
+        note_launch();
         encode_direct_kernel<L, SCHEME><<<dim3(gx, static_cast<unsigned>(gy)), 256, 0, st>>>(
             pl.mp, rows, k, k_pad, X, ldx, limbs, vec_ok);
     } else {
         const int64_t tiles = ((rows + kTR - 1) / kTR) * ((k_pad + kTK - 1) / kTK);
         CUtensorMap map;
-        static const bool no_tma = getenv("FF_ENC_NOTMA") != nullptr;    // experiment: the LSU-load version
-        if (!no_tma && make_src_map(&map, X, rows, k, ldx)) {
-            static bool attr = false;
-            if (!attr) {
-                cudaFuncSetAttribute(encode_trans_tma_kernel<L, SCHEME>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     kTmaSmem);
-                attr = true;
-            }
+        if (!knobs().enc_notma && make_src_map(&map, X, rows, k, ldx)) {   // FF_ENC_NOTMA: the LSU-load version
+            set_smem_attr(reinterpret_cast<const void*>(encode_trans_tma_kernel<L, SCHEME>), kTmaSmem);
             const int64_t cap = (int64_t)num_sms() * 2;
+            note_launch();
             encode_trans_tma_kernel<L, SCHEME><<<static_cast<int>(tiles < cap ? tiles : cap), 256, kTmaSmem, st>>>(
                 map, pl.mp, rows, k_pad, limbs);
             return;
         }
         const int64_t cap = (int64_t)num_sms() * 8;
+        note_launch();
         encode_trans_kernel<L, SCHEME><<<static_cast<int>(tiles < cap ? tiles : cap), 256, 0, st>>>(
             pl.mp, rows, k, k_pad, X, ldx, limbs);
     }
@@ -601,25 +598,23 @@ cudaError_t launch_encode(const Plan& pl, int kmajor_src, int64_t rows, int64_t 
             if (gy > 65535) gy = 65535;
             if (gy < 1) gy = 1;
             const int vec_ok = ((ldx % 4) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0) ? 1 : 0;
+            note_launch();
             encode_crt_direct_kernel<<<dim3(gx, static_cast<unsigned>(gy)), 256, 0, st>>>(
                 pl.mp, pl.cc, rows, k, k_pad, X, ldx, limbs, vec_ok);
         } else {
             const int64_t tiles = ((rows + kTR - 1) / kTR) * ((k_pad + kTK - 1) / kTK);
             CUtensorMap map;
-            static const bool no_tma = getenv("FF_ENC_NOTMA") != nullptr;
-            if (!no_tma && make_src_map(&map, X, rows, k, ldx)) {
-                static bool attr = false;
-                if (!attr) {
-                    cudaFuncSetAttribute(encode_crt_trans_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         kCrtTmaSmem);
-                    attr = true;
-                }
+            if (!knobs().enc_notma && make_src_map(&map, X, rows, k, ldx)) {
+                const cudaError_t ea = set_smem_attr(reinterpret_cast<const void*>(encode_crt_trans_tma_kernel), kCrtTmaSmem);
+                if (ea != cudaSuccess) return ea;
                 const int64_t capt = (int64_t)num_sms() * 2;
+                note_launch();
                 encode_crt_trans_tma_kernel<<<static_cast<int>(tiles < capt ? tiles : capt), 256, kCrtTmaSmem, st>>>(
                     map, pl.mp, pl.cc, rows, k_pad, limbs);
                 return cudaGetLastError();
             }
             const int64_t cap = (int64_t)num_sms() * 8;
+            note_launch();
             encode_crt_trans_kernel<<<static_cast<int>(tiles < cap ? tiles : cap), 256, 0, st>>>(
                 pl.mp, pl.cc, rows, k, k_pad, X, ldx, limbs);
         }
@@ -649,6 +644,7 @@ cudaError_t launch_scale_c(const ModP& mp, int64_t m, int64_t n, int32_t* C, int
     if (gy > 65535) gy = 65535;
     if (gy < 1) gy = 1;
     const int vec_ok = ((ldc % 4) == 0 && (reinterpret_cast<uintptr_t>(C) & 15) == 0) ? 1 : 0;
+    note_launch();
     scale_c_kernel<<<dim3(gx, static_cast<unsigned>(gy)), 256, 0, st>>>(mp, m, n, C, ldc, vec_ok);
     return cudaGetLastError();
 }

@@ -398,17 +398,14 @@ __global__ void __launch_bounds__(kSThreads) small_gemm_wide_kernel(const __grid
 // grid barrier; FF_ERR_INTERNAL if the grid cannot be co-resident (the caller
 // then takes the tcgen05 path).
 int launch_small(const void* fn, dim3 grid, int smem, SmallArgs& a, bool alias, cudaStream_t st) {
-    static const void* done[4] = {nullptr, nullptr, nullptr, nullptr};   // attribute set once per kernel
-    bool seen = false;
-    for (const void* d : done) seen = seen || d == fn;
-    if (!seen) {
-        if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return FF_ERR_CUDA;
-        for (auto& d : done)
-            if (!d) { d = fn; break; }
-    }
+    if (set_smem_attr(fn, smem) != cudaSuccess) return FF_ERR_CUDA;
     void* args[] = {&a};
     if (!alias) {
-        if (cudaLaunchKernel(fn, grid, dim3(kSThreads), args, static_cast<size_t>(smem), st) != cudaSuccess) {
+        note_launch();
+        prof_gemm_begin(st);
+        const cudaError_t le = cudaLaunchKernel(fn, grid, dim3(kSThreads), args, static_cast<size_t>(smem), st);
+        prof_gemm_end(st);
+        if (le != cudaSuccess) {
             cudaGetLastError();
             return FF_ERR_CUDA;
         }
@@ -420,7 +417,11 @@ int launch_small(const void* fn, dim3 grid, int smem, SmallArgs& a, bool alias, 
         return FF_ERR_INTERNAL;
     }
     if (static_cast<int64_t>(per_sm) * num_sms() < static_cast<int64_t>(grid.x) * grid.y) return FF_ERR_INTERNAL;
-    if (cudaLaunchCooperativeKernel(fn, grid, dim3(kSThreads), args, static_cast<size_t>(smem), st) != cudaSuccess) {
+    note_launch();
+    prof_gemm_begin(st);
+    const cudaError_t le = cudaLaunchCooperativeKernel(fn, grid, dim3(kSThreads), args, static_cast<size_t>(smem), st);
+    prof_gemm_end(st);
+    if (le != cudaSuccess) {
         cudaGetLastError();
         return FF_ERR_CUDA;
     }
@@ -501,7 +502,10 @@ int launch_gemm_small(const Plan& pl, bool tA, bool tB, int64_t m, int64_t n, in
     a.reduce = 0;
     const dim3 grid(static_cast<unsigned>((n + kSN - 1) / kSN), static_cast<unsigned>((m + kSM - 1) / kSM));
     if (grid.y > 65535u) return FF_ERR_INTERNAL;
+    note_launch();
+    prof_gemm_begin(st);
     small_gemm_kernel<<<grid, kSThreads, 0, st>>>(a);
+    prof_gemm_end(st);
     return cudaGetLastError() == cudaSuccess ? 0 : FF_ERR_CUDA;
 }
 

@@ -83,7 +83,6 @@ struct GemmArgs {
     int32_t hints;      // bit0: TMA loads evict_last; bit1: C stores evict_first
     int32_t last_use;   // 1 if no later launch reads these outputs (streaming stores allowed)
     unsigned long long* trace;  // optional per-CTA cycle counters (FF_TRACE=1), else null
-    int32_t debug_same_tile;    // experiment only: tm, tn taken mod this (wrong results)
     int32_t korder;             // 1 group-outer, 2 k-outer
     uint32_t kinv, kinv_sh;     // k-outer: 256^-(G-1) mod p
     const uint8_t* die_map;     // die-aware schedule (dies.cu): die of each %smid, or null
@@ -126,7 +125,6 @@ __device__ __forceinline__ void tile_coords(const GemmArgs& a, int t, int& tm, i
     const int rows_in_band = min(a.raster, a.tiles_m - band * a.raster);
     tm = band * a.raster + idx % rows_in_band;
     tn = idx / rows_in_band;
-    if (a.debug_same_tile) { tm %= a.debug_same_tile; tn %= a.debug_same_tile; }   // experiment only
 }
 
 // The common schedule every role walks: tiles in pairs (one per TMEM slot);
@@ -150,9 +148,6 @@ __device__ __forceinline__ void for_each_step(const GemmArgs& a, int unit, int n
         }
     }
 }
-
-// programmatic dependent launch of the GEMM after its encoders (FF_NOPDL=1: off)
-const bool g_pdl = getenv("FF_NOPDL") == nullptr;
 
 template <int kPair, bool kTrace>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -192,6 +187,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (threadIdx.x == 0 && leader) {
         const int nclusters = gridDim.x / kPair;
         int unit = blockIdx.x / kPair, nunits = nclusters, base = 0, count = a.num_tiles;
+#ifdef FF_EXPERIMENTS
         if (a.die_map) {
             uint32_t smid;
             asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
@@ -207,6 +203,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             base = d ? T0 : 0;
             count = d ? a.num_tiles - T0 : T0;
         }
+#endif
         sh->sched[0] = unit; sh->sched[1] = nunits; sh->sched[2] = base; sh->sched[3] = count;
     }
     ptx::tc_fence_before();
@@ -240,8 +237,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint64_t polB = polA;
             if (a.hints & 4) { polA = ptx::policy_evict_last(); polB = ptx::policy_evict_first(); }
             if (a.hints & 8) { polA = ptx::policy_evict_first(); polB = ptx::policy_evict_last(); }
+#ifdef FF_EXPERIMENTS
             int pair_idx = 0;
+#endif
             for_each_step(a, unit, nunits, tbase, tcount, [&](int tile, int slot, int g, int kb) {
+#ifdef FF_EXPERIMENTS
                 if (a.throttle && leader && slot == 0 && kb == 0 && g == a.G - 1) {
                     // soft lockstep: start tile pair j only once every cluster (on
                     // average) has started pair j - S, so the tiles in flight stay a
@@ -252,6 +252,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         while (*reinterpret_cast<volatile int*>(a.progress) < need) __nanosleep(128);
                     ++pair_idx;
                 }
+#endif
                 int tm, tn;
                 tile_coords(a, tile, tm, tn);
                 const int arow = tm * K::BM + static_cast<int>(rank) * 128;
@@ -644,25 +645,27 @@ int launch_impl(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A
     }
     a.throttle = 0;
     a.progress = nullptr;
-    if (const char* e = getenv("FF_THROTTLE")) {        // experiment: soft lockstep of the clusters
+#ifdef FF_EXPERIMENTS
+    if (knobs().throttle > 0) {        // experiment: soft lockstep of the clusters
         static int* ring = nullptr;
         static unsigned slot = 0;
         if (!ring && cudaMalloc(&ring, 4096 * sizeof(int)) != cudaSuccess) ring = nullptr;
-        if (ring && atoi(e) > 0) {
+        if (ring) {
             int* c = ring + (slot++ % 4096);
             if (cudaMemsetAsync(c, 0, sizeof(int), st) == cudaSuccess) {
                 a.progress = c;
-                a.throttle = atoi(e);
+                a.throttle = knobs().throttle;
             }
         }
     }
+#endif
     a.crt = pl.crt ? 1 : 0;
     a.cc = pl.cc;
     a.scratch = static_cast<uint8_t*>(scratch);
     if (pl.crt && pl.cc.nq > 1 && !scratch) return FF_ERR_INTERNAL;
     a.trace = nullptr;
     static unsigned long long* trace_buf = nullptr;
-    const bool tracing = getenv("FF_TRACE") != nullptr;
+    const bool tracing = knobs().trace;
     if (tracing) {
         if (!trace_buf) cudaMalloc(&trace_buf, 8 * 1024 * sizeof(unsigned long long));
         cudaMemsetAsync(trace_buf, 0, 8 * 1024 * sizeof(unsigned long long), st);
@@ -670,6 +673,7 @@ int launch_impl(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A
     }
     a.die_map = nullptr;
     a.sched = nullptr;
+#ifdef FF_EXPERIMENTS
     {
         const uint8_t* dm = nullptr;
         int* ring = nullptr;
@@ -683,28 +687,21 @@ int launch_impl(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A
             }
         }
     }
-    a.debug_same_tile = 0;
-    if (const char* e = getenv("FF_DEBUG_SAMETILE")) a.debug_same_tile = atoi(e) > 0 ? atoi(e) : 1;
+#endif
     a.kinv = pl.kinv;
     a.kinv_sh = pl.kinv_sh;
     a.raster = kRasterDefault;
     a.hints = 3;  // TMA loads evict_last, C stores streaming (swept on c4)
-    if (const char* e = getenv("FF_RASTER")) a.raster = atoi(e) > 0 ? atoi(e) : kRasterDefault;
-    if (const char* e = getenv("FF_HINTS")) a.hints = atoi(e);
+    if (knobs().raster > 0) a.raster = knobs().raster;
+    if (knobs().hints >= 0) a.hints = knobs().hints;
 
     CUtensorMap mapA, mapB;
     if (!make_plane_map(&mapA, A_limbs, I.L, m, I.k_pad, 128)) return FF_ERR_CUDA;
     if (!make_plane_map(&mapB, B_limbs, I.L, n, I.k_pad, K::BN / kPair)) return FF_ERR_CUDA;
 
-    static bool attr_set = false;
-    if (!attr_set) {
-        if (cudaFuncSetAttribute(ffgemm_tc_kernel<kPair, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM) !=
-                cudaSuccess ||
-            cudaFuncSetAttribute(ffgemm_tc_kernel<kPair, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM) !=
-                cudaSuccess)
-            return FF_ERR_CUDA;
-        attr_set = true;
-    }
+    if (set_smem_attr(reinterpret_cast<const void*>(ffgemm_tc_kernel<kPair, false>), K::SMEM) != cudaSuccess ||
+        set_smem_attr(reinterpret_cast<const void*>(ffgemm_tc_kernel<kPair, true>), K::SMEM) != cudaSuccess)
+        return FF_ERR_CUDA;
     const int64_t units = (num_sms() - pl.reserve_sms) / kPair;
     const int grid = static_cast<int>((nt < units ? nt : units) * kPair);
     cudaLaunchConfig_t cfg = {};
@@ -718,13 +715,16 @@ int launch_impl(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // prologue overlaps the encoders
-    attr[1].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+    attr[1].val.programmaticStreamSerializationAllowed = knobs().pdl ? 1 : 0;
     attr[2].id = cudaLaunchAttributeCooperative;   // all CTAs co-resident (die-aware registration)
     attr[2].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = a.die_map ? 3 : 2;
+    note_launch();
+    prof_gemm_begin(st);
     const cudaError_t lerr = tracing ? cudaLaunchKernelEx(&cfg, ffgemm_tc_kernel<kPair, true>, mapA, mapB, a)
                                      : cudaLaunchKernelEx(&cfg, ffgemm_tc_kernel<kPair, false>, mapA, mapB, a);
+    prof_gemm_end(st);
     if (lerr != cudaSuccess) return FF_ERR_CUDA;
     if (tracing) {  // development aid: per-CTA cycle counters, averaged over MMA-issuing CTAs
         unsigned long long h[8 * 1024];

@@ -72,6 +72,7 @@ struct Plan {
     uint32_t kinv, kinv_sh;          // 256^-(G-1) mod p and its Shoup constant (k-outer carry)
     bool all_auto;                   // no option forced: the planner may route to the small-field path
     bool canonical_ab;               // (internal callers) A, B hold canonical residues in [0, p)
+    int small_mode;                  // small-field kernels: -1 size rule, 0 never, 1 whenever valid
 };
 
 constexpr int64_t kKbLocalityBytes = 8192;  // L * kb per row-slice in k-outer order (swept on c4, c5)
@@ -137,6 +138,36 @@ cudaError_t launch_fill_uniform(int32_t* X, int64_t rows, int64_t cols, int64_t 
                                 cudaStream_t st);
 
 int num_sms();
+
+// Per-device, thread-safe cudaFuncSetAttribute(MaxDynamicSharedMemorySize) on the
+// current device, done once per (device, kernel): the attribute is per device
+// context, so a process-wide "done" flag would skip it on a second GPU.
+cudaError_t set_smem_attr(const void* fn, int bytes);
+
+// Developer knobs, read from the environment ONCE per process.
+// None changes a result: they pick between exact code paths or turn on
+// diagnostics.  Experiments that needed extra machinery (cluster throttling,
+// the die-aware schedule) are compiled only with -DFF_EXPERIMENTS.
+struct Knobs {
+    int small;          // FF_SMALL: -1 default rule, 0 never, 1 whenever valid
+    bool pdl;           // !FF_NOPDL: programmatic dependent launch of the GEMM
+    bool trace;         // FF_TRACE: per-CTA cycle counters (diagnostic kernel build)
+    int raster;         // FF_RASTER: tile rows per raster band (0 = default)
+    int hints;          // FF_HINTS: L2 policy bits (-1 = default)
+    int korder;         // FF_KORDER: 0 default, 1 group-outer, 2 k-outer
+    int64_t kbloc;      // FF_KBLOC: k-outer locality bytes (0 = default)
+    bool enc_notma;     // FF_ENC_NOTMA: LSU-load transposing encoders
+    int throttle;       // FF_THROTTLE (FF_EXPERIMENTS builds only)
+    bool die_aware;     // FF_DIE_AWARE (FF_EXPERIMENTS builds only)
+};
+const Knobs& knobs();
+
+// Benchmark instrumentation (ff_prof_start/stop, include/ffgemm.h): count every
+// kernel launch of the fgemm path, and bracket each GEMM-kernel launch with
+// two CUDA events on its stream while recording is on.  No-ops otherwise.
+void note_launch(int n = 1);
+void prof_gemm_begin(cudaStream_t st);
+void prof_gemm_end(cudaStream_t st);
 
 // api.cu: the classical device path (encode A, encode B, tcgen05 GEMM) for
 // callers inside the library (trsm.cu), and its workspace size.

@@ -1060,17 +1060,10 @@ int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t* A, int64_t lda, int64_
     std::vector<int32_t> hout(4 + 4 * kMaxSwaps);
     std::vector<int64_t> hp(4 * kMaxSwaps);
     const uint32_t neg1 = p - 1;
-    static bool attr = false;
-    if (!attr) {
-        if (cudaFuncSetAttribute(panel_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes) !=
-                cudaSuccess ||
-            cudaFuncSetAttribute(panel2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPanel2Smem) !=
-                cudaSuccess ||
-            cudaFuncSetAttribute(panel_spec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSpecSmem) !=
-                cudaSuccess)
-            return fail_cuda_now();
-        attr = true;
-    }
+    if (set_smem_attr(reinterpret_cast<const void*>(panel_kernel<true>), kSmemBytes) != cudaSuccess ||
+        set_smem_attr(reinterpret_cast<const void*>(panel2_kernel), kPanel2Smem) != cudaSuccess ||
+        set_smem_attr(reinterpret_cast<const void*>(panel_spec_kernel), kSpecSmem) != cudaSuccess)
+        return fail_cuda_now();
     static const bool use_pair = getenv("FF_LQUP_ONECTA") == nullptr;   // experiment: one-CTA panels only
     // speculative no-swap panels; given up after kSpecGiveUp failures (small fields)
     constexpr int kSpecGiveUp = 2;

@@ -260,7 +260,7 @@ int make_limb_plan(uint32_t p, int64_t k, const ff_opts& o, int64_t half, int64_
     // Step order: k-outer needs 256 invertible mod p when there are several groups.
     int korder = o.korder == 0 ? 2 : o.korder;
     pl.korder_auto = (o.korder == 0 && o.kb_override == 0);
-    if (const char* e = getenv("FF_KORDER")) { korder = atoi(e) == 1 ? 1 : 2; pl.korder_auto = false; }  // experiment only
+    if (knobs().korder > 0) { korder = knobs().korder == 1 ? 1 : 2; pl.korder_auto = false; }  // experiment only
     if (korder == 2 && L > 1 && (p % 2) == 0) korder = 1;
     pl.korder = korder;
     I.korder = korder;
@@ -270,7 +270,7 @@ int make_limb_plan(uint32_t p, int64_t k, const ff_opts& o, int64_t half, int64_
         kb = o.kb_override;
     } else if (korder == 2) {
         int64_t loc = (kKbLocalityBytes / L + kBK - 1) / kBK * kBK;   // L=1: 8192, 2: 4096, 3: 2816, 4: 2048
-        if (const char* e = getenv("FF_KBLOC")) loc = atoll(e) > 0 ? atoll(e) : loc;  // experiment only
+        if (knobs().kbloc > 0) loc = knobs().kbloc;  // experiment only
         kb = loc < kb ? loc : kb;
     }
     kb = (kb / kBK) * kBK;
@@ -311,12 +311,14 @@ int make_plan(uint32_t p, int64_t k, const ff_opts* opts, Plan* out) {
     if (o.cta_group < 0 || o.cta_group > 2) return FF_ERR_OPTS;
     if (o.korder < 0 || o.korder > 2) return FF_ERR_OPTS;
     if (o.inputs_canonical < 0 || o.inputs_canonical > 1) return FF_ERR_OPTS;
+    if (o.small_path < -1 || o.small_path > 1) return FF_ERR_OPTS;
 
     Plan pl;
     std::memset(&pl, 0, sizeof(pl));
     pl.all_auto = o.scheme == FF_SCHEME_AUTO && o.winograd == 0 && o.kb_override == 0 && o.cta_group == 0 &&
                   o.korder == 0 && o.debug_saturate == 0 && o.debug_unchecked_kb == 0;
     pl.canonical_ab = o.inputs_canonical != 0;
+    pl.small_mode = o.small_path != 0 ? (o.small_path > 0 ? 1 : 0) : knobs().small;
     ff_plan_info& I = pl.info;
     // Centred residues lie in [-neg, half]: neg = half for odd p, half + 1 for p = 2.
     const int64_t half = (int64_t)(p - 1) / 2;

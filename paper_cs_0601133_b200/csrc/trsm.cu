@@ -501,13 +501,8 @@ int ff_trsm_ex(uint32_t p, char side, char uplo, char transA, char diag, int64_t
     ia.mu64 = static_cast<unsigned long long>((static_cast<unsigned __int128>(1) << 64) / p);
     ia.W = reinterpret_cast<int32_t*>(ws + w.lvl_off[0]);
     const size_t smem = kInvSmem;
-    static bool attr = false;
-    if (!attr) {
-        if (cudaFuncSetAttribute(trsm_diag_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-            cudaSuccess)
-            return FF_ERR_CUDA;
-        attr = true;
-    }
+    if (set_smem_attr(reinterpret_cast<const void*>(trsm_diag_inv_kernel), (int)smem) != cudaSuccess)
+        return FF_ERR_CUDA;
     trsm_diag_inv_kernel<<<static_cast<unsigned>((d + kNb - 1) / kNb), kInvThreads, smem, st>>>(ia);
     if (cudaGetLastError() != cudaSuccess) return FF_ERR_CUDA;
     // double the inverted blocks up to kLeaf: W_s = [W1, X; 0, W3] (upper)

@@ -119,6 +119,7 @@ int run_winograd(const Plan& half, bool transA, bool transB, int64_t m, int64_t 
     const int32_t* B12 = quad(B, ldb, transB, hk, hn, 0, 1);
     const int32_t* B21 = quad(B, ldb, transB, hk, hn, 1, 0);
     const int32_t* B22 = quad(B, ldb, transB, hk, hn, 1, 1);
+    note_launch(2);
     preadd_kernel<<<grid2(a_rows, a_cols), 256, 0, st>>>(half.mp, 0, a_rows, a_cols, A11, A12, A21, A22, lda, S[0],
                                                          S[1], S[2], S[3]);
     preadd_kernel<<<grid2(b_rows, b_cols), 256, 0, st>>>(half.mp, 1, b_rows, b_cols, B11, B12, B21, B22, ldb, T[0],

@@ -33,7 +33,7 @@ class ff_opts(ctypes.Structure):
     _fields_ = [("winograd", _i32), ("scheme", _i32), ("kb_override", _i64),
                 ("debug_saturate", _i32), ("cta_group", _i32), ("host_block", _i32),
                 ("korder", _i32), ("debug_unchecked_kb", _i32), ("inputs_canonical", _i32),
-                ("reserved", _i32 * 2)]
+                ("small_path", _i32), ("reserved", _i32 * 1)]
 
 
 class ff_plan_info(ctypes.Structure):
@@ -70,6 +70,9 @@ _SIGS = {
     "ff_lqup_workspace_size": ([_u32, _i64, _i64, _OPTS_P], _sz),
     "ff_lqup_ex": ([_u32, _i64, _i64, _p, _i64, _p, _p, _p, _OPTS_P, _p, _sz, _p], ctypes.c_int),
     "ff_rank_det": ([_u32, _i64, _i64, _p, _i64, _p, _p], ctypes.c_int),
+    "ff_prof_start": ([_i32], ctypes.c_int),
+    "ff_prof_stop": ([_p, _i32, _p], ctypes.c_int),
+    "ff_mma_ceiling": ([_i32, _p], ctypes.c_int),
 }
 for _name, (_args, _res) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -185,6 +188,28 @@ def ff_trsm_ex(p, side, uplo, transA, diag, m, n, alpha, A, lda, B, ldb, opts=No
     _check(_lib.ff_trsm_ex(p, _tr(side), _tr(uplo), _tr(transA), _tr(diag), m, n, alpha % 2 ** 32, _ptr(A),
                            lda, _ptr(B), ldb, _opts(opts), _ptr(workspace), workspace_bytes, _stream(stream)),
            "ff_trsm_ex")
+
+
+def ff_prof_start(capacity: int) -> None:
+    """Start bracketing the library's GEMM-kernel launches with CUDA events (benchmarks)."""
+    _check(_lib.ff_prof_start(capacity), "ff_prof_start")
+
+
+def ff_prof_stop(capacity: int):
+    """Stop recording; returns (per-launch GEMM kernel times in ms, kernel launches counted)."""
+    buf = (ctypes.c_float * max(1, capacity))()
+    launches = ctypes.c_int64(0)
+    n = _lib.ff_prof_stop(buf, capacity, ctypes.byref(launches))
+    if n < 0:
+        raise FFError(-n, "ff_prof_stop")
+    return [buf[i] for i in range(min(n, capacity))], launches.value
+
+
+def ff_mma_ceiling(iters: int = 200000) -> float:
+    """Measured int8 tcgen05 MMA-only throughput of the current device (TOPS)."""
+    out = ctypes.c_double(0.0)
+    _check(_lib.ff_mma_ceiling(iters, ctypes.byref(out)), "ff_mma_ceiling")
+    return out.value
 
 
 # ---------------------------------------------------------------- marshalling helpers

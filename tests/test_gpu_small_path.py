@@ -1,6 +1,7 @@
 """The small-field latency path (gemm_small.cu: p < 2^16, warp-level mma.sync on
 byte-split residues, no encoders) against the oracle, forced on
-with FF_SMALL=1 for every shape, and bit-identical to the tcgen05 path."""
+with ff_opts.small_path = 1 for every shape, and bit-identical to the tcgen05 path
+(small_path = -1)."""
 import numpy as np
 import pytest
 
@@ -22,7 +23,7 @@ def env():
 
 @pytest.mark.parametrize("p", PRIMES)
 @pytest.mark.parametrize("tA,tB", [("N", "N"), ("T", "N"), ("N", "T"), ("T", "T")])
-def test_small_path_vs_oracle(env, p, tA, tB, monkeypatch):
+def test_small_path_vs_oracle(env, p, tA, tB):
     torch, ff = env
     rng = np.random.default_rng(p + ord(tA) * 7 + ord(tB))
     for (m, n, k) in [(1, 1, 1), (5, 3, 7), (64, 64, 32), (65, 63, 33), (128, 300, 128), (200, 70, 1000),
@@ -35,19 +36,19 @@ def test_small_path_vs_oracle(env, p, tA, tB, monkeypatch):
         for alpha, beta in [(1, 0), (p - 1, 1), (int(rng.integers(0, p)), int(rng.integers(0, p)))]:
             want = oracle.fgemm(p, tA, tB, alpha, A[:, :ac], B[:, :bc], beta, C[:, :n], m=m, n=n, k=k)
             outs = []
-            for mode in ("1", "0"):
-                monkeypatch.setenv("FF_SMALL", mode)
+            for mode in (1, -1):
                 dA, dB, dC = (torch.from_numpy(x).cuda() for x in (A, B, C))
-                ff.ff_gemm_ex(p, tA, tB, m, n, k, alpha, dA, A.shape[1], dB, B.shape[1], beta, dC, C.shape[1])
+                ff.ff_gemm_ex(p, tA, tB, m, n, k, alpha, dA, A.shape[1], dB, B.shape[1], beta, dC, C.shape[1],
+                              {"small_path": mode})
                 torch.cuda.synchronize()
                 got = dC.cpu().numpy()
-                np.testing.assert_array_equal(got[:, :n], want, err_msg="FF_SMALL=%s m=%d n=%d k=%d" % (mode, m, n, k))
+                np.testing.assert_array_equal(got[:, :n], want, err_msg="small_path=%s m=%d n=%d k=%d" % (mode, m, n, k))
                 np.testing.assert_array_equal(got[:, n:], C[:, n:])
                 outs.append(got)
             np.testing.assert_array_equal(outs[0], outs[1])
 
 
-def test_small_path_k_at_the_s32_bound(env, monkeypatch):
+def test_small_path_k_at_the_s32_bound(env):
     """K = 32768 with every byte 255 (x = 65535 is not a residue mod 65521, but
     p - 1 = 65520 = 0xFFF0 maximises the high bytes): each byte product sum
     reaches 32768 * 255^2 < 2^31, the largest K the path accepts."""
@@ -58,15 +59,14 @@ def test_small_path_k_at_the_s32_bound(env, monkeypatch):
     B = np.full((k, n), p - 1, np.int32)
     C = np.zeros((m, n), np.int32)
     want = oracle.fgemm(p, "N", "N", 1, A, B, 0, C, m=m, n=n, k=k)
-    monkeypatch.setenv("FF_SMALL", "1")
     dA, dB, dC = (torch.from_numpy(x).cuda() for x in (A, B, C))
-    ff.ff_gemm_ex(p, "N", "N", m, n, k, 1, dA, k, dB, n, 0, dC, n)
+    ff.ff_gemm_ex(p, "N", "N", m, n, k, 1, dA, k, dB, n, 0, dC, n, {"small_path": 1})
     torch.cuda.synchronize()
     np.testing.assert_array_equal(dC.cpu().numpy(), want)
 
 
 @pytest.mark.parametrize("p", [2, 251, 65521, 65537, 8388593, 16777259, 67108859, 2 ** 31 - 1])
-def test_small_path_canonical_inputs(env, p, monkeypatch):
+def test_small_path_canonical_inputs(env, p):
     """inputs_canonical = 1 (A, B already in [0, p)): the cp.async variants
     stream them raw (p < 2^16: two bytes, four byte products; larger p: three
     or four bytes, 9 or 16 byte products); ragged K and n exercise its partial (zero-filled) 16-byte
@@ -85,38 +85,31 @@ def test_small_path_canonical_inputs(env, p, monkeypatch):
         C = rng.integers(-2 ** 31, 2 ** 31, size=(m, n), dtype=np.int64).astype(np.int32)
         alpha, beta = p - 1, 1
         want = oracle.fgemm(p, tA, tB, alpha, A[:, :ac], B[:, :bc], beta, C, m=m, n=n, k=k)
-        for mode in ("1", None):
-            if mode is None:
-                monkeypatch.delenv("FF_SMALL", raising=False)
-            else:
-                monkeypatch.setenv("FF_SMALL", mode)
+        for mode in (1, 0):
             dA, dB, dC = (torch.from_numpy(x).cuda() for x in (A, B, C))
-            ff.ff_gemm_ex(p, tA, tB, m, n, k, alpha, dA, la, dB, lb, beta, dC, n, {"inputs_canonical": 1})
+            ff.ff_gemm_ex(p, tA, tB, m, n, k, alpha, dA, la, dB, lb, beta, dC, n,
+                          {"inputs_canonical": 1, "small_path": mode})
             torch.cuda.synchronize()
-            np.testing.assert_array_equal(dC.cpu().numpy(), want, err_msg="m=%d n=%d k=%d %s%s FF_SMALL=%s" % (
+            np.testing.assert_array_equal(dC.cpu().numpy(), want, err_msg="m=%d n=%d k=%d %s%s small_path=%s" % (
                 m, n, k, tA, tB, mode))
 
 
 @pytest.mark.parametrize("p", [65521, 8388593])
 @pytest.mark.parametrize("canonical", [0, 1])
-def test_in_place_products(env, p, canonical, monkeypatch):
+def test_in_place_products(env, p, canonical):
     """C aliasing B (X <- W X) or A (X <- X W), as LQUP's U_rest / G products
     do: the small paths read A and B while other CTAs write C, so an overlap
     must either take the grid-barrier variant (canonical inputs) or the
     tcgen05 path (which reads only its encoded planes).  Forced small paths
-    (FF_SMALL=1) included; results bit-exact."""
+    (small_path = 1) included; results bit-exact."""
     torch, ff = env
     rng = np.random.default_rng(p + canonical)
-    for mode in ("1", None):
-        if mode is None:
-            monkeypatch.delenv("FF_SMALL", raising=False)
-        else:
-            monkeypatch.setenv("FF_SMALL", mode)
+    for mode in (1, 0):
         for (r, c) in [(128, 1000), (300, 128), (128, 128)]:
             k = r if c >= r else c
             W = rng.integers(0, p, size=(k, k), dtype=np.int64).astype(np.int32)
             X = rng.integers(0, p, size=(r, c), dtype=np.int64).astype(np.int32)
-            opts = {"inputs_canonical": canonical}
+            opts = {"inputs_canonical": canonical, "small_path": mode}
             dW = torch.from_numpy(W).cuda()
             if c >= r:      # X <- W X  (C = B)
                 dX = torch.from_numpy(X).cuda()
@@ -127,4 +120,37 @@ def test_in_place_products(env, p, canonical, monkeypatch):
                 ff.ff_gemm_ex(p, "N", "N", r, c, c, 1, dX, c, dW, k, 0, dX, c, opts)
                 want = oracle.fgemm(p, "N", "N", 1, X, W, 0, None, m=r, n=c, k=c)
             torch.cuda.synchronize()
-            np.testing.assert_array_equal(dX.cpu().numpy(), want, err_msg="%dx%d FF_SMALL=%s" % (r, c, mode))
+            np.testing.assert_array_equal(dX.cpu().numpy(), want, err_msg="%dx%d small_path=%s" % (r, c, mode))
+
+
+@pytest.mark.parametrize("p", [251, 65521])
+def test_streaming_kernel_reduces_raw_operands(env, p):
+    """The default rule's raw-input branch of the streaming kernel (non-transposed
+    A and B with 16-byte rows: leading dimensions multiples of 4, any int32
+    values, each K slice reduced in shared memory), ragged m, n, k, and an
+    in-place call (C aliasing A) with raw inputs; bit-exact vs the oracle, with
+    the size rule (small_path = 0) and forced (1)."""
+    torch, ff = env
+    rng = np.random.default_rng(p + 99)
+    for (m, n, k) in [(65, 63, 33), (200, 70, 1000), (128, 256, 512), (1, 4, 4)]:
+        la, lb = (k + 3) // 4 * 4, (n + 3) // 4 * 4
+        A = rng.integers(-2 ** 31, 2 ** 31, size=(m, la), dtype=np.int64).astype(np.int32)
+        B = rng.integers(-2 ** 31, 2 ** 31, size=(k, lb), dtype=np.int64).astype(np.int32)
+        C = rng.integers(-2 ** 31, 2 ** 31, size=(m, n), dtype=np.int64).astype(np.int32)
+        for alpha, beta in [(1, 0), (p - 1, 1)]:
+            want = oracle.fgemm(p, "N", "N", alpha, A[:, :k], B[:, :n], beta, C, m=m, n=n, k=k)
+            for mode in (0, 1):
+                dA, dB, dC = (torch.from_numpy(x).cuda() for x in (A, B, C))
+                ff.ff_gemm_ex(p, "N", "N", m, n, k, alpha, dA, la, dB, lb, beta, dC, n, {"small_path": mode})
+                torch.cuda.synchronize()
+                np.testing.assert_array_equal(dC.cpu().numpy(), want, err_msg="%dx%dx%d mode %d" % (m, n, k, mode))
+    # in place, raw inputs: X <- X W with X m x k (ld multiple of 4), W k x k
+    m, k = 96, 64
+    X = rng.integers(-2 ** 31, 2 ** 31, size=(m, k), dtype=np.int64).astype(np.int32)
+    W = rng.integers(-2 ** 31, 2 ** 31, size=(k, k), dtype=np.int64).astype(np.int32)
+    want = oracle.fgemm(p, "N", "N", 1, X, W, 0, None, m=m, n=k, k=k)
+    for mode in (0, 1):
+        dX, dW = torch.from_numpy(X).cuda(), torch.from_numpy(W).cuda()
+        ff.ff_gemm_ex(p, "N", "N", m, k, k, 1, dX, k, dW, k, 0, dX, k, {"small_path": mode})
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(dX.cpu().numpy(), want, err_msg="in place, mode %d" % mode)

@@ -335,3 +335,14 @@ def test_generator_vector_matches_scalar_and_blocks():
     assert np.array_equal(M.ravel(), v[:1000])
     assert np.array_equal(ffgen.uniform_matrix(p, 5, ffgen.STREAM_A, 40, 25, row0=7, nrows=3), M[7:10])
     assert v.min() >= 0 and v.max() < p
+
+
+def test_generator_c_twin_matches_numpy():
+    # ffgen/gen.c (OpenMP, used for large host inputs) against the numpy recipe,
+    # including an index window past 2^32 and every config prime
+    for p in [2, 251, 65521, 8388593, 67108859, 2 ** 31 - 1]:
+        for start in (0, 12345, (1 << 32) - 1000):
+            a = ffgen.uniform_flat(p, 3, ffgen.STREAM_B, start, 1 << 17)
+            b = ffgen.uniform_flat_numpy(p, 3, ffgen.STREAM_B, start, 1 << 17)
+            assert np.array_equal(a, b)
+    assert ffgen._c_gen() is not None

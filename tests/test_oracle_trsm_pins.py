@@ -205,10 +205,12 @@ def test_dot_product_and_winograd_bounds():
     for p in [65521, 1048583, 8388617]:            # (2^53 / (p-1)^2 not an integer)
         assert bounds.k_winograd(p, 53, 0) == bounds.lambda_dot(p, 53) + 1
     # Theorem 3.1 / Cor 3.2 at l = 1 with the positive representation: the bound
-    # ((1+3)/2)^2 floor(k/2) (p-1)^2 fits gamma bits just below k_W
+    # ((1+3)/2)^2 floor(k/2) (p-1)^2 fits gamma bits just below k_W (here the
+    # printed formula's quotient is such that it equals the exact threshold)
     p, g = 65521, 53
     kw = bounds.k_winograd(p, g, 1)
-    assert 4 * ((kw - 1) // 2) * (p - 1) ** 2 < 2 ** (g + 2) * 2 // 2
+    assert 4 * ((kw - 1) // 2) * (p - 1) ** 2 < 2 ** g
+    assert 4 * (kw // 2) * (p - 1) ** 2 >= 2 ** g
 
 
 # ---------------------------------------------------------------- rank / det oracle (Sec. 6)
