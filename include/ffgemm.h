@@ -73,9 +73,11 @@ extern "C" {
 /* FP64: the paper-literal "Zpz-double" engine: centred
  * residues as doubles on the fp64 tensor cores (DMMA), lambda products
  * accumulated exactly between floating-point reductions, lambda from Eq. (2)
- * with gamma = 53.  Only when chosen explicitly; needs lambda >= 4, i.e.
- * p <= 2^26 + 1 (the paper's feasibility bound, l.882).  Not available for
- * ff_encode / ff_gemm_limbs / ff_gemm_host / Winograd (FF_ERR_OPTS). */
+ * with gamma = 53, or l recursive Winograd levels with no reduction at all
+ * under Corollary 3.4 (ff_opts.winograd = l).  Only when chosen explicitly;
+ * needs lambda >= 4, i.e. p <= 2^26 + 1 (the paper's feasibility bound,
+ * l.882).  Not available for ff_encode / ff_gemm_limbs / ff_gemm_host
+ * (FF_ERR_OPTS). */
 #define FF_SCHEME_FP64 4
 
 /* Options for the _ex / split entry points.  Zero-initialise and set fields;
@@ -83,7 +85,11 @@ extern "C" {
 typedef struct ff_opts {
     int32_t winograd;       /* 0 auto, 1 one Winograd level (Table 2; needs even
                                m, n, k with m, n >= 512 and k >= 256, else FF_ERR_OPTS),
-                               -1 never */
+                               -1 never.  FF_SCHEME_FP64: l = 1, 2 or 3 recursive levels
+                               with unreduced pre-additions (Sec. 3.2.3; any
+                               shape: m, n zero-padded to multiples of 2^l, the last
+                               k mod 2^l columns peeled), accepted iff k < k_winograd[l]
+                               of ff_plan_info, else FF_ERR_OPTS */
     int32_t scheme;         /* FF_SCHEME_*; AUTO picks the fewest int8 products: limbs
                                (S on ties) unless CRT needs clearly fewer */
     int64_t kb_override;    /* 0: planner k-block; else k-block length in elements,
@@ -100,8 +106,9 @@ typedef struct ff_opts {
                                weight group over all of k), 2 k-outer (each k-block through
                                all groups: L2 locality) */
     int32_t debug_unchecked_kb; /* test builds only: accept a kb_override above the safe
-                               bound (to show that the bound is needed); results are then
-                               not guaranteed */
+                               bound, or (FF_SCHEME_FP64) Winograd levels with k past
+                               k_winograd (to show that the bounds are needed); results
+                               are then not guaranteed */
     int32_t inputs_canonical; /* 1: the caller guarantees every element of op(A), op(B) is a
                                canonical residue in [0, p) (C may still be any int32): for
                                p < 2^16 short-K products may then stream A and B raw
@@ -138,6 +145,11 @@ typedef struct ff_plan_info {
                                 q_i <= 256, with prod q_i >= 4 k centre_max^2 */
     int32_t log2_M_floor;    /* CRT: floor(log2(prod q_i)) */
     int32_t log2_bound_ceil; /* CRT: ceil(log2(4 k centre_max^2)) (<= log2_M_floor) */
+    int64_t k_winograd[4];   /* FF_SCHEME_FP64: l = 1..3 Winograd levels without any
+                                reduction are accepted iff k < k_winograd[l] (Corollary 3.4,
+                                PAPER.md l.304-312, exact form: ceil(2^53 / v_l^2) 2^l with
+                                v_l = 3^l centre_max, Theorem 3.1 on the balanced range);
+                                [0] = lambda + 1 (Eq. (2)); 0 for the int8 schemes */
 } ff_plan_info;
 
 /* Library version (major*10000 + minor*100 + patch). Host only. */
@@ -172,6 +184,16 @@ int ff_gemm_ex(uint32_t p, char transA, char transB, int64_t m, int64_t n, int64
                uint32_t alpha, const int32_t *A, int64_t lda, const int32_t *B, int64_t ldb,
                uint32_t beta, int32_t *C, int64_t ldc, const ff_opts *opts,
                void *workspace, size_t workspace_bytes, void *stream);
+
+/* *levels <- the Winograd levels ff_gemm_ex would run for this problem with
+ * these options (host only, no GPU needed): 0 classical, 1 one level (int8
+ * engines: forced by opts->winograd or, by default, where it was measured to
+ * win -- DESIGN.md §7), 1..3 (FF_SCHEME_FP64 with opts->winograd = l).
+ * Returns 0, -1 p, -2 m, -3 n, -4 k, -6 levels NULL, or FF_ERR_OPTS (options
+ * invalid, or a forced level the shape or Corollary 3.4 does not allow).  The
+ * multi-GPU driver uses it to decide whether a rank multiplies its panel in
+ * one call. */
+int ff_gemm_winograd_levels(uint32_t p, int64_t m, int64_t n, int64_t k, const ff_opts *opts, int32_t *levels);
 
 /* As ff_gemm, but A, B and C are HOST pointers (pinned for full PCIe speed;
  * pageable works).  Copies in, computes on the current device, copies C back

@@ -120,7 +120,7 @@ bool winograd_auto_wins(const Plan& pl, int64_t m, int64_t n, int64_t k) {
 }
 
 size_t ws_bytes(const Plan& pl, int64_t m, int64_t n) {
-    if (pl.fp64) return f64_ws_bytes(pl, m, n);
+    if (pl.fp64) return f64_ws_bytes(pl, m, n, 0, 0);
     const size_t L = static_cast<size_t>(pl.info.L), kp = static_cast<size_t>(pl.info.k_pad);
     return align256(L * static_cast<size_t>(m) * kp) + align256(L * static_cast<size_t>(n) * kp) +
            align256(crt_scratch_bytes(pl));
@@ -133,7 +133,13 @@ int cuda_rc(cudaError_t e) { return e == cudaSuccess ? 0 : FF_ERR_CUDA; }
 // or FF_ERR_OPTS (forced but the shape is not even).
 int use_winograd(const Plan& pl, const ff_opts* opts, int64_t m, int64_t n, int64_t k) {
     const int w = opts ? opts->winograd : 0;
-    if (pl.fp64) return w == 1 ? -FF_ERR_OPTS : 0;     // the fp64 engine is classical only
+    if (pl.fp64) {
+        // l levels of delayed Winograd (Sec. 3.2.3), only when asked for and
+        // only while Corollary 3.4 allows it (the planner's exact k_winograd[l])
+        if (w <= 0) return 0;
+        if (k >= pl.info.k_winograd[w] && !(opts && opts->debug_unchecked_kb)) return -FF_ERR_OPTS;
+        return w;
+    }
     const bool even = (m % 2 == 0) && (n % 2 == 0) && (k % 2 == 0) && m >= 512 && n >= 512 && k >= 256;
     if (w == 1) return even ? 1 : -FF_ERR_OPTS;
     if (w < 0) return 0;
@@ -178,7 +184,7 @@ bool prefer_small_wide(const Plan& pl, int64_t m, int64_t n, int64_t k) {
 int run(const Plan& pl, char transA, char transB, int64_t m, int64_t n, int64_t k, const int32_t* A,
         int64_t lda, const int32_t* B, int64_t ldb, int32_t* C, int64_t ldc, void* ws, cudaStream_t st) {
     if (k == 0 || pl.mp.alpha == 0) return cuda_rc(launch_scale_c(pl.mp, m, n, C, ldc, st));
-    if (pl.fp64) return run_f64(pl, is_t(transA), is_t(transB), m, n, k, A, lda, B, ldb, C, ldc, ws, st);
+    if (pl.fp64) return run_f64(pl, 0, is_t(transA), is_t(transB), m, n, k, A, lda, B, ldb, C, ldc, ws, st);
     // The small paths read A and B while other CTAs write C, so C must not overlap
     // them (an in-place product, e.g. LQUP's U_rest = L11^-1 A_rest, takes the
     // tcgen05 path, which reads only the encoded planes).  Conservative span test.
@@ -378,12 +384,33 @@ size_t ff_gemm_workspace_size(uint32_t p, char transA, char transB, int64_t m, i
     Plan pl;
     if (make_plan(p, k, opts, &pl)) return 0;
     size_t need = ws_bytes(pl, m, n);
+    if (pl.fp64) {
+        const int lv = use_winograd(pl, opts, m, n, k);
+        return f64_ws_bytes(pl, m, n, k, lv > 0 ? lv : 0);
+    }
     if (use_winograd(pl, opts, m, n, k) == 1) {
         Plan half;
         if (make_plan(p, k / 2, opts, &half)) return 0;
         need = std::max(need, winograd_ws_bytes(half, m, n, k));
     }
     return need;
+}
+
+int ff_gemm_winograd_levels(uint32_t p, int64_t m, int64_t n, int64_t k, const ff_opts* opts, int32_t* levels) {
+    if (p < 2 || p >= (1u << 31)) return -1;
+    if (m < 0) return -2;
+    if (n < 0) return -3;
+    if (k < 0) return -4;
+    if (!levels) return -6;
+    Plan pl;
+    const int e = make_plan(p, k, opts, &pl);
+    if (e) return e;
+    *levels = 0;
+    if (m == 0 || n == 0 || k == 0) return 0;
+    const int w = use_winograd(pl, opts, m, n, k);
+    if (w < 0) return -w;
+    *levels = w;
+    return 0;
 }
 
 int ff_gemm_ex(uint32_t p, char transA, char transB, int64_t m, int64_t n, int64_t k, uint32_t alpha,
@@ -399,7 +426,7 @@ int ff_gemm_ex(uint32_t p, char transA, char transB, int64_t m, int64_t n, int64
     const int wino = (k == 0 || pl.mp.alpha == 0) ? 0 : use_winograd(pl, opts, m, n, k);
     if (wino < 0) return -wino;
     Plan half;
-    if (wino) {
+    if (wino && !pl.fp64) {
         if ((e = make_plan(p, k / 2, opts, &half))) return e;
         set_scalars(&half, alpha, beta);
     }
@@ -407,8 +434,11 @@ int ff_gemm_ex(uint32_t p, char transA, char transB, int64_t m, int64_t n, int64
     e = arch_check(dev);
     if (e) return e;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const size_t need = wino ? winograd_ws_bytes(half, m, n, k) : ws_bytes(pl, m, n);
+    const size_t need = pl.fp64 ? f64_ws_bytes(pl, m, n, k, wino)
+                                : wino ? winograd_ws_bytes(half, m, n, k) : ws_bytes(pl, m, n);
     auto go = [&](void* w) {
+        if (pl.fp64 && wino)
+            return run_f64(pl, wino, is_t(transA), is_t(transB), m, n, k, A, lda, B, ldb, C, ldc, w, st);
         return wino ? run_winograd(half, is_t(transA), is_t(transB), m, n, k, A, lda, B, ldb, C, ldc, w, st)
                     : run(pl, transA, transB, m, n, k, A, lda, B, ldb, C, ldc, w, st);
     };

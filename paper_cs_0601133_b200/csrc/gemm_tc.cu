@@ -91,16 +91,16 @@ struct GemmArgs {
     int32_t throttle;           // slack S in tile pairs (0: off)
     int32_t crt;                // 1: groups are CRT moduli
     CrtConsts cc;
-    uint8_t* scratch;           // CRT: per CTA and slot, G-1 byte planes of kCrtPlane bytes
+    uint8_t* scratch;           // CRT: per CTA and slot, G byte planes of kCrtPlane bytes
 };
 
-// CRT residue scratch: one 128 x 256 byte plane per (CTA, slot, modulus 1..G-1),
+// CRT residue scratch: one 128 x 256 byte plane per (CTA, slot, modulus 0..G-1),
 // laid out [h: 64-column quarter][c: 16-column chunk][row 0..127][16 bytes] so
 // that a warp's 32 rows store / load 512 contiguous bytes per instruction.
 constexpr int kCrtPlane = 128 * kTileN;
 
 __device__ __forceinline__ uint8_t* crt_plane(const GemmArgs& a, int slot, int g) {
-    return a.scratch + (static_cast<size_t>(blockIdx.x * 2 + slot) * (a.G - 1) + (g - 1)) * kCrtPlane;
+    return a.scratch + (static_cast<size_t>(blockIdx.x * 2 + slot) * a.G + g) * kCrtPlane;
 }
 
 __device__ __forceinline__ unsigned long long clk() {
@@ -146,6 +146,18 @@ __device__ __forceinline__ void for_each_step(const GemmArgs& a, int unit, int n
                 for (int kb = 0; kb < a.nkb; ++kb)
                     for (int s = 0; s < nslots; ++s) f(base + (s == 0 ? t0 : t1), s, g, kb);
         }
+    }
+}
+
+// Hand a TMEM accumulator slot back to the MMA issuer (all epilogue warps of
+// both CTAs arrive on the leader's barrier).
+template <int kPair>
+__device__ __forceinline__ void release_slot(Smem* sh, int slot, uint32_t lane, uint32_t leader0, uint32_t leader1) {
+    ptx::tc_fence_before();
+    __syncwarp();
+    if (lane == 0) {
+        if (kPair == 2) ptx::mbar_arrive_cluster(slot ? leader1 : leader0);
+        else ptx::mbar_arrive(&sh->accempty[slot]);
     }
 }
 
@@ -357,10 +369,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             const bool rescale = (a.korder == 2) && g == 0 && !last_kb;
             const uint32_t tcol = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + slot * kTileN + h * 64;
             const int crow = q * 32 + static_cast<int>(lane);   // row of this thread within the CTA tile
-            if (a.crt && !final_step) {
+            // The TMEM slot is handed back to the MMA as soon as the accumulator has been
+            // read; for CRT plans that happens BEFORE the final step's reconstruction and
+            // output stores, which then overlap the next tile's MMAs on this slot.
+            const bool crt_final = a.crt && final_step;
+            if (a.crt) {
                 // CRT: between k-blocks keep the centred residue
                 // mod q_g; after the last one store u_g = (S_g mod q_g) v_g mod q_g
-                // to this CTA's scratch (read back by the final step of the tile).
+                // to this CTA's scratch (read back by the final step of the tile,
+                // modulus 0 included).
                 uint32_t v[64];
                 ptx::tmem_ld64(tcol, v);
                 ptx::tmem_wait_ld();
@@ -390,6 +407,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                         *reinterpret_cast<uint4*>(dst + c * 128 * 16) = make_uint4(w[0], w[1], w[2], w[3]);
                     }
                 }
+            }
+            if (crt_final) release_slot<kPair>(sh, slot, lane, accempty_leader0, accempty_leader1);
+            if (a.crt && !final_step) {
+                // (done above)
             } else if (rescale) {
                 uint32_t v[64];
                 ptx::tmem_ld64(tcol, v);
@@ -427,30 +448,33 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
                 for (int half = 0; half < 2; ++half) {
                     uint32_t v[32];
-                    ptx::tmem_ld32(tcol + half * 32, v);
-                    ptx::tmem_wait_ld();
+                    if (a.crt) {       // (the accumulator was released: everything comes from scratch)
+#pragma unroll
+                        for (int t = 0; t < 32; ++t) v[t] = 0;
+                    } else {
+                        ptx::tmem_ld32(tcol + half * 32, v);
+                        ptx::tmem_wait_ld();
+                    }
                     if (row >= a.m) continue;
                     const int col0 = tn * K::BN + h * 64 + half * 32;
                     if (a.crt) {
                         // X = sum_i u_i M_i - t M exactly, t = round(sum_i u_i / q_i)
                         // (|X| <= M/4); X mod p = sum_i u_i (M_i mod p) + t (p - M mod p).
-                        const uint32_t q0 = a.cc.q[0], mu0 = a.cc.mu[0], off0 = a.cc.off31[0], v0 = a.cc.v[0];
+                        // Every u_i (i = 0 too) comes from this thread's scratch bytes.
 #pragma unroll
                         for (int cc = 0; cc < 4; ++cc) {      // 8 columns at a time (register budget)
                             unsigned long long S[8];
                             uint32_t F[8];
 #pragma unroll
                             for (int j = 0; j < 8; ++j) {
-                                const uint32_t u = mulmod_small(
-                                    residue_small(static_cast<int32_t>(v[cc * 8 + j]), q0, mu0, off0), v0, q0, mu0);
-                                S[j] = static_cast<unsigned long long>(u) * a.cc.W[0];
-                                F[j] = u * a.cc.R[0];
+                                S[j] = 0;
+                                F[j] = 0;
                             }
-                            const uint8_t* src = crt_plane(a, slot, 1) +
+                            const uint8_t* src = crt_plane(a, slot, 0) +
                                                  ((h * 4 + half * 2 + (cc >> 1)) * 128 + crow) * 16 + (cc & 1) * 8;
 #pragma unroll 1
-                            for (int g2 = 1; g2 < a.G; ++g2) {
-                                const uint2 x = *reinterpret_cast<const uint2*>(src + static_cast<size_t>(g2 - 1) * kCrtPlane);
+                            for (int g2 = 0; g2 < a.G; ++g2) {
+                                const uint2 x = *reinterpret_cast<const uint2*>(src + static_cast<size_t>(g2) * kCrtPlane);
                                 const uint32_t W = a.cc.W[g2], R = a.cc.R[g2];
 #pragma unroll
                                 for (int j = 0; j < 8; ++j) {
@@ -511,12 +535,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
             }
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) {
-                if (kPair == 2) ptx::mbar_arrive_cluster(slot ? accempty_leader1 : accempty_leader0);
-                else ptx::mbar_arrive(&sh->accempty[slot]);
-            }
+            if (!crt_final) release_slot<kPair>(sh, slot, lane, accempty_leader0, accempty_leader1);
             if (kTrace) {
                 const unsigned long long t2 = clk();
                 e_wait += t1 - t0;
@@ -662,7 +681,7 @@ int launch_impl(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A
     a.crt = pl.crt ? 1 : 0;
     a.cc = pl.cc;
     a.scratch = static_cast<uint8_t*>(scratch);
-    if (pl.crt && pl.cc.nq > 1 && !scratch) return FF_ERR_INTERNAL;
+    if (pl.crt && !scratch) return FF_ERR_INTERNAL;
     a.trace = nullptr;
     static unsigned long long* trace_buf = nullptr;
     const bool tracing = knobs().trace;
@@ -749,9 +768,9 @@ int launch_impl(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A
 }  // namespace
 
 size_t crt_scratch_bytes(const Plan& pl) {
-    if (!pl.crt || pl.cc.nq <= 1) return 0;
+    if (!pl.crt) return 0;
     // grid <= num_sms() CTAs (both kernels), 2 TMEM slots each
-    return static_cast<size_t>(num_sms()) * 2 * static_cast<size_t>(pl.cc.nq - 1) * kCrtPlane;
+    return static_cast<size_t>(num_sms()) * 2 * static_cast<size_t>(pl.cc.nq) * kCrtPlane;
 }
 
 int launch_gemm_tc_multi(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A_limbs,

@@ -127,9 +127,11 @@ size_t winograd_ws_bytes(const Plan& half, int64_t m, int64_t n, int64_t k);
 int run_winograd(const Plan& half, bool transA, bool transB, int64_t m, int64_t n, int64_t k, const int32_t* A,
                  int64_t lda, const int32_t* B, int64_t ldb, int32_t* C, int64_t ldc, void* ws, cudaStream_t st);
 
-// gemm_f64.cu: the paper-literal fp64 engine (workspace = two double planes)
-size_t f64_ws_bytes(const Plan& pl, int64_t m, int64_t n);
-int run_f64(const Plan& pl, bool transA, bool transB, int64_t m, int64_t n, int64_t k, const int32_t* A,
+// gemm_f64.cu: the paper-literal fp64 engine (workspace = two double planes; with
+// `levels` > 0 recursive Winograd levels without reduction, Sec. 3.2.3,
+// also the unreduced result and the recursion's temporaries)
+size_t f64_ws_bytes(const Plan& pl, int64_t m, int64_t n, int64_t k, int levels);
+int run_f64(const Plan& pl, int levels, bool transA, bool transB, int64_t m, int64_t n, int64_t k, const int32_t* A,
             int64_t lda, const int32_t* B, int64_t ldb, int32_t* C, int64_t ldc, void* ws, cudaStream_t st);
 
 // gen.cu

@@ -212,6 +212,19 @@ int make_f64_plan(int64_t k, const ff_opts& o, int64_t cmax, Plan& pl) {
     pl.korder = 1;
     I.korder = 1;
     pl.npairs = 0;
+    // Corollary 3.4, exact form (reading R21): l
+    // recursive Winograd levels without any reduction are safe while
+    // floor(k / 2^l) v_l^2 < 2^53, v_l = 3^l cmax (Theorem 3.1 on the balanced
+    // range [-cmax, cmax]), i.e. for k < k_winograd[l] = ceil(2^53 / v_l^2) 2^l.
+    for (int l = 1; l <= 3; ++l) {
+        const u128 v = (u128)cmax * (l == 1 ? 3 : l == 2 ? 9 : 27);
+        const u128 v2 = v * v;
+        const u128 two53 = (u128)1 << 53;
+        const u128 d = (two53 + v2 - 1) / v2;               // ceil(2^53 / v^2)
+        const u128 kw = d << l;
+        I.k_winograd[l] = kw > (u128)INT64_MAX ? INT64_MAX : (int64_t)kw;
+    }
+    I.k_winograd[0] = lam + 1;                              // l = 0: the dot-product bound, k <= lambda
     return 0;
 }
 
@@ -306,7 +319,8 @@ int make_plan(uint32_t p, int64_t k, const ff_opts* opts, Plan* out) {
     std::memset(&o, 0, sizeof(o));
     if (opts) o = *opts;
     if (o.scheme < FF_SCHEME_AUTO || o.scheme > FF_SCHEME_FP64) return FF_ERR_OPTS;
-    if (o.winograd < -1 || o.winograd > 1) return FF_ERR_OPTS;
+    if (o.winograd < -1 || o.winograd > 3) return FF_ERR_OPTS;
+    if (o.winograd > 1 && o.scheme != FF_SCHEME_FP64) return FF_ERR_OPTS;   // several levels: fp64 only
     if (o.kb_override < 0) return FF_ERR_OPTS;
     if (o.cta_group < 0 || o.cta_group > 2) return FF_ERR_OPTS;
     if (o.korder < 0 || o.korder > 2) return FF_ERR_OPTS;

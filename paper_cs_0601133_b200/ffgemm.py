@@ -42,7 +42,7 @@ class ff_plan_info(ctypes.Structure):
                 ("group_bound_max", _i64), ("kb_max", _i64), ("kb", _i64), ("k_pad", _i64),
                 ("num_kblocks", _i64), ("centre_max", _i32), ("reserved0", _i32),
                 ("carry_max", _i64), ("korder", _i32), ("nmod", _i32), ("moduli", _u32 * 16),
-                ("log2_M_floor", _i32), ("log2_bound_ceil", _i32)]
+                ("log2_M_floor", _i32), ("log2_bound_ceil", _i32), ("k_winograd", _i64 * 4)]
 
 
 _OPTS_P = ctypes.POINTER(ff_opts)
@@ -73,6 +73,7 @@ _SIGS = {
     "ff_prof_start": ([_i32], ctypes.c_int),
     "ff_prof_stop": ([_p, _i32, _p], ctypes.c_int),
     "ff_mma_ceiling": ([_i32, _p], ctypes.c_int),
+    "ff_gemm_winograd_levels": ([_u32, _i64, _i64, _i64, _OPTS_P, _p], ctypes.c_int),
 }
 for _name, (_args, _res) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -131,7 +132,7 @@ def ff_plan_query(p: int, k: int, opts=None) -> dict:
             "num_kblocks": info.num_kblocks, "centre_max": info.centre_max,
             "carry_max": info.carry_max, "korder": info.korder, "nmod": info.nmod,
             "moduli": list(info.moduli[:info.nmod]), "log2_M_floor": info.log2_M_floor,
-            "log2_bound_ceil": info.log2_bound_ceil}
+            "log2_bound_ceil": info.log2_bound_ceil, "k_winograd": list(info.k_winograd)}
 
 
 def ff_gemm(p, transA, transB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc) -> None:
@@ -149,6 +150,13 @@ def ff_gemm_ex(p, transA, transB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, 
     _check(_lib.ff_gemm_ex(p, _tr(transA), _tr(transB), m, n, k, alpha % 2 ** 32, _ptr(A), lda,
                            _ptr(B), ldb, beta % 2 ** 32, _ptr(C), ldc, _opts(opts),
                            _ptr(workspace), workspace_bytes, _stream(stream)), "ff_gemm_ex")
+
+
+def ff_gemm_winograd_levels(p, m, n, k, opts=None) -> int:
+    """Winograd levels ff_gemm_ex would use for this shape (host only)."""
+    lv = ctypes.c_int32(0)
+    _check(_lib.ff_gemm_winograd_levels(p, m, n, k, _opts(opts), ctypes.byref(lv)), "ff_gemm_winograd_levels")
+    return lv.value
 
 
 def ff_gemm_host(p, transA, transB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, opts=None) -> None:

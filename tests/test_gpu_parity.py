@@ -420,15 +420,30 @@ def test_baseline_config_sampled_rows_and_freivalds(env, name):
     assert out.min() >= 0 and out.max() < p
 
 
-@pytest.mark.parametrize("world,name", [(2, "c1"), (4, "c1"), (3, "mixed")])
+@pytest.mark.parametrize("world,name", [(2, "c1"), (4, "c1"), (3, "mixed"), (3, "c5int32"), (2, "c5wino"),
+                                        (3, "c3planes")])
 def test_row_panel_virtual_ranks_match_single_gpu(env, world, name):
-    """The multi-GPU row-panel path run as `world` virtual ranks on one GPU (B limbs
-    encoded by rank 0 and copied to the others, standing in for the broadcast):
-    the concatenated panels must equal the single-GPU result bit for bit."""
+    """The multi-GPU row-panel path run as `world` virtual ranks on one GPU (rank
+    0's broadcast buffers -- encoded planes, or int32 chunks of B -- copied to the
+    others, standing in for the NCCL broadcast): the concatenated panels must
+    equal the single-GPU result bit for bit.  c5int32 / c5wino are c5-shaped
+    (p = 2^26 - 5, CRT, alpha = -1, beta = 1): int32 broadcast with per-rank
+    encoding, and (forced Winograd) one ff_gemm_ex per panel with the local
+    one-level Winograd of SURVEY §8(e)."""
     torch, ff = env
     from paper_cs_0601133_b200.sharded import Problem, RowPanelGemm
+    opts, mode = None, None
     if name == "c1":
         p, m, n, k, tA, tB, alpha, beta = 65521, 512, 512, 512, "N", "N", 1, 0
+    elif name == "c5int32":
+        p, m, n, k, tA, tB, alpha, beta = 67108859, 1000, 1300, 777, "N", "N", 67108858, 1
+        mode = "int32"
+    elif name == "c5wino":
+        p, m, n, k, tA, tB, alpha, beta = 67108859, 2048, 1536, 1024, "N", "N", 67108858, 1
+        opts, mode = {"winograd": 1}, "int32"
+    elif name == "c3planes":
+        p, m, n, k, tA, tB, alpha, beta = 251, 1024, 768, 2048, "T", "N", 1, 0
+        mode = "planes"
     else:
         p, m, n, k, tA, tB, alpha, beta = 67108859, 700, 1100, 300, "T", "N", 67108858, 1
     rng = np.random.default_rng(world)
@@ -439,13 +454,18 @@ def test_row_panel_virtual_ranks_match_single_gpu(env, world, name):
     want = _dev(torch, C)
     ff.fgemm(p, dA, dB, want, alpha, beta, tA, tB)
     prob = Problem(p, m, n, k, tA, tB, alpha, beta)
-    engs = [RowPanelGemm(prob, chunks=3, world=world, rank=r) for r in range(world)]
+    engs = [RowPanelGemm(prob, chunks=3, world=world, rank=r, opts=opts, mode=mode or "auto")
+            for r in range(world)]
+    if mode:
+        assert all(e.mode == mode for e in engs)
+    if name == "c5wino":
+        assert all(e.whole for e in engs)
     out = _dev(torch, C)
     eng0 = engs[0]
     eng0.step(eng0.a_panel_view(dA), dB, out[eng0.row0:eng0.row1])
     torch.cuda.synchronize()
     for e in engs[1:]:
-        for dst, src in zip(e.Bl, eng0.Bl):
+        for dst, src in zip(e.bcast_buffers(), eng0.bcast_buffers()):
             dst.copy_(src)                       # stands in for the NCCL broadcast
         e.step(e.a_panel_view(dA), None, out[e.row0:e.row1])
     torch.cuda.synchronize()

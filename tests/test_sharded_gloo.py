@@ -41,10 +41,24 @@ def test_chunk_bounds():
 
 
 class ByteBackend:
-    """CPU stand-in for the CUDA library with the same call signatures."""
+    """CPU stand-in for the CUDA library with the same call signatures.
+    ``wino`` is what ff_gemm_winograd_levels reports (1: the rank multiplies
+    its whole panel with one ff_gemm_ex call)."""
 
-    def __init__(self):
+    def __init__(self, wino=0):
         self.calls = []
+        self.wino = wino
+
+    def ff_gemm_winograd_levels(self, p, m, n, k, opts=None):
+        return self.wino
+
+    def ff_gemm_ex(self, p, tA, tB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, opts=None,
+                   workspace=None, workspace_bytes=0, stream=None):
+        self.calls.append(("gemm_ex", m, n))
+        a = A.numpy() if tA in "Nn" else A.numpy()
+        out = oracle.fgemm(p, tA, tB, alpha, np.ascontiguousarray(a), np.ascontiguousarray(B.numpy()), beta,
+                           np.ascontiguousarray(C[:m, :n].numpy()), m=m, n=n, k=k)
+        C[:m, :n].copy_(torch.from_numpy(out))
 
     def ff_plan_query(self, p, k, opts=None):
         return {"L": 4, "k_pad": (k + 15) // 16 * 16}
@@ -76,52 +90,77 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, case, q):
+CASES = [
+    # encoded planes broadcast (forced: the stand-in has 4 planes per element)
+    (65521, 300, 700, 257, "N", "N", 1, 0, 3, "planes", 0),
+    (67108859, 257, 520, 100, "T", "N", 67108858, 1, 2, "planes", 0),
+    (251, 129, 300, 64, "N", "T", 3, 2, 4, "planes", 0),
+    # int32 broadcast, per-rank encode of every chunk (auto: 4 planes >= 4 bytes)
+    (67108859, 257, 520, 100, "T", "N", 67108858, 1, 3, "auto", 0),
+    (8388593, 300, 700, 257, "N", "T", 5, 7, 2, "auto", 0),
+    # int32 broadcast of all of B, one call per panel (the library would use Winograd)
+    (67108859, 300, 520, 129, "N", "N", 67108858, 1, 3, "auto", 1),
+    (251, 257, 300, 64, "T", "T", 3, 2, 2, "auto", 1),
+    # a rank with no rows (m smaller than one 128-row unit per rank)
+    (65521, 100, 300, 40, "N", "N", 1, 0, 2, "auto", 0),
+]
+
+
+def _worker(rank, world, port, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        p, m, n, k, tA, tB, alpha, beta, chunks = case
-        rng = np.random.default_rng(123)
-        A = rng.integers(0, p, size=(m, k) if tA == "N" else (k, m), dtype=np.int64).astype(np.int32)
-        B = rng.integers(0, p, size=(k, n) if tB == "N" else (n, k), dtype=np.int64).astype(np.int32)
-        C = rng.integers(0, p, size=(m, n), dtype=np.int64).astype(np.int32)
-        be = ByteBackend()
-        eng = RowPanelGemm(Problem(p, m, n, k, tA, tB, alpha, beta), chunks=chunks,
-                           device=torch.device("cpu"), backend=be)
-        At = torch.from_numpy(A)
-        Ap = eng.a_panel_view(At)
-        Bt = torch.from_numpy(B) if rank == 0 else None      # B lives on rank 0 only
-        Cp = torch.from_numpy(C[eng.row0:eng.row1].copy())
-        eng.step(Ap, Bt, Cp)
-        want = oracle.fgemm(p, tA, tB, alpha, A, B, beta, C)[eng.row0:eng.row1]
-        ok = np.array_equal(Cp.numpy(), want)
-        n_enc_b = sum(1 for c in be.calls if c[0] == "encode") - (1 if eng.mr else 0)
-        q.put((rank, ok, eng.row0, eng.row1, len(eng.chunks), n_enc_b))
+        for ci, case in enumerate(CASES):
+            p, m, n, k, tA, tB, alpha, beta, chunks, mode, wino = case
+            rng = np.random.default_rng(123 + ci)
+            A = rng.integers(0, p, size=(m, k) if tA == "N" else (k, m), dtype=np.int64).astype(np.int32)
+            B = rng.integers(0, p, size=(k, n) if tB == "N" else (n, k), dtype=np.int64).astype(np.int32)
+            C = rng.integers(0, p, size=(m, n), dtype=np.int64).astype(np.int32)
+            be = ByteBackend(wino)
+            eng = RowPanelGemm(Problem(p, m, n, k, tA, tB, alpha, beta), chunks=chunks,
+                               device=torch.device("cpu"), backend=be, mode=mode)
+            At = torch.from_numpy(A)
+            Ap = eng.a_panel_view(At)
+            Bt = torch.from_numpy(B) if rank == 0 else None      # B lives on rank 0 only
+            Cp = torch.from_numpy(C[eng.row0:eng.row1].copy())
+            eng.step(Ap, Bt, Cp)
+            want = oracle.fgemm(p, tA, tB, alpha, A, B, beta, C)[eng.row0:eng.row1]
+            ok = np.array_equal(Cp.numpy(), want)
+            n_enc = sum(1 for c in be.calls if c[0] == "encode")
+            n_ex = sum(1 for c in be.calls if c[0] == "gemm_ex")
+            q.put((ci, rank, ok, eng.row0, eng.row1, len(eng.chunks), n_enc, n_ex, eng.mode, eng.whole))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("case", [
-    (65521, 300, 700, 257, "N", "N", 1, 0, 3),
-    (67108859, 257, 520, 100, "T", "N", 67108858, 1, 2),
-    (251, 129, 300, 64, "N", "T", 3, 2, 4),
-])
-def test_row_panel_world2_gloo(case):
+def test_row_panel_world2_gloo():
+    """All CASES in one pair of gloo processes (spawn + torch import once)."""
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for pr in procs:
         pr.start()
-    res = sorted(q.get(timeout=120) for _ in range(world))
+    res = [q.get(timeout=300) for _ in range(world * len(CASES))]
     for pr in procs:
         pr.join(timeout=60)
         assert pr.exitcode == 0
-    m = case[1]
-    assert res[0][2] == 0 and res[-1][3] == m and res[0][3] == res[1][2]
-    for rank, ok, r0, r1, nchunks, n_enc_b in res:
-        assert ok, (rank, r0, r1)
-        # only rank 0 encodes B (one encode per chunk); the others receive limbs
-        assert n_enc_b == (nchunks if rank == 0 else 0)
+    for ci, case in enumerate(CASES):
+        rr = sorted(r[1:] for r in res if r[0] == ci)
+        m = case[1]
+        assert rr[0][2] == 0 and rr[-1][3] == m and rr[0][3] == rr[1][2], case
+        assert rr[0][4] == rr[1][4] and rr[0][8] == rr[1][8], case      # same chunking / mode on both ranks
+        for rank, ok, r0, r1, nchunks, n_enc, n_ex, mode, whole in rr:
+            assert ok, (case, rank, r0, r1)
+            has_rows = r1 > r0
+            if mode == "planes":
+                # only rank 0 encodes B (one encode per chunk); the others receive planes
+                assert n_enc == (nchunks if rank == 0 else 0) + (1 if has_rows else 0) and n_ex == 0, case
+            elif not whole:
+                # int32 chunks: every rank encodes its A panel and each chunk it receives
+                assert mode == "int32" and n_ex == 0, case
+                assert n_enc == ((1 + nchunks) if has_rows else 0), case
+            else:
+                assert mode == "int32" and n_enc == 0 and n_ex == (1 if has_rows else 0), case
