@@ -358,10 +358,10 @@ def roofline_entry(peaks, ops_per_launch, gemm_ms, elapsed_ms, kernel):
             "frac_of_sustained_peak": ach / peaks["sustained"]}
 
 
-def _kernel_name(ff, cfg, launches_per_step):
+def _kernel_name(ff, cfg, launches_per_step, launches_total_per_step):
     info = ff.ff_plan_query(cfg.p, cfg.k)
-    if cfg.p < 65536 and cfg.k <= 1024 and cfg.m * cfg.n <= (1 << 21):
-        return "small_gemm_canon_kernel (mma.sync byte products, p < 2^16 latency path)"
+    if launches_total_per_step == 1 and cfg.p < 65536:
+        return "lat_gemm_kernel (tcgen05.mma.kind::i8 byte products, split-K cluster, p < 2^16 latency path)"
     wino = " x7 (one Winograd level)" if launches_per_step == 7 else ""
     return "ffgemm_tc_kernel (tcgen05.mma.kind::i8, %s)%s" % (info["scheme"], wino)
 
@@ -393,7 +393,7 @@ def bench_single_config(ff, cfg, steps, warmup, peaks, dev, verify=True, with_cl
            "tensor_frac_of_step": ops_step / (ms / 1e3) / 1e12 / peaks["burst"],
            "l2": "flushed between steps (inputs < 2 x L2)" if flush else "inputs larger than L2 (no flush)",
            "roofline": roofline_entry(peaks, ops_step / n_gemm, gemm_ms, elapsed,
-                                      _kernel_name(ff, cfg, n_gemm))}
+                                      _kernel_name(ff, cfg, n_gemm, launches / steps))}
     if clk:
         rec["clocks"] = clk.summary()
     if verify:

@@ -113,8 +113,10 @@ typedef struct ff_opts {
                                canonical residue in [0, p) (C may still be any int32): for
                                p < 2^16 short-K products may then stream A and B raw
                                (DESIGN.md §4.10).  Results are undefined if violated. */
-    int32_t small_path;     /* small-field latency kernels: 0 by the size
-                               rule, 1 whenever they apply, -1 never (results are identical) */
+    int32_t small_path;     /* latency kernels for small fields: 0 by the
+                               size rule, 1 the mma.sync kernels whenever they apply, 2 the
+                               tcgen05 split-K kernel whenever it applies, -1 never (results
+                               are identical) */
     int32_t reserved[1];
 } ff_opts;
 

@@ -155,9 +155,22 @@ namespace {
 // The whole path on device pointers.
 // Small-field latency path (gemm_small.cu) for short K and small problems:
 // FF_SMALL=0 never, FF_SMALL=1 whenever valid (experiments); default by size.
+// The tcgen05 latency kernel (gemm_lat.cu): small_path = 2 forces it, 0 / 1 exclude it.
+bool prefer_lat(const Plan& pl, int64_t m, int64_t n, int64_t k) {
+    const int mode = pl.small_mode;
+    if (mode >= 0) return mode == 2;
+    // measured (p = 65521, alpha = -1, beta = 1, one B200): it wins while
+    // one wave of 128 x 64 tiles covers the output and each CTA has a few K chunks --
+    // 512^3 18 vs 27 us (mma.sync) / 42 us (encoders + tcgen05), 256^2 x 4096 31 vs 76 us,
+    // 128 x 8192 x 1024 51 vs 58 us; below K = 256 the mma.sync kernels are faster
+    // (128^3: 14 vs 20 us), beyond one wave the encoder + tcgen05 path (4096^2 x 128)
+    const int64_t tiles = ((m + 127) / 128) * ((n + 63) / 64);
+    return k >= 256 && tiles <= num_sms() && tiles * ((k + 127) / 128) <= 1024;
+}
+
 bool prefer_small(const Plan& pl, int64_t m, int64_t n, int64_t k) {
     const int mode = pl.small_mode;
-    if (mode >= 0) return mode > 0;
+    if (mode >= 0) return mode == 1;
     // measured (p = 65521, alpha = -1, beta = 1): 128^3 19.9 vs 31.5 us, 128 x 8192 x 128
     // 21.9 vs 33.3 us; but 512^3 40.8 vs 36.4 us, 128 x 8192 x 1024 98 vs 51 us and
     // 4096^2 x 128 233 vs 90 us -- the tcgen05 path wins beyond short K and ~2M outputs
@@ -167,7 +180,7 @@ bool prefer_small(const Plan& pl, int64_t m, int64_t n, int64_t k) {
 // The cp.async variant for canonical operands (internal callers): FF_SMALL as above.
 bool prefer_small_canon(const Plan& pl, int64_t m, int64_t n, int64_t k) {
     const int mode = pl.small_mode;
-    if (mode >= 0) return mode > 0;
+    if (mode >= 0) return mode == 1;
     // measured against the tcgen05 path (p = 65521, alpha = -1, beta = 1): 512^3 21 vs
     // 36 us, 128 x 8192 x 128 20 vs 33 us, 128 x 8192 x 1024 51 vs 51 us, 1024^3
     // 51 vs 41 us, 4096^2 x 128 146 vs 90 us
@@ -177,7 +190,7 @@ bool prefer_small_canon(const Plan& pl, int64_t m, int64_t n, int64_t k) {
 // The same for 2^16 <= p < 2^31 (3-4 bytes per residue): FF_SMALL as above.
 bool prefer_small_wide(const Plan& pl, int64_t m, int64_t n, int64_t k) {
     const int mode = pl.small_mode;
-    if (mode >= 0) return mode > 0;
+    if (mode >= 0) return mode == 1;
     return k <= 1024 && m * n <= (int64_t{1} << 21) && m * n * k < (int64_t{1} << 29);
 }
 
@@ -197,6 +210,9 @@ int run(const Plan& pl, char transA, char transB, int64_t m, int64_t n, int64_t 
     const auto sc = span(C, m, n, ldc);
     const bool c_disjoint = (sc.second <= sa.first || sa.second <= sc.first) &&
                             (sc.second <= sb.first || sb.second <= sc.first);
+    // the tcgen05 latency kernel: one launch, no encoders (C must not overlap A, B)
+    if (pl.all_auto && c_disjoint && lat_path_ok(pl, m, n, k) && prefer_lat(pl, m, n, k))
+        return launch_gemm_lat(pl, is_t(transA), is_t(transB), m, n, k, A, lda, B, ldb, C, ldc, st);
     // (the canonical-input variants handle overlap with a grid barrier instead)
     if (pl.all_auto && small_canon_ok(pl, is_t(transA), is_t(transB), m, n, k, A, lda, B, ldb) &&
         prefer_small_canon(pl, m, n, k)) {

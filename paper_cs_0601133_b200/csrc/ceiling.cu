@@ -25,8 +25,13 @@ __global__ void __launch_bounds__(128, 1) mma_ceiling_kernel(int iters, uint32_t
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* done = reinterpret_cast<uint64_t*>(smem + kStagesC * kStageBytes);
     uint32_t* holder = reinterpret_cast<uint32_t*>(done + 1);
-    for (int i = threadIdx.x; i < kStagesC * kStageBytes / 4; i += blockDim.x)
-        reinterpret_cast<uint32_t*>(smem)[i] = 0x01010101u * (i & 7);
+    // random operand bytes: the tensor core's power (hence the clock it sustains
+    // under the 1 kW cap) depends on how many operand bits toggle
+    for (int i = threadIdx.x; i < kStagesC * kStageBytes / 4; i += blockDim.x) {
+        uint32_t z = static_cast<uint32_t>(i) * 0x9E3779B9u + blockIdx.x * 0x85EBCA6Bu;
+        z ^= z >> 16; z *= 0x7FEB352Du; z ^= z >> 15; z *= 0x846CA68Bu; z ^= z >> 16;
+        reinterpret_cast<uint32_t*>(smem)[i] = z;
+    }
     const int warp = threadIdx.x / 32;
     if (threadIdx.x == 0) {
         ptx::mbar_init(done, 1);

@@ -72,7 +72,8 @@ struct Plan {
     uint32_t kinv, kinv_sh;          // 256^-(G-1) mod p and its Shoup constant (k-outer carry)
     bool all_auto;                   // no option forced: the planner may route to the small-field path
     bool canonical_ab;               // (internal callers) A, B hold canonical residues in [0, p)
-    int small_mode;                  // small-field kernels: -1 size rule, 0 never, 1 whenever valid
+    int small_mode;                  // small-field kernels: -1 size rule, 0 never, 1 mma.sync kernels
+                                     // whenever valid, 2 the tcgen05 latency kernel whenever valid
 };
 
 constexpr int64_t kKbLocalityBytes = 8192;  // L * kb per row-slice in k-outer order (swept on c4, c5)
@@ -109,6 +110,11 @@ bool small_wide_ok(const Plan& pl, bool tA, bool tB, int64_t m, int64_t n, int64
                    const int32_t* B, int64_t ldb);
 int launch_gemm_small_wide(const Plan& pl, int64_t m, int64_t n, int64_t k, const int32_t* A, int64_t lda,
                            const int32_t* B, int64_t ldb, int32_t* C, int64_t ldc, bool alias, cudaStream_t st);
+
+// gemm_lat.cu: p < 2^16 latency path on tcgen05 (one kernel, split-K cluster, no encoders)
+bool lat_path_ok(const Plan& pl, int64_t m, int64_t n, int64_t k);
+int launch_gemm_lat(const Plan& pl, bool tA, bool tB, int64_t m, int64_t n, int64_t k, const int32_t* A, int64_t lda,
+                    const int32_t* B, int64_t ldb, int32_t* C, int64_t ldc, cudaStream_t st);
 
 // gemm_tc.cu
 struct OutSpec {          // C <- (a * A B + b * C) mod p for one output block

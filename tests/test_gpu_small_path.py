@@ -154,3 +154,52 @@ def test_streaming_kernel_reduces_raw_operands(env, p):
         ff.ff_gemm_ex(p, "N", "N", m, k, k, 1, dX, k, dW, k, 0, dX, k, {"small_path": mode})
         torch.cuda.synchronize()
         np.testing.assert_array_equal(dX.cpu().numpy(), want, err_msg="in place, mode %d" % mode)
+
+
+# ---------------------------------------------------------------- tcgen05 latency kernel (gemm_lat.cu)
+
+@pytest.mark.parametrize("p", [2, 3, 251, 257, 4099, 65521])
+@pytest.mark.parametrize("tA,tB", [("N", "N"), ("T", "N"), ("N", "T"), ("T", "T")])
+def test_lat_kernel_vs_oracle(env, p, tA, tB):
+    """The one-launch tcgen05 kernel (split-K cluster, DSMEM reduction, coalesced
+    epilogue) forced on (small_path = 2): any int32 inputs, ragged shapes across
+    tile / chunk / cluster boundaries, every transpose; bit-exact vs the oracle
+    and bit-identical to the encoder + tcgen05 path (small_path = -1)."""
+    torch, ff = env
+    rng = np.random.default_rng(p * 7 + ord(tA) + 3 * ord(tB))
+    for (m, n, k) in [(1, 1, 1), (5, 3, 7), (128, 64, 128), (129, 65, 129), (512, 512, 512), (200, 300, 1000),
+                      (64, 1000, 2048), (300, 70, 5000)]:
+        ar, ac = (m, k) if tA == "N" else (k, m)
+        br, bc = (k, n) if tB == "N" else (n, k)
+        A = rng.integers(-2 ** 31, 2 ** 31, size=(ar, ac + 3), dtype=np.int64).astype(np.int32)
+        B = rng.integers(-2 ** 31, 2 ** 31, size=(br, bc + 1), dtype=np.int64).astype(np.int32)
+        C = rng.integers(-2 ** 31, 2 ** 31, size=(m, n + 2), dtype=np.int64).astype(np.int32)
+        for alpha, beta in [(1, 0), (p - 1, 1), (int(rng.integers(0, p)), int(rng.integers(0, p)))]:
+            want = oracle.fgemm(p, tA, tB, alpha, A[:, :ac], B[:, :bc], beta, C[:, :n], m=m, n=n, k=k)
+            outs = []
+            for mode in (2, -1):
+                dA, dB, dC = (torch.from_numpy(x).cuda() for x in (A, B, C))
+                ff.ff_gemm_ex(p, tA, tB, m, n, k, alpha, dA, A.shape[1], dB, B.shape[1], beta, dC, C.shape[1],
+                              {"small_path": mode})
+                torch.cuda.synchronize()
+                got = dC.cpu().numpy()
+                np.testing.assert_array_equal(got[:, :n], want, err_msg="mode %d %dx%dx%d" % (mode, m, n, k))
+                np.testing.assert_array_equal(got[:, n:], C[:, n:])
+                outs.append(got)
+            np.testing.assert_array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("m,n", [(64, 64), (1024, 1024)])
+def test_lat_kernel_at_the_s32_bound(env, m, n):
+    """K = 16384 (the kernel's limit) with every residue p - 1 = 0xFFF0: the middle
+    weight group of a CTA reaches 2 K 240 255 ~ 2^31 when one CTA takes all of K
+    (1024^2: enough tiles that the cluster is 1 CTA); (p-1)^2 = 1 mod p gives
+    the closed form (AB)_ij = K mod p (oracle pin, tests/test_oracle_pins.py)."""
+    torch, ff = env
+    p, k = 65521, 16384
+    dA = torch.full((m, k), p - 1, dtype=torch.int32, device="cuda")
+    dB = torch.full((k, n), p - 1, dtype=torch.int32, device="cuda")
+    dC = torch.zeros((m, n), dtype=torch.int32, device="cuda")
+    ff.ff_gemm_ex(p, "N", "N", m, n, k, 1, dA, k, dB, n, 0, dC, n, {"small_path": 2})
+    torch.cuda.synchronize()
+    assert bool((dC == k % p).all())
