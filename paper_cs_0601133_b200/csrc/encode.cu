@@ -271,6 +271,11 @@ __device__ __forceinline__ CrtDigitsIn crt_split(int32_t c) {
     return d;
 }
 
+// The low bytes of four words, in order, in one word (three byte permutes).
+__device__ __forceinline__ uint32_t pack_lo4(uint32_t x0, uint32_t x1, uint32_t x2, uint32_t x3) {
+    return __byte_perm(__byte_perm(x0, x1, 0x0040), __byte_perm(x2, x3, 0x0040), 0x5410);
+}
+
 __device__ __forceinline__ uint32_t crt_digit(int32_t c, const CrtDigitsIn& d, const CrtConsts& C, int i) {
     if (C.q[i] == 256u) return static_cast<uint32_t>(c) & 0xFFu;
     const float s = fmaf(d.h1, C.fw15[i], d.h0);
@@ -316,21 +321,22 @@ __global__ void __launch_bounds__(256) encode_crt_direct_kernel(ModP M, CrtConst
             uint32_t w0[4];
 #pragma unroll
             for (int q4 = 0; q4 < 4; ++q4)
-                w0[q4] = (static_cast<uint32_t>(c[4 * q4]) & 0xFFu) | ((static_cast<uint32_t>(c[4 * q4 + 1]) & 0xFFu) << 8) |
-                         ((static_cast<uint32_t>(c[4 * q4 + 2]) & 0xFFu) << 16) | (static_cast<uint32_t>(c[4 * q4 + 3]) << 24);
+                w0[q4] = pack_lo4(c[4 * q4], c[4 * q4 + 1], c[4 * q4 + 2], c[4 * q4 + 3]);
             *reinterpret_cast<uint4*>(dst) = make_uint4(w0[0], w0[1], w0[2], w0[3]);
 #pragma unroll 1
             for (int i = 1; i < C.nq; ++i) {
                 const float fq = C.fq[i], fi = C.finv[i], fw = C.fw15[i];
-                uint32_t w[4] = {0, 0, 0, 0};
+                uint32_t b[16];
 #pragma unroll
                 for (int t = 0; t < 16; ++t) {
                     const float sv = fmaf(dg[t].h1, fw, dg[t].h0);
                     const float tq = fmaf(sv, fi, 12582912.0f) - 12582912.0f;
                     const float rr = fmaf(-fq, tq, sv);
-                    w[t >> 2] |= (__float_as_uint(rr + 12582912.0f) & 0xFFu) << (8 * (t & 3));
+                    b[t] = __float_as_uint(rr + 12582912.0f);      // the residue's byte is the low byte
                 }
-                *reinterpret_cast<uint4*>(dst + i * plane) = make_uint4(w[0], w[1], w[2], w[3]);
+                *reinterpret_cast<uint4*>(dst + i * plane) =
+                    make_uint4(pack_lo4(b[0], b[1], b[2], b[3]), pack_lo4(b[4], b[5], b[6], b[7]),
+                               pack_lo4(b[8], b[9], b[10], b[11]), pack_lo4(b[12], b[13], b[14], b[15]));
             }
         }
     }
@@ -484,22 +490,23 @@ __global__ void __launch_bounds__(256) encode_crt_trans_tma_kernel(const __grid_
 #pragma unroll
             for (int g = 0; g < 4; ++g)
                 *reinterpret_cast<uint32_t*>(&tile[0][r][kg * 16 + 4 * g]) =
-                    (static_cast<uint32_t>(c[4 * g]) & 0xFFu) | ((static_cast<uint32_t>(c[4 * g + 1]) & 0xFFu) << 8) |
-                    ((static_cast<uint32_t>(c[4 * g + 2]) & 0xFFu) << 16) | (static_cast<uint32_t>(c[4 * g + 3]) << 24);
+                    pack_lo4(c[4 * g], c[4 * g + 1], c[4 * g + 2], c[4 * g + 3]);
         }
 #pragma unroll 1
         for (int pl = 1; pl < nq; ++pl) {
             const float fq = C.fq[pl], fi = C.finv[pl], fw = C.fw15[pl];
-            uint32_t w[4] = {0, 0, 0, 0};
+            uint32_t b[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
                 const float sv = fmaf(dg[i].h1, fw, dg[i].h0);
                 const float tq = fmaf(sv, fi, 12582912.0f) - 12582912.0f;
                 const float rr = fmaf(-fq, tq, sv);
-                w[i >> 2] |= (__float_as_uint(rr + 12582912.0f) & 0xFFu) << (8 * (i & 3));
+                b[i] = __float_as_uint(rr + 12582912.0f);
             }
 #pragma unroll
-            for (int g = 0; g < 4; ++g) *reinterpret_cast<uint32_t*>(&tile[pl][r][kg * 16 + 4 * g]) = w[g];
+            for (int g = 0; g < 4; ++g)
+                *reinterpret_cast<uint32_t*>(&tile[pl][r][kg * 16 + 4 * g]) =
+                    pack_lo4(b[4 * g], b[4 * g + 1], b[4 * g + 2], b[4 * g + 3]);
         }
         __syncthreads();
         const int64_t rr = (t % tiles_r) * kTR + wr;

@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int pi = a.group_first[g]; pi < a.group_first[g] + a.group_len[g]; ++pi) {
                     const int li = a.pair_i[pi], lj = a.pair_j[pi];
                     for (int ks = ks0; ks < ks1; ++ks) {
-                        ptx::mbar_wait(&sh->empty[stage], phase ^ 1);
+                        ptx::mbar_wait_sleep(&sh->empty[stage], phase ^ 1);
                         uint8_t* sa = smem + stage * K::STAGE;
                         if (kPair == 1) {
                             ptx::mbar_arrive_expect_tx(&sh->full[stage], K::STAGE);
@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         unsigned long long e_wait = 0, e_busy = 0, e_final = 0;
         for_each_step(a, unit, nunits, tbase, tcount, [&](int tile, int slot, int g, int kb) {
             const unsigned long long t0 = kTrace ? clk() : 0;
-            ptx::mbar_wait(&sh->accfull[slot], acc_par[slot]);
+            ptx::mbar_wait_sleep(&sh->accfull[slot], acc_par[slot]);
             const unsigned long long t1 = kTrace ? clk() : 0;
             acc_par[slot] ^= 1;
             ptx::tc_fence_after();

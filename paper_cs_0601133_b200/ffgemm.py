@@ -13,6 +13,9 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libffgemm.so")
+# development A/B runs only: load another build of the same library (same ABI)
+if os.environ.get("FF_LIB_OVERRIDE"):
+    LIB_PATH = os.environ["FF_LIB_OVERRIDE"]
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
