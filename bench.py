@@ -396,6 +396,16 @@ def bench_single_config(ff, cfg, steps, warmup, peaks, dev, verify=True, with_cl
                                       _kernel_name(ff, cfg, n_gemm, launches / steps))}
     if clk:
         rec["clocks"] = clk.summary()
+        if rec["clocks"].get("samples", 0) < 3:
+            # a short timed region: sample the clocks over ~0.6 s of the same steps (untimed)
+            with ClockSampler(local) as clk2:
+                time.sleep(0.3)
+                t_end = time.perf_counter() + 0.6
+                while time.perf_counter() < t_end:
+                    for _ in range(20):
+                        eng.step()
+                    torch.cuda.synchronize()
+            rec["clocks"] = dict(clk2.summary(), window="0.6 s of repeated steps after the timed region")
     if verify:
         eng.reset_c()
         eng.step()

@@ -98,6 +98,7 @@ struct GemmArgs {
 // laid out [h: 64-column quarter][c: 16-column chunk][row 0..127][16 bytes] so
 // that a warp's 32 rows store / load 512 contiguous bytes per instruction.
 constexpr int kCrtPlane = 128 * kTileN;
+constexpr int kCrtBatch = 5;    // scratch bytes of this many moduli loaded together in the final step
 
 __device__ __forceinline__ uint8_t* crt_plane(const GemmArgs& a, int slot, int g) {
     return a.scratch + (static_cast<size_t>(blockIdx.x * 2 + slot) * a.G + g) * kCrtPlane;
@@ -145,6 +146,79 @@ __device__ __forceinline__ void for_each_step(const GemmArgs& a, int unit, int n
             for (int g = a.G - 1; g >= 0; --g)
                 for (int kb = 0; kb < a.nkb; ++kb)
                     for (int s = 0; s < nslots; ++s) f(base + (s == 0 ? t0 : t1), s, g, kb);
+        }
+    }
+}
+
+// One 8-column group of the final step of a CRT tile, for one thread (one row of
+// its 64-column quarter), after the accumulator has been released: X = sum_i u_i
+// M_i - t M exactly, t = round(sum_i u_i / q_i) (|X| <= M/4), X mod p =
+// sum_i u_i (M_i mod p) + t (p - M mod p), every u_i from this thread's scratch
+// bytes; then every output C_q <- (a_q X + b_q C_q) mod p for these columns.
+// plane0: this thread's bytes in modulus 0's scratch plane; grp = 0..7.
+__device__ __forceinline__ void crt_group(const GemmArgs& a, const ModP& M, const uint8_t* plane0, int row, int col_q,
+                                          int grp) {
+    if (row >= a.m) return;
+    const int col0 = col_q + grp * 8;
+    const uint8_t* src = plane0 + (grp >> 1) * 128 * 16 + (grp & 1) * 8;
+    unsigned long long S[8];
+    uint32_t F[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { S[j] = 0; F[j] = 0; }
+#pragma unroll 1
+    for (int g0 = 0; g0 < a.G; g0 += kCrtBatch) {
+        // a batch of moduli's bytes in flight together (one L2 round trip per batch)
+        uint2 xb[kCrtBatch];
+#pragma unroll
+        for (int b = 0; b < kCrtBatch; ++b)
+            xb[b] = (g0 + b < a.G) ? *reinterpret_cast<const uint2*>(src + static_cast<size_t>(g0 + b) * kCrtPlane)
+                                   : make_uint2(0, 0);
+#pragma unroll
+        for (int b = 0; b < kCrtBatch; ++b) {
+            if (g0 + b >= a.G) break;
+            const uint32_t W = a.cc.W[g0 + b], R = a.cc.R[g0 + b];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const uint32_t u = ((j < 4 ? xb[b].x : xb[b].y) >> (8 * (j & 3))) & 0xFFu;
+                S[j] += static_cast<unsigned long long>(u) * W;
+                F[j] += u * R;
+            }
+        }
+    }
+    uint32_t X[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const uint32_t t = (F[j] + (1u << 23)) >> 24;
+        X[j] = residue_u64(S[j] + static_cast<unsigned long long>(t) * a.cc.Mneg, a.cc.mu64, M.p);
+    }
+#pragma unroll 1
+    for (int qo = 0; qo < a.nout; ++qo) {
+        const GemmOut O = a.out[qo];
+        int32_t* cr = O.C + static_cast<int64_t>(row) * a.ldc + col0;
+        const bool full = O.vec && (col0 + 8 <= a.n);
+        uint32_t o[8];
+        if (O.b != 0) {
+            if (full) {
+                const int4 x0 = *reinterpret_cast<const int4*>(cr), x1 = *reinterpret_cast<const int4*>(cr + 4);
+                o[0] = x0.x; o[1] = x0.y; o[2] = x0.z; o[3] = x0.w; o[4] = x1.x; o[5] = x1.y; o[6] = x1.z; o[7] = x1.w;
+            } else {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) o[j] = (col0 + j < a.n) ? cr[j] : 0;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            uint32_t r = mulmod_shoup(X[j], O.a, O.a_sh, M.p);
+            if (O.b != 0) r = addmod(r, mulmod_shoup(residue_i32(static_cast<int32_t>(o[j]), M), O.b, O.b_sh, M.p), M.p);
+            o[j] = r;
+        }
+        if (full) {
+            *reinterpret_cast<int4*>(cr) = make_int4(o[0], o[1], o[2], o[3]);
+            *reinterpret_cast<int4*>(cr + 4) = make_int4(o[4], o[5], o[6], o[7]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (col0 + j < a.n) cr[j] = static_cast<int32_t>(o[j]);
         }
     }
 }
@@ -354,9 +428,36 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t accempty_leader1 = kPair == 2 ? ptx::mapa(ptx::smem_u32(&sh->accempty[1]), 0) : 0;
         uint32_t acc_par[2] = {0, 0};
         unsigned long long e_wait = 0, e_busy = 0, e_final = 0;
+        // CRT plans: the final step of a tile only stores u_0 and releases TMEM; its
+        // reconstruction + outputs (8 groups of 8 columns) are deferred and done while
+        // this thread would otherwise wait for the next accumulator, so that they never
+        // hold back the release of a slot the MMA needs.
+        int pend_tile[2] = {0, 0}, pend_grp[2] = {8, 8};
+        auto pend_work = [&](int ps) {
+            int tm, tn;
+            tile_coords(a, pend_tile[ps], tm, tn);
+            const int row = tm * K::BM + static_cast<int>(rank) * 128 + q * 32 + static_cast<int>(lane);
+            const int crow = q * 32 + static_cast<int>(lane);
+            crt_group(a, M, crt_plane(a, ps, 0) + (h * 4 * 128 + crow) * 16, row, tn * K::BN + h * 64, pend_grp[ps]);
+            ++pend_grp[ps];
+        };
         for_each_step(a, unit, nunits, tbase, tcount, [&](int tile, int slot, int g, int kb) {
             const unsigned long long t0 = kTrace ? clk() : 0;
-            ptx::mbar_wait_sleep(&sh->accfull[slot], acc_par[slot]);
+            if (a.crt) {
+                // this slot's pending work must finish before its scratch is reused
+                for (;;) {
+                    const bool ready = ptx::mbar_test(&sh->accfull[slot], acc_par[slot]);
+                    const int ps = pend_grp[slot] < 8 ? slot : (pend_grp[slot ^ 1] < 8 ? (slot ^ 1) : -1);
+                    if (ready && ps != slot) break;
+                    if (ps < 0) {
+                        ptx::mbar_wait_sleep(&sh->accfull[slot], acc_par[slot]);
+                        break;
+                    }
+                    pend_work(ps);
+                }
+            } else {
+                ptx::mbar_wait_sleep(&sh->accfull[slot], acc_par[slot]);
+            }
             const unsigned long long t1 = kTrace ? clk() : 0;
             acc_par[slot] ^= 1;
             ptx::tc_fence_after();
@@ -441,6 +542,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 ptx::tmem_st64(tcol, v);
                 ptx::tmem_wait_st();
+            } else if (a.crt) {
+                pend_tile[slot] = tile;        // deferred: see pend_work
+                pend_grp[slot] = 0;
             } else {
                 int tm, tn;
                 tile_coords(a, tile, tm, tn);
@@ -448,52 +552,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
                 for (int half = 0; half < 2; ++half) {
                     uint32_t v[32];
-                    if (a.crt) {       // (the accumulator was released: everything comes from scratch)
-#pragma unroll
-                        for (int t = 0; t < 32; ++t) v[t] = 0;
-                    } else {
-                        ptx::tmem_ld32(tcol + half * 32, v);
-                        ptx::tmem_wait_ld();
-                    }
+                    ptx::tmem_ld32(tcol + half * 32, v);
+                    ptx::tmem_wait_ld();
                     if (row >= a.m) continue;
                     const int col0 = tn * K::BN + h * 64 + half * 32;
-                    if (a.crt) {
-                        // X = sum_i u_i M_i - t M exactly, t = round(sum_i u_i / q_i)
-                        // (|X| <= M/4); X mod p = sum_i u_i (M_i mod p) + t (p - M mod p).
-                        // Every u_i (i = 0 too) comes from this thread's scratch bytes.
 #pragma unroll
-                        for (int cc = 0; cc < 4; ++cc) {      // 8 columns at a time (register budget)
-                            unsigned long long S[8];
-                            uint32_t F[8];
-#pragma unroll
-                            for (int j = 0; j < 8; ++j) {
-                                S[j] = 0;
-                                F[j] = 0;
-                            }
-                            const uint8_t* src = crt_plane(a, slot, 0) +
-                                                 ((h * 4 + half * 2 + (cc >> 1)) * 128 + crow) * 16 + (cc & 1) * 8;
-#pragma unroll 1
-                            for (int g2 = 0; g2 < a.G; ++g2) {
-                                const uint2 x = *reinterpret_cast<const uint2*>(src + static_cast<size_t>(g2) * kCrtPlane);
-                                const uint32_t W = a.cc.W[g2], R = a.cc.R[g2];
-#pragma unroll
-                                for (int j = 0; j < 8; ++j) {
-                                    const uint32_t u = ((j < 4 ? x.x : x.y) >> (8 * (j & 3))) & 0xFFu;
-                                    S[j] += static_cast<unsigned long long>(u) * W;
-                                    F[j] += u * R;
-                                }
-                            }
-#pragma unroll
-                            for (int j = 0; j < 8; ++j) {
-                                const uint32_t t = (F[j] + (1u << 23)) >> 24;
-                                v[cc * 8 + j] = residue_u64(S[j] + static_cast<unsigned long long>(t) * a.cc.Mneg,
-                                                            a.cc.mu64, M.p);
-                            }
-                        }
-                    } else {
-#pragma unroll
-                        for (int t = 0; t < 32; ++t) v[t] = residue_i32(static_cast<int32_t>(v[t]), M);  // exact R
-                    }
+                    for (int t = 0; t < 32; ++t) v[t] = residue_i32(static_cast<int32_t>(v[t]), M);  // exact R
+
 #pragma unroll 1
                     for (int qo = 0; qo < a.nout; ++qo) {
                         const GemmOut O = a.out[qo];
@@ -542,6 +607,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (final_step) e_final += t2 - t1; else e_busy += t2 - t1;
             }
         });
+        for (int ps = 0; ps < 2; ++ps)
+            while (pend_grp[ps] < 8) pend_work(ps);
         if (kTrace && warp == 2 && lane == 0) {
             unsigned long long* tr = a.trace + blockIdx.x * 8;
             tr[4] = e_wait;   // epilogue waiting for an accumulator
