@@ -4,7 +4,7 @@ timed with CUDA events; reports the C read+write bandwidth.  Development aid.
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch  # noqa: E402
 
 import paper_cs_0601133_b200 as ff  # noqa: E402

@@ -3,7 +3,7 @@ on a grid of shapes (p = 65521), CUDA events.  Run once per setting.  Developmen
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch  # noqa: E402
 
 import paper_cs_0601133_b200 as ff  # noqa: E402

@@ -3,7 +3,7 @@ row block of an n x n matrix (ld = n), in place (C = B).  Development aid."""
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch  # noqa: E402
 
 import paper_cs_0601133_b200 as ff  # noqa: E402
