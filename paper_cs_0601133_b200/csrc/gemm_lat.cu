@@ -268,8 +268,8 @@ __global__ void __launch_bounds__(kLThreads, 1) lat_gemm_kernel(const __grid_con
             const unsigned long long x = static_cast<unsigned long long>(v0[t]) +
                                          (static_cast<unsigned long long>(v1[t]) << 8) +
                                          (static_cast<unsigned long long>(v2[t]) << 16);
-            // swizzle the column by the row to spread banks (read back by rows below)
-            part[row * kLN + ((c0 + t) ^ ((row & 7) << 2))] = residue_u64(x, a.mu64, p);
+            // column XOR (row mod 32): the 32 rows of a warp hit 32 banks (read back by rows below)
+            part[row * kLN + ((c0 + t) ^ (row & 31))] = residue_u64(x, a.mu64, p);
         }
     }
     ptx::tc_fence_before();
@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(kLThreads, 1) lat_gemm_kernel(const __grid_con
         const int r = rA + warp + j * kLWarps, gr = m0 + r;
         if (r >= rB || gr >= a.m) continue;
         uint32_t acc0 = 0, acc1 = 0;
-        const int sc0 = c2 ^ ((r & 7) << 2), sc1 = (c2 + 1) ^ ((r & 7) << 2);
+        const int sc0 = c2 ^ (r & 31), sc1 = (c2 + 1) ^ (r & 31);
         if (S == 1) {
             acc0 = part[r * kLN + sc0];
             acc1 = part[r * kLN + sc1];

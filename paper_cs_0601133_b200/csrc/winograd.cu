@@ -42,27 +42,59 @@ __global__ void __launch_bounds__(256) preadd_kernel(ModP M, int which, int64_t 
                                                      const int32_t* __restrict__ q21, const int32_t* __restrict__ q22,
                                                      int64_t ld, int32_t* __restrict__ o1, int32_t* __restrict__ o2,
                                                      int32_t* __restrict__ o3, int32_t* __restrict__ o4) {
+    auto sums = [&](int32_t a11, int32_t a12, int32_t a21, int32_t a22, uint32_t (&s)[4]) {
+        const uint32_t x11 = residue_i32(a11, M), x12 = residue_i32(a12, M);
+        const uint32_t x21 = residue_i32(a21, M), x22 = residue_i32(a22, M);
+        if (which == 0) {
+            s[0] = addmod(x21, x22, M.p);      // S1 = A21 + A22
+            s[1] = submod(s[0], x11, M.p);     // S2 = S1 - A11
+            s[2] = submod(x11, x21, M.p);      // S3 = A11 - A21
+            s[3] = submod(x12, s[1], M.p);     // S4 = A12 - S2
+        } else {
+            s[0] = submod(x12, x11, M.p);      // T1 = B12 - B11
+            s[1] = submod(x22, s[0], M.p);     // T2 = B22 - T1
+            s[2] = submod(x22, x12, M.p);      // T3 = B22 - B12
+            s[3] = submod(s[1], x21, M.p);     // T4 = T2 - B21
+        }
+    };
+    // 16-byte accesses (4 elements per thread) when every row of every operand is
+    // 16-byte aligned: the kernel is HBM-bound (4 x 4 B read + 4 x 4 B written per element)
+    const bool vec = (ld % 4 == 0) && (cols % 4 == 0) &&
+                     ((reinterpret_cast<uintptr_t>(q11) | reinterpret_cast<uintptr_t>(q12) |
+                       reinterpret_cast<uintptr_t>(q21) | reinterpret_cast<uintptr_t>(q22) |
+                       reinterpret_cast<uintptr_t>(o1) | reinterpret_cast<uintptr_t>(o2) |
+                       reinterpret_cast<uintptr_t>(o3) | reinterpret_cast<uintptr_t>(o4)) & 15) == 0;
+    if (vec) {
+        for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
+            for (int64_t c = 4 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x); c < cols;
+                 c += 4 * (int64_t)gridDim.x * blockDim.x) {
+                const int64_t i = r * ld + c, o = r * cols + c;
+                const int4 v11 = __ldg(reinterpret_cast<const int4*>(q11 + i));
+                const int4 v12 = __ldg(reinterpret_cast<const int4*>(q12 + i));
+                const int4 v21 = __ldg(reinterpret_cast<const int4*>(q21 + i));
+                const int4 v22 = __ldg(reinterpret_cast<const int4*>(q22 + i));
+                uint32_t s0[4], s1[4], s2[4], s3[4];
+                sums(v11.x, v12.x, v21.x, v22.x, s0);
+                sums(v11.y, v12.y, v21.y, v22.y, s1);
+                sums(v11.z, v12.z, v21.z, v22.z, s2);
+                sums(v11.w, v12.w, v21.w, v22.w, s3);
+                *reinterpret_cast<int4*>(o1 + o) = make_int4(s0[0], s1[0], s2[0], s3[0]);
+                *reinterpret_cast<int4*>(o2 + o) = make_int4(s0[1], s1[1], s2[1], s3[1]);
+                *reinterpret_cast<int4*>(o3 + o) = make_int4(s0[2], s1[2], s2[2], s3[2]);
+                *reinterpret_cast<int4*>(o4 + o) = make_int4(s0[3], s1[3], s2[3], s3[3]);
+            }
+        }
+        return;
+    }
     for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
         for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < cols; c += (int64_t)gridDim.x * blockDim.x) {
             const int64_t i = r * ld + c, o = r * cols + c;
-            const uint32_t x11 = residue_i32(__ldg(q11 + i), M), x12 = residue_i32(__ldg(q12 + i), M);
-            const uint32_t x21 = residue_i32(__ldg(q21 + i), M), x22 = residue_i32(__ldg(q22 + i), M);
-            uint32_t s1, s2, s3, s4;
-            if (which == 0) {
-                s1 = addmod(x21, x22, M.p);      // S1 = A21 + A22
-                s2 = submod(s1, x11, M.p);       // S2 = S1 - A11
-                s3 = submod(x11, x21, M.p);      // S3 = A11 - A21
-                s4 = submod(x12, s2, M.p);       // S4 = A12 - S2
-            } else {
-                s1 = submod(x12, x11, M.p);      // T1 = B12 - B11
-                s2 = submod(x22, s1, M.p);       // T2 = B22 - T1
-                s3 = submod(x22, x12, M.p);      // T3 = B22 - B12
-                s4 = submod(s2, x21, M.p);       // T4 = T2 - B21
-            }
-            o1[o] = static_cast<int32_t>(s1);
-            o2[o] = static_cast<int32_t>(s2);
-            o3[o] = static_cast<int32_t>(s3);
-            o4[o] = static_cast<int32_t>(s4);
+            uint32_t s[4];
+            sums(__ldg(q11 + i), __ldg(q12 + i), __ldg(q21 + i), __ldg(q22 + i), s);
+            o1[o] = static_cast<int32_t>(s[0]);
+            o2[o] = static_cast<int32_t>(s[1]);
+            o3[o] = static_cast<int32_t>(s[2]);
+            o4[o] = static_cast<int32_t>(s[3]);
         }
     }
 }
@@ -103,7 +135,8 @@ int run_winograd(const Plan& half, bool transA, bool transB, int64_t m, int64_t 
     const int64_t a_rows = transA ? hk : hm, a_cols = transA ? hm : hk;
     const int64_t b_rows = transB ? hn : hk, b_cols = transB ? hk : hn;
     auto grid2 = [&](int64_t rows, int64_t cols) {
-        int gx = static_cast<int>((cols + 255) / 256);
+        // 4 columns per thread on the (usual) 16-byte-aligned path
+        int gx = static_cast<int>((cols + 1023) / 1024);
         if (gx > 32) gx = 32;
         int64_t gy = (int64_t)num_sms() * 8 / gx;
         if (gy > rows) gy = rows;
