@@ -247,24 +247,29 @@ def verify_output(cfg, C_out, row0=0, nsample=8, trials=2):
     import ffgen
     import oracle
     t0 = time.perf_counter()
+    # torchrun sets OMP_NUM_THREADS=1: give each local rank its share of the host cores
+    nth = max(1, len(os.sched_getaffinity(0)) // max(1, _env_int("LOCAL_WORLD_SIZE", 1)))
+    ffgen.set_threads(nth)
     p, mr = cfg.p, C_out.shape[0]
-    A = ffgen.uniform_matrix(p, cfg.seed, ffgen.STREAM_A, *cfg.a_shape)
-    A_rows = A[row0:row0 + mr] if cfg.transA == "N" else A[:, row0:row0 + mr]
+    if cfg.transA == "N":
+        A_rows = ffgen.uniform_matrix(p, cfg.seed, ffgen.STREAM_A, *cfg.a_shape, row0=row0, nrows=mr)
+    else:
+        A_rows = ffgen.uniform_matrix(p, cfg.seed, ffgen.STREAM_A, *cfg.a_shape)[:, row0:row0 + mr]
     B = ffgen.uniform_matrix(p, cfg.seed, ffgen.STREAM_B, *cfg.b_shape)
     beta_nz = cfg.beta % p != 0
     Cin = ffgen.uniform_matrix(p, cfg.seed, ffgen.STREAM_C, cfg.m, cfg.n, row0=row0, nrows=mr) if beta_nz else None
     rows = sorted({0, mr - 1} | {int(r) for r in np.linspace(0, mr - 1, nsample).astype(int)})
     want = oracle.fgemm_rows(p, cfg.transA, cfg.transB, cfg.alpha, A_rows, B, cfg.beta,
-                             None if Cin is None else Cin[rows], rows, mr, cfg.n, cfg.k)
+                             None if Cin is None else Cin[rows], rows, mr, cfg.n, cfg.k, nthreads=nth)
     rows_ok = bool(np.array_equal(C_out[rows], want))
     frei_ok = True
     for t in range(trials):
         x = ffgen.uniform_vector(p, cfg.seed, 8 + t, cfg.n)
-        lhs = oracle.matvec(p, "N", C_out, x)
-        bx = oracle.matvec(p, cfg.transB, B, x)
-        rhs = oracle.matvec(p, cfg.transA, A_rows, bx).astype(np.int64) * (cfg.alpha % p) % p
+        lhs = oracle.matvec(p, "N", C_out, x, nthreads=nth)
+        bx = oracle.matvec(p, cfg.transB, B, x, nthreads=nth)
+        rhs = oracle.matvec(p, cfg.transA, A_rows, bx, nthreads=nth).astype(np.int64) * (cfg.alpha % p) % p
         if Cin is not None:
-            rhs = (rhs + oracle.matvec(p, "N", Cin, x).astype(np.int64) * (cfg.beta % p)) % p
+            rhs = (rhs + oracle.matvec(p, "N", Cin, x, nthreads=nth).astype(np.int64) * (cfg.beta % p)) % p
         frei_ok = frei_ok and bool(np.array_equal(lhs.astype(np.int64), rhs))
     return {"ok": rows_ok and frei_ok, "rows_checked": len(rows), "rows_bitexact": rows_ok,
             "freivalds_trials": trials, "freivalds_ok": frei_ok, "rows": [row0, row0 + mr],
@@ -523,11 +528,16 @@ def main():
                 ff, lambda: eng.step(A_panel, B, C_panel), args.steps, args.warmup, scratch, barrier)
         chunks = len(eng.chunks)
         n_gemm = max(1, len(gemm_ms) // args.steps)
-        ops_step = prods * 2.0 * mr * cfg.n * cfg.k
+        wino = eng.whole and n_gemm == 7
+        ops_step = prods * 2.0 * mr * cfg.n * cfg.k * (7.0 / 8.0 if wino else 1.0)
         roofline = roofline_entry(peaks, ops_step / n_gemm, gemm_ms, elapsed_ms,
-                                  "ffgemm_tc_kernel (tcgen05.mma.kind::i8, %s)" % info["scheme"])
-        parallelism_extra = {"path": "RowPanelGemm (ff_encode + NCCL broadcast + ff_gemm_limbs)",
-                             "rank_rows": [r0, r1]}
+                                  "ffgemm_tc_kernel (tcgen05.mma.kind::i8, %s)%s" % (
+                                      info["scheme"], " x7 (one Winograd level per panel)" if wino else ""))
+        path = {"planes": "RowPanelGemm: encoded B planes broadcast (NCCL), ff_encode + ff_gemm_limbs per chunk",
+                "int32": "RowPanelGemm: int32 B broadcast (NCCL), per-rank encode + ff_gemm_limbs per chunk"}[eng.mode]
+        if eng.whole:
+            path = "RowPanelGemm: int32 B broadcast (NCCL), one ff_gemm_ex per panel (local Winograd)"
+        parallelism_extra = {"path": path, "rank_rows": [r0, r1], "broadcast_mode": eng.mode}
         if not args.no_verify:
             reset_c()
             eng.step(A_panel, B, C_panel)

@@ -99,10 +99,19 @@ def _c_gen():
             c.ffgen_uniform_flat.argtypes = [ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int64,
                                              ctypes.c_int64, ctypes.c_void_p]
             c.ffgen_uniform_flat.restype = None
+            c.ffgen_set_threads.argtypes = [ctypes.c_int]
+            c.ffgen_set_threads.restype = None
             _clib = c
         except Exception:
             _clib = False
     return _clib or None
+
+
+def set_threads(n: int) -> None:
+    """Threads of the C generator (no-op without it)."""
+    c = _c_gen()
+    if c is not None:
+        c.ffgen_set_threads(int(n))
 
 
 def uniform_flat(p: int, seed: int, stream: int, start: int, count: int) -> np.ndarray:

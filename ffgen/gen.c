@@ -4,6 +4,9 @@
  * arithmetic: splitmix64's output function and a final "mod p" only.
  *   v[i] = (mix64(key + (i + 1) * GAMMA) >> 11) mod p,  i = start .. start+count-1 */
 #include <stdint.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 static inline uint64_t mix64(uint64_t z) {
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
@@ -17,4 +20,14 @@ void ffgen_uniform_flat(uint32_t p, uint64_t key, int64_t start, int64_t count, 
         const uint64_t z = key + (uint64_t)(start + i + 1) * 0x9E3779B97F4A7C15ULL;
         out[i] = (int32_t)((mix64(z) >> 11) % p);
     }
+}
+
+/* Threads for the loop above (0: leave the OpenMP default); torchrun sets
+ * OMP_NUM_THREADS=1 for every rank, which the bench's per-rank checks override. */
+void ffgen_set_threads(int n) {
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
 }

@@ -61,6 +61,7 @@ struct Cfg {
 // into up to four quadrants of C.
 struct GemmOut {
     int32_t* C;
+    int64_t ld;        // leading dimension of this output
     uint32_t a, a_sh, b, b_sh;
     int32_t vec;       // 1 if rows of C are 16-byte aligned
 };
@@ -90,6 +91,8 @@ struct GemmArgs {
     int* progress;              // throttle (FF_THROTTLE=S): tile pairs started, all clusters
     int32_t throttle;           // slack S in tile pairs (0: off)
     int32_t crt;                // 1: groups are CRT moduli
+    const int32_t* addend;      // optional: residues in [0, p) added to R (mod p) before the outputs
+    int64_t ld_add;             //   (Winograd: P1 stored once, added by P6's epilogue)
     CrtConsts cc;
     uint8_t* scratch;           // CRT: per CTA and slot, G byte planes of kCrtPlane bytes
 };
@@ -191,10 +194,16 @@ __device__ __forceinline__ void crt_group(const GemmArgs& a, const ModP& M, cons
         const uint32_t t = (F[j] + (1u << 23)) >> 24;
         X[j] = residue_u64(S[j] + static_cast<unsigned long long>(t) * a.cc.Mneg, a.cc.mu64, M.p);
     }
+    if (a.addend) {
+        const int32_t* ad = a.addend + static_cast<int64_t>(row) * a.ld_add + col0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (col0 + j < a.n) X[j] = addmod(X[j], static_cast<uint32_t>(ad[j]), M.p);
+    }
 #pragma unroll 1
     for (int qo = 0; qo < a.nout; ++qo) {
         const GemmOut O = a.out[qo];
-        int32_t* cr = O.C + static_cast<int64_t>(row) * a.ldc + col0;
+        int32_t* cr = O.C + static_cast<int64_t>(row) * O.ld + col0;
         const bool full = O.vec && (col0 + 8 <= a.n);
         uint32_t o[8];
         if (O.b != 0) {
@@ -558,11 +567,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int col0 = tn * K::BN + h * 64 + half * 32;
 #pragma unroll
                     for (int t = 0; t < 32; ++t) v[t] = residue_i32(static_cast<int32_t>(v[t]), M);  // exact R
+                    if (a.addend) {
+                        const int32_t* ad = a.addend + static_cast<int64_t>(row) * a.ld_add + col0;
+#pragma unroll
+                        for (int t = 0; t < 32; ++t)
+                            if (col0 + t < a.n) v[t] = addmod(v[t], static_cast<uint32_t>(ad[t]), M.p);
+                    }
 
 #pragma unroll 1
                     for (int qo = 0; qo < a.nout; ++qo) {
                         const GemmOut O = a.out[qo];
-                        int32_t* crow = O.C + static_cast<int64_t>(row) * a.ldc + col0;
+                        int32_t* crow = O.C + static_cast<int64_t>(row) * O.ld + col0;
                         const bool full = O.vec && (col0 + 32 <= a.n);
                         uint32_t o[32];
                         if (O.b != 0) {
@@ -675,7 +690,8 @@ uint32_t shoup_host(uint32_t w, uint32_t p) { return static_cast<uint32_t>((stat
 
 template <int kPair>
 int launch_impl(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A_limbs, const int8_t* B_limbs,
-                const OutSpec* outs, int nout, int64_t ldc, int last_use, void* scratch, cudaStream_t st) {
+                const OutSpec* outs, int nout, int64_t ldc, int last_use, void* scratch, cudaStream_t st,
+                const int32_t* addend, int64_t ld_add) {
     using K = Cfg<kPair>;
     const ff_plan_info& I = pl.info;
     if (m > INT32_MAX - K::BM || n > INT32_MAX - K::BN) return -2;
@@ -687,12 +703,15 @@ int launch_impl(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A
     for (int q = 0; q < nout; ++q) {
         const uint32_t p = pl.mp.p;
         a.out[q].C = outs[q].C;
+        a.out[q].ld = outs[q].ld > 0 ? outs[q].ld : ldc;
         a.out[q].a = outs[q].a % p;
         a.out[q].a_sh = shoup_host(a.out[q].a, p);
         a.out[q].b = outs[q].b % p;
         a.out[q].b_sh = shoup_host(a.out[q].b, p);
-        a.out[q].vec = ((ldc % 4) == 0 && (reinterpret_cast<uintptr_t>(outs[q].C) & 15) == 0) ? 1 : 0;
+        a.out[q].vec = ((a.out[q].ld % 4) == 0 && (reinterpret_cast<uintptr_t>(outs[q].C) & 15) == 0) ? 1 : 0;
     }
+    a.addend = addend;
+    a.ld_add = ld_add;
     a.last_use = last_use;
     a.ldc = ldc;
     a.m = static_cast<int32_t>(m);
@@ -842,18 +861,18 @@ size_t crt_scratch_bytes(const Plan& pl) {
 
 int launch_gemm_tc_multi(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A_limbs,
                          const int8_t* B_limbs, const OutSpec* outs, int nout, int64_t ldc, int last_use,
-                         void* scratch, cudaStream_t st) {
+                         void* scratch, cudaStream_t st, const int32_t* addend, int64_t ld_add) {
     // The CTA-pair kernel unless the problem has too few 256 x 256 tiles to
     // occupy the GPU (then the 128 x 256 single-CTA kernel gives more CTAs).
     const int64_t pair_tiles = ((m + 255) / 256) * ((n + 255) / 256);
     if (pl.force_pair == 1 || (pl.force_pair == 0 && pair_tiles * 2 < num_sms()))
-        return launch_impl<1>(pl, m, n, k, A_limbs, B_limbs, outs, nout, ldc, last_use, scratch, st);
-    return launch_impl<2>(pl, m, n, k, A_limbs, B_limbs, outs, nout, ldc, last_use, scratch, st);
+        return launch_impl<1>(pl, m, n, k, A_limbs, B_limbs, outs, nout, ldc, last_use, scratch, st, addend, ld_add);
+    return launch_impl<2>(pl, m, n, k, A_limbs, B_limbs, outs, nout, ldc, last_use, scratch, st, addend, ld_add);
 }
 
 int launch_gemm_tc(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A_limbs, const int8_t* B_limbs,
                    int32_t* C, int64_t ldc, void* scratch, cudaStream_t st) {
-    const OutSpec o = {C, pl.mp.alpha, pl.mp.beta};
+    const OutSpec o = {C, pl.mp.alpha, pl.mp.beta, 0};
     return launch_gemm_tc_multi(pl, m, n, k, A_limbs, B_limbs, &o, 1, ldc, 1, scratch, st);
 }
 

@@ -230,3 +230,25 @@ def test_struct_layouts_match_the_header(ff, tmp_path):
         assert got[(name, "sizeof")] == ctypes.sizeof(cls), name
         for fname, _ in cls._fields_:
             assert got[(name, fname)] == getattr(cls, fname).offset, (name, fname)
+
+
+def test_winograd_levels_query_host_only():
+    """ff_gemm_winograd_levels (host only): the measured default rule (one level
+    for several limbs / CRT planes on large shapes), forced levels,
+    the fp64 engine's Corollary 3.4 limit, and argument errors."""
+    import paper_cs_0601133_b200 as ff
+    lv = ff.ff_gemm_winograd_levels
+    assert lv(67108859, 16384, 16384, 16384) == 1          # c5: CRT + one level by default
+    assert lv(67108859, 8192, 16384, 16384) == 1           # c5 panel at 2 GPUs: local Winograd
+    assert lv(67108859, 2048, 16384, 16384) == 0           # c5 panel at 8 GPUs: too few half tiles
+    assert lv(65521, 32768, 32768, 8192) == 0              # c4: two limbs, measured to lose
+    assert lv(65521, 4096, 4096, 4096, {"winograd": 1}) == 1
+    assert lv(65521, 4096, 4096, 4096, {"winograd": -1}) == 0
+    assert lv(65521, 1000, 1000, 1000, {"scheme": 4, "winograd": 3}) == 3
+    with pytest.raises(ff.FFError):
+        lv(8388593, 64, 64, 114, {"scheme": 4, "winograd": 1})   # k = k_winograd: Cor 3.4 refuses
+    assert lv(8388593, 64, 64, 113, {"scheme": 4, "winograd": 1}) == 1
+    with pytest.raises(ff.FFError):
+        lv(65521, 511, 512, 512, {"winograd": 1})           # odd / too small for the int8 level
+    with pytest.raises(ff.FFError):
+        lv(1, 10, 10, 10)                                    # p out of range
