@@ -11,7 +11,9 @@ and the Table 2 schedule) and ``bounds.py`` (the paper's
 delayed-reduction thresholds: Eq. (1)/(2), Cor. 3.4, Thm. 4.2, Eq. (4)/(5))
 in exact Python ints.
 
-Parity status: every function here is pinned by tests/test_oracle_pins.py.
+Parity status: every function here is pinned (tests/test_oracle_pins.py,
+test_oracle_trsm_pins.py, test_oracle_winograd_bound.py); none is "parity
+unpinned".
 """
 from __future__ import annotations
 

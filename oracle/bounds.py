@@ -5,7 +5,10 @@ TEST INFRASTRUCTURE (pins for the planner and for the trsm cascade thresholds).
   largest number lambda of products of residues that can be accumulated
   without reduction, lambda (p-1)^2 < 2^gamma (positive) or
   lambda ((p-1)/2)^2 < 2^(gamma-1) (balanced).
-* ``k_winograd(p, gamma, l, balanced)`` -- Corollary 3.4 (l.302-312).
+* ``k_winograd(p, gamma, l, balanced)`` -- Corollary 3.4 (l.302-312) as printed.
+* ``winograd_v``, ``thm31_bound`` -- Theorem 3.1's v_l and bound (l.284-290,
+  App. A.1-A.2); ``k_winograd_exact`` -- the corollary's exact threshold
+  (reading R21: the printed "+1" admits up to 2^l unsafe k).
 * ``trsm_u_v(M, m, k)`` -- Theorem 4.2 (l.404-420): the bounds u_k, v_k on the
   entries of the integer solution of a unit upper triangular system.
 * ``trsm_worst_case(M, m, n)`` -- the system of Corollary 4.3 (l.448-458); it
@@ -26,7 +29,9 @@ the text's "n <= 6" for balanced p = 1001 is reproduced by neither (garble,
 SURVEY §8(c).15).
 
 Parity status: pinned (tests/test_oracle_pins.py::test_paper_thresholds_*,
-test_trsm_bound_*).
+test_trsm_bound_*; tests/test_oracle_trsm_pins.py; Theorem 3.1 / Cor. 3.2-3.4 by
+tests/test_oracle_winograd_bound.py: the App. A.6 witnesses attain thm31_bound
+exactly, brute force over all 2 x 2 pairs, SURVEY's k_Winograd values).
 """
 from __future__ import annotations
 

@@ -15,7 +15,14 @@
   ``step16_operand`` selects which, so the tests can show the printed form is
   wrong and the fixed form equals alpha*A*B + beta*C.
 
-Parity status: pinned (tests/test_oracle_pins.py::test_table1_*, test_table2_*).
+* ``witness(l, MA, mA, MB, mB)`` -- the optimality witnesses A_l, B_l of
+  Appendix A.6 (l.1087-1117); ``winograd_traced(A, B, l)`` -- l levels of
+  App. A.2's form over Z returning the product and the largest |intermediate|
+  (the quantity Theorem 3.1 bounds).
+
+Parity status: pinned (tests/test_oracle_pins.py::test_table1_*, test_table2_*;
+tests/test_oracle_winograd_bound.py: traced product = plain product, witnesses
+attain Theorem 3.1's bound, exhaustive 2 x 2 optimality).
 """
 from __future__ import annotations
 

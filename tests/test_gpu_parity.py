@@ -588,3 +588,30 @@ def test_more_than_2_31_elements_sampled_rows(env):
         np.testing.assert_array_equal(got[i:i + 1], want, err_msg="row %d" % r)
     del A, C
     torch.cuda.empty_cache()
+
+
+# ---------------------------------------------------------------- instrumentation used by bench.py
+
+def test_prof_events_and_launch_counts(env):
+    """ff_prof_start/stop: one event pair per GEMM-kernel launch on its own stream,
+    a count of every fgemm-path launch (encoders included), durations > 0; and
+    ff_mma_ceiling returns a plausible tcgen05 int8 rate."""
+    torch, ff = env
+    p = 65521
+    A = torch.randint(0, p, (2048, 2048), dtype=torch.int32, device="cuda")
+    B = torch.randint(0, p, (2048, 2048), dtype=torch.int32, device="cuda")
+    C = torch.zeros((2048, 2048), dtype=torch.int32, device="cuda")
+    ff.fgemm(p, A, B, C)
+    torch.cuda.synchronize()
+    ff.ff_prof_start(16)
+    for _ in range(3):
+        ff.fgemm(p, A, B, C)                       # encode A, encode B, tcgen05 GEMM
+    ms, launches = ff.ff_prof_stop(16)
+    assert len(ms) == 3 and all(t > 0 for t in ms)
+    assert launches == 9
+    ff.ff_prof_start(4)
+    ff.fgemm(p, A[:512, :512], B[:512, :512], C[:512, :512])   # one latency-kernel launch
+    ms, launches = ff.ff_prof_stop(4)
+    assert len(ms) == 1 and launches == 1
+    tops = ff.ff_mma_ceiling(20000)
+    assert 1000 < tops < 6000
