@@ -64,6 +64,7 @@ struct GemmOut {
     int64_t ld;        // leading dimension of this output
     uint32_t a, a_sh, b, b_sh;
     int32_t vec;       // 1 if rows of C are 16-byte aligned
+    int32_t add;       // 1: this output takes R + addend (mod p) instead of R
 };
 
 struct GemmArgs {
@@ -91,8 +92,8 @@ struct GemmArgs {
     int* progress;              // throttle (FF_THROTTLE=S): tile pairs started, all clusters
     int32_t throttle;           // slack S in tile pairs (0: off)
     int32_t crt;                // 1: groups are CRT moduli
-    const int32_t* addend;      // optional: residues in [0, p) added to R (mod p) before the outputs
-    int64_t ld_add;             //   (Winograd: P1 stored once, added by P6's epilogue)
+    const int32_t* addend;      // optional: residues in [0, p) added to R (mod p) for the outputs
+    int64_t ld_add;             //   with `add` set (Winograd temporaries U2 = P1 + P6)
     CrtConsts cc;
     uint8_t* scratch;           // CRT: per CTA and slot, G byte planes of kCrtPlane bytes
 };
@@ -194,17 +195,19 @@ __device__ __forceinline__ void crt_group(const GemmArgs& a, const ModP& M, cons
         const uint32_t t = (F[j] + (1u << 23)) >> 24;
         X[j] = residue_u64(S[j] + static_cast<unsigned long long>(t) * a.cc.Mneg, a.cc.mu64, M.p);
     }
-    if (a.addend) {
-        const int32_t* ad = a.addend + static_cast<int64_t>(row) * a.ld_add + col0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-            if (col0 + j < a.n) X[j] = addmod(X[j], static_cast<uint32_t>(ad[j]), M.p);
-    }
+    bool added = false;    // outputs with `add` come last (sorted on the host)
 #pragma unroll 1
     for (int qo = 0; qo < a.nout; ++qo) {
         const GemmOut O = a.out[qo];
         int32_t* cr = O.C + static_cast<int64_t>(row) * O.ld + col0;
         const bool full = O.vec && (col0 + 8 <= a.n);
+        if (O.add && !added) {
+            const int32_t* ad = a.addend + static_cast<int64_t>(row) * a.ld_add + col0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (col0 + j < a.n) X[j] = addmod(X[j], static_cast<uint32_t>(ad[j]), M.p);
+            added = true;
+        }
         uint32_t o[8];
         if (O.b != 0) {
             if (full) {
@@ -567,17 +570,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int col0 = tn * K::BN + h * 64 + half * 32;
 #pragma unroll
                     for (int t = 0; t < 32; ++t) v[t] = residue_i32(static_cast<int32_t>(v[t]), M);  // exact R
-                    if (a.addend) {
-                        const int32_t* ad = a.addend + static_cast<int64_t>(row) * a.ld_add + col0;
-#pragma unroll
-                        for (int t = 0; t < 32; ++t)
-                            if (col0 + t < a.n) v[t] = addmod(v[t], static_cast<uint32_t>(ad[t]), M.p);
-                    }
 
+                    bool added = false;    // outputs with `add` come last (sorted on the host)
 #pragma unroll 1
                     for (int qo = 0; qo < a.nout; ++qo) {
                         const GemmOut O = a.out[qo];
                         int32_t* crow = O.C + static_cast<int64_t>(row) * O.ld + col0;
+                        if (O.add && !added) {
+                            const int32_t* ad = a.addend + static_cast<int64_t>(row) * a.ld_add + col0;
+#pragma unroll
+                            for (int t = 0; t < 32; ++t)
+                                if (col0 + t < a.n) v[t] = addmod(v[t], static_cast<uint32_t>(ad[t]), M.p);
+                            added = true;
+                        }
                         const bool full = O.vec && (col0 + 32 <= a.n);
                         uint32_t o[32];
                         if (O.b != 0) {
@@ -700,6 +705,14 @@ int launch_impl(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A
     a.mp = pl.mp;
     if (nout < 1 || nout > 4) return -10;
     a.nout = nout;
+    // the kernels add the addend in place before the first output that takes it,
+    // so the outputs that do come last
+    OutSpec so[4];
+    int ns = 0;
+    for (int pass = 0; pass < 2; ++pass)
+        for (int q = 0; q < nout; ++q)
+            if ((outs[q].add && addend ? 1 : 0) == pass) so[ns++] = outs[q];
+    outs = so;
     for (int q = 0; q < nout; ++q) {
         const uint32_t p = pl.mp.p;
         a.out[q].C = outs[q].C;
@@ -709,6 +722,7 @@ int launch_impl(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A
         a.out[q].b = outs[q].b % p;
         a.out[q].b_sh = shoup_host(a.out[q].b, p);
         a.out[q].vec = ((a.out[q].ld % 4) == 0 && (reinterpret_cast<uintptr_t>(outs[q].C) & 15) == 0) ? 1 : 0;
+        a.out[q].add = (outs[q].add && addend) ? 1 : 0;
     }
     a.addend = addend;
     a.ld_add = ld_add;
@@ -872,7 +886,7 @@ int launch_gemm_tc_multi(const Plan& pl, int64_t m, int64_t n, int64_t k, const 
 
 int launch_gemm_tc(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A_limbs, const int8_t* B_limbs,
                    int32_t* C, int64_t ldc, void* scratch, cudaStream_t st) {
-    const OutSpec o = {C, pl.mp.alpha, pl.mp.beta, 0};
+    const OutSpec o = {C, pl.mp.alpha, pl.mp.beta, 0, 0};
     return launch_gemm_tc_multi(pl, m, n, k, A_limbs, B_limbs, &o, 1, ldc, 1, scratch, st);
 }
 

@@ -121,10 +121,11 @@ struct OutSpec {          // C <- (a * A B + b * C) mod p for one output block
     int32_t* C;
     uint32_t a, b;
     int64_t ld;           // leading dimension of C (0: the launch's ldc)
+    int32_t add;          // 1: C <- (a * (A B + addend) + b * C) mod p (the launch's addend)
 };
 // `scratch`: crt_scratch_bytes(pl) bytes of device memory (ignored for limb plans).
 // `addend` (optional, residues in [0, p), leading dimension ld_add): added to the
-// product mod p before every output's a * (.) + b * C (a Winograd temporary).
+// product mod p for the outputs with `add` set (a Winograd temporary).
 int launch_gemm_tc_multi(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A_limbs,
                          const int8_t* B_limbs, const OutSpec* outs, int nout, int64_t ldc, int last_use,
                          void* scratch, cudaStream_t st, const int32_t* addend = nullptr, int64_t ld_add = 0);

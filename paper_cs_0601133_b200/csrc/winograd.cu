@@ -18,9 +18,9 @@
 //
 // Instead of Table 2's temporaries X1..X3 and post-additions, each product's
 // fused epilogue adds +-alpha P_i (mod p) directly into every C quadrant it
-// contributes to, so the products are never stored -- except P1, kept once as
-// a temporary that P6's epilogue adds into C12, C21, C22 (launch order P1, P2,
-// P6, P3, P4, P5, P7; beta applied by the first write of each quadrant).
+// contributes to, so the products are never stored -- except two temporaries
+// (T = P1 and U = P6 + T) that later epilogues add, which keep every product at
+// <= 2 read-modify-written quadrants (schedule in run_winograd).
 #include <cuda_runtime.h>
 
 #include <vector>
@@ -114,7 +114,7 @@ size_t winograd_ws_bytes(const Plan& half, int64_t m, int64_t n, int64_t k) {
     const size_t hm = m / 2, hn = n / 2, hk = k / 2;
     const size_t L = half.info.L, kp = half.info.k_pad;
     return 4 * align256(4 * hm * hk) + 4 * align256(4 * hk * hn) + 7 * align256(L * hm * kp) +
-           7 * align256(L * hn * kp) + align256(crt_scratch_bytes(half)) + align256(4 * hm * hn);
+           7 * align256(L * hn * kp) + align256(crt_scratch_bytes(half)) + 2 * align256(4 * hm * hn);
 }
 
 int run_winograd(const Plan& half, bool transA, bool transB, int64_t m, int64_t n, int64_t k, const int32_t* A,
@@ -161,12 +161,12 @@ int run_winograd(const Plan& half, bool transA, bool transB, int64_t m, int64_t 
                                                          T[1], T[2], T[3]);
     if (cudaGetLastError() != cudaSuccess) return FF_ERR_CUDA;
 
-    // Product operands: (A side, ld), (B side, ld), in launch order P1, P2, P6, P3, P4,
-    // P5, P7.  S/T temporaries are dense, stored orientation.
-    const int32_t* aop[7] = {A11, A12, S[1], S[3], A22, S[0], S[2]};
-    const int64_t ald[7] = {lda, lda, a_cols, a_cols, lda, a_cols, a_cols};
-    const int32_t* bop[7] = {B11, B21, T[1], B22, T[3], T[0], T[2]};
-    const int64_t bld[7] = {ldb, ldb, b_cols, ldb, b_cols, b_cols, b_cols};
+    // Product operands: (A side, ld), (B side, ld), in launch order P1, P2, P6, P7, P5,
+    // P3, P4.  S/T temporaries are dense, stored orientation.
+    const int32_t* aop[7] = {A11, A12, S[1], S[2], S[0], S[3], A22};
+    const int64_t ald[7] = {lda, lda, a_cols, a_cols, a_cols, a_cols, lda};
+    const int32_t* bop[7] = {B11, B21, T[1], T[2], T[0], B22, T[3]};
+    const int64_t bld[7] = {ldb, ldb, b_cols, b_cols, b_cols, ldb, b_cols};
     for (int i = 0; i < 7; ++i) {
         if (launch_encode(half, transA ? 0 : 1, hm, hk, aop[i], ald[i], Al[i], st) != cudaSuccess) return FF_ERR_CUDA;
         if (launch_encode(half, transB ? 1 : 0, hn, hk, bop[i], bld[i], Bl[i], st) != cudaSuccess) return FF_ERR_CUDA;
@@ -176,25 +176,31 @@ int run_winograd(const Plan& half, bool transA, bool transB, int64_t m, int64_t 
     int32_t* C12 = C + hn;
     int32_t* C21 = C + hm * ldc;
     int32_t* C22 = C + hm * ldc + hn;
-    // P1 appears in all four quadrants; instead of four read-modify-writes in its
-    // epilogue (the heaviest of the seven, and the one that held the MMA back), it
-    // writes C11 and a temporary P1 mod p, and P6's epilogue -- which updates C12,
-    // C21, C22 anyway -- adds it: C_q <- alpha (P6 + P1) + beta C_q.  beta enters at
-    // the first write of each quadrant (P1 for C11, P6 for the others).
-    int32_t* P1t = reinterpret_cast<int32_t*>(take(4 * hm * hn));
+    // Schedule with two stored temporaries so that no product's epilogue updates
+    // more than two quadrants (a slow epilogue holds the MMA back):
+    //   P1 -> C11 <- a P1 + b C11,  T = P1                        (T stored raw)
+    //   P2 -> C11 += a P2
+    //   P6 -> U = P6 + T  (= U2 of App. A.2)                      (U stored raw)
+    //   P7 -> C21 <- a (P7 + U) + b C21,  C22 <- a (P7 + U) + b C22
+    //   P5 -> C12 <- a (P5 + U) + b C12,  C22 += a P5
+    //   P3 -> C12 += a P3,   P4 -> C21 -= a P4
+    // beta enters at the first write of each quadrant.
+    int32_t* Tt = reinterpret_cast<int32_t*>(take(4 * hm * hn));
+    int32_t* Ut = reinterpret_cast<int32_t*>(take(4 * hm * hn));
     const uint32_t p = half.mp.p, al = half.mp.alpha, be = half.mp.beta, nal = (p - al) % p;
-    const OutSpec o1[2] = {{C11, al, be, 0}, {P1t, 1, 0, hn}};                          // P1
-    const OutSpec o2[1] = {{C11, al, 1, 0}};                                              // P2
-    const OutSpec o6[3] = {{C12, al, be, 0}, {C21, al, be, 0}, {C22, al, be, 0}};        // P6 (+ P1)
-    const OutSpec o3[1] = {{C12, al, 1, 0}};                                              // P3
-    const OutSpec o4[1] = {{C21, nal, 1, 0}};                                             // P4
-    const OutSpec o5[2] = {{C12, al, 1, 0}, {C22, al, 1, 0}};                            // P5
-    const OutSpec o7[2] = {{C21, al, 1, 0}, {C22, al, 1, 0}};                            // P7
-    const OutSpec* outs[7] = {o1, o2, o6, o3, o4, o5, o7};
-    const int nouts[7] = {2, 1, 3, 1, 1, 2, 2};
+    const OutSpec o1[2] = {{C11, al, be, 0, 0}, {Tt, 1, 0, hn, 0}};                    // P1
+    const OutSpec o2[1] = {{C11, al, 1, 0, 0}};                                         // P2
+    const OutSpec o6[1] = {{Ut, 1, 0, hn, 1}};                                          // P6 (+T)
+    const OutSpec o7[2] = {{C21, al, be, 0, 1}, {C22, al, be, 0, 1}};                   // P7 (+U)
+    const OutSpec o5[2] = {{C12, al, be, 0, 1}, {C22, al, 1, 0, 0}};                    // P5 (+U for C12)
+    const OutSpec o3[1] = {{C12, al, 1, 0, 0}};                                         // P3
+    const OutSpec o4[1] = {{C21, nal, 1, 0, 0}};                                        // P4
+    const OutSpec* outs[7] = {o1, o2, o6, o7, o5, o3, o4};
+    const int nouts[7] = {2, 1, 1, 2, 2, 1, 1};
+    const int32_t* adds[7] = {nullptr, nullptr, Tt, Ut, Ut, nullptr, nullptr};
     for (int i = 0; i < 7; ++i) {
         const int e = launch_gemm_tc_multi(half, hm, hn, hk, Al[i], Bl[i], outs[i], nouts[i], ldc, i == 6 ? 1 : 0,
-                                             scratch, st, i == 2 ? P1t : nullptr, hn);
+                                             scratch, st, adds[i], hn);
         if (e) return e;
     }
     return 0;
