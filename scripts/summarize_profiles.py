@@ -77,7 +77,33 @@ def full(rep, cfg, rnd):
               open(os.path.join(ROOT, "profiles", "ncu_gemm_%s.json" % cfg), "w"), indent=1)
 
 
+MULTI_WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+              "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+              "sm__throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_sector_hit_rate.pct",
+              "sm__cycles_elapsed.avg.per_second", "launch__registers_per_thread", "launch__grid_size",
+              "launch__cluster_dim_x", "launch__shared_mem_per_block_dynamic"]
+
+
+def multi(rep, out, title):
+    """Every launch of a --set full report, one block each (multi <rep> <out> <title>)."""
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    r = list(csv.reader(raw.splitlines()))
+    h, u = r[0], r[1]
+    txt = ["# " + title]
+    for li, v in enumerate(r[2:]):
+        txt.append("## launch %d: %s" % (li, v[h.index("Kernel Name")][:90]))
+        for w in MULTI_WANT:
+            if w in h:
+                i = h.index(w)
+                txt.append("%-70s %20s %s" % (w, v[i], u[i]))
+    open(out, "w").write("\n".join(txt) + "\n")
+    print(open(out).read())
+
+
 if __name__ == "__main__":
+    if sys.argv[1] == "multi":
+        multi(sys.argv[2], sys.argv[3], sys.argv[4])
+        sys.exit(0)
     rnd, cfg, lc = sys.argv[1], sys.argv[2], sys.argv[3]
     launches(lc, os.path.join(ROOT, "profiles", "r%s_%s_launches.csv" % (rnd, cfg)))
     if len(sys.argv) > 4:
