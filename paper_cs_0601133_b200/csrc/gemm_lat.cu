@@ -89,24 +89,49 @@ __device__ __forceinline__ void item_rc(int it, bool kmajor_src, int& r, int& c)
 
 // Global loads of one item: 16 consecutive k of row r0 + r of the K-major view of
 // X (kmajor_src: X[r * ld + kk], else X[kk * ld + r]); zero outside the matrix.
+// Loads are unconditional, from addresses clamped into the matrix, and the
+// out-of-range values are zeroed afterwards: per-element guarded loads compile
+// to a branch per load (~25 instructions each), which made issuing a chunk's 48
+// loads per thread instruction-bound.
 __device__ __forceinline__ void load_item(const LatArgs& a, const int32_t* X, int64_t ld, bool kmajor_src, int gr,
                                           int rmax, int gk, uint32_t (&v)[16]) {
+    const bool rin = gr < rmax;
+    const int grc = rin ? gr : rmax - 1;
     if (kmajor_src) {
-        const int32_t* src = X + static_cast<int64_t>(gr) * ld + gk;
-        if (gr < rmax && gk + 16 <= a.k && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
+        const int32_t* src = X + static_cast<int64_t>(grc) * ld + gk;
+        if (gk + 16 <= a.k && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const int4 t4 = __ldg(reinterpret_cast<const int4*>(src) + q);
                 v[4 * q] = t4.x; v[4 * q + 1] = t4.y; v[4 * q + 2] = t4.z; v[4 * q + 3] = t4.w;
             }
         } else {
+            const int32_t* row = X + static_cast<int64_t>(grc) * ld;
 #pragma unroll
-            for (int t = 0; t < 16; ++t) v[t] = (gr < rmax && gk + t < a.k) ? __ldg(src + t) : 0;
+            for (int t = 0; t < 16; ++t) v[t] = __ldg(row + min(gk + t, a.k - 1));
+#pragma unroll
+            for (int t = 0; t < 16; ++t)
+                if (gk + t >= a.k) v[t] = 0;
         }
     } else {
+        if (gk + 16 <= a.k) {
+            const int32_t* src = X + static_cast<int64_t>(gk) * ld + grc;
 #pragma unroll
-        for (int t = 0; t < 16; ++t)
-            v[t] = (gr < rmax && gk + t < a.k) ? __ldg(X + static_cast<int64_t>(gk + t) * ld + gr) : 0;
+            for (int t = 0; t < 16; ++t) {
+                v[t] = __ldg(src);
+                src += ld;
+            }
+        } else {
+#pragma unroll
+            for (int t = 0; t < 16; ++t) v[t] = __ldg(X + static_cast<int64_t>(min(gk + t, a.k - 1)) * ld + grc);
+#pragma unroll
+            for (int t = 0; t < 16; ++t)
+                if (gk + t >= a.k) v[t] = 0;
+        }
+    }
+    if (!rin) {
+#pragma unroll
+        for (int t = 0; t < 16; ++t) v[t] = 0;
     }
 }
 
@@ -323,7 +348,7 @@ __global__ void __launch_bounds__(kLThreads, 1) lat_gemm_kernel(const __grid_con
         }
     }
     lat_mark(a, 7);
-    if (S > 1) ptx::cluster_sync();   // peers' shared memory stays valid until every CTA has read it
+    if (S > 1) ptx::cluster_sync_relaxed();   // peers' shared memory stays valid until every CTA has read it
     lat_mark(a, 8);
 }
 

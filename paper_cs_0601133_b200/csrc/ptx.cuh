@@ -294,6 +294,13 @@ __device__ __forceinline__ void named_bar_sync(int id, int n) {
 __device__ __forceinline__ void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// Exit barrier of a cluster whose CTAs only READ each other's shared memory
+// since the last release: no ordering of this thread's own writes is needed
+// (the release form compiles to a GPU-scope MEMBAR that waits for every
+// outstanding global store of the thread).
+__device__ __forceinline__ void cluster_sync_relaxed() {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+}
 
 // shared::cluster address of the same SMEM offset in CTA `rank` of this cluster.
 __device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
