@@ -77,8 +77,9 @@ __global__ void __launch_bounds__(256) encode_direct_kernel(ModP M, int64_t rows
                 uint32_t w[L];
 #pragma unroll
                 for (int i = 0; i < L; ++i) w[i] = 0;
+                centre_all(x[u], M);
 #pragma unroll
-                for (int t = 0; t < 4; ++t) put_digits<L, SCHEME>(centre(residue_i32(x[u][t], M), M), t, w);
+                for (int t = 0; t < 4; ++t) put_digits<L, SCHEME>(x[u][t], t, w);
                 uint32_t* dst = reinterpret_cast<uint32_t*>(limbs + r * k_pad);
 #pragma unroll
                 for (int i = 0; i < L; ++i) dst[g + i * (plane / 4)] = w[i];
@@ -128,13 +129,14 @@ __global__ void __launch_bounds__(256) encode_trans_kernel(ModP M, int64_t rows,
         const int64_t r0 = (t % tiles_r) * kTR;
         const int64_t kk0 = (t / tiles_r) * kTK;
         __syncthreads();
+        centre_all(xv, M);
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
             uint32_t w[L];
 #pragma unroll
             for (int l = 0; l < L; ++l) w[l] = 0;
 #pragma unroll
-            for (int e = 0; e < 4; ++e) put_digits<L, SCHEME>(centre(residue_i32(xv[4 * g + e], M), M), e, w);
+            for (int e = 0; e < 4; ++e) put_digits<L, SCHEME>(xv[4 * g + e], e, w);
 #pragma unroll
             for (int l = 0; l < L; ++l) *reinterpret_cast<uint32_t*>(&tile[l][lr][4 * lk + 32 * g]) = w[l];
         }
@@ -208,9 +210,12 @@ __global__ void __launch_bounds__(256) encode_trans_tma_kernel(const __grid_cons
         for (int g = 0; g < 4; ++g)
 #pragma unroll
             for (int l = 0; l < L; ++l) w[g][l] = 0;
+        int32_t xv[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i)
-            put_digits<L, SCHEME>(centre(residue_i32(T[(kg * 16 + i) * kTR + r], M), M), i & 3, w[i >> 2]);
+        for (int i = 0; i < 16; ++i) xv[i] = T[(kg * 16 + i) * kTR + r];
+        centre_all(xv, M);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) put_digits<L, SCHEME>(xv[i], i & 3, w[i >> 2]);
         ptx::mbar_arrive(&empty[s]);                            // this stage may be refilled
         if (tid == 0 && j + kTmaStages < mine) {
             ptx::mbar_wait(&empty[s], par);
@@ -324,11 +329,9 @@ __global__ void __launch_bounds__(256) encode_crt_direct_kernel(ModP M, CrtConst
                 for (int t = 0; t < 16; ++t) c[t] = (kk + t < k) ? __ldg(src + kk + t) : 0;
             }
             CrtDigitsIn dg[16];
+            centre_all(c, M);
 #pragma unroll
-            for (int t = 0; t < 16; ++t) {
-                c[t] = centre(residue_i32(c[t], M), M);
-                dg[t] = crt_split(c[t]);
-            }
+            for (int t = 0; t < 16; ++t) dg[t] = crt_split(c[t]);
             int8_t* dst = planes + r * k_pad + kk;
             // plane 0 is q = 256 (the planner picks 256 first): the low byte of c
             uint32_t w0[4];
@@ -388,7 +391,8 @@ __global__ void __launch_bounds__(256) encode_crt_trans_kernel(ModP M, CrtConsts
         const int64_t kk0 = (t / tiles_r) * kTK;
         int32_t cv[kTK / 8];
 #pragma unroll
-        for (int i = 0; i < kTK / 8; ++i) cv[i] = centre(residue_i32(xv[i], M), M);
+        for (int i = 0; i < kTK / 8; ++i) cv[i] = xv[i];
+        centre_all(cv, M);
         if (t + gridDim.x < ntiles) load_tile(t + gridDim.x);     // next tile's loads in flight
         const int64_t r = r0 + wr;
         const int64_t kc = kk0 + wc;
@@ -489,10 +493,10 @@ __global__ void __launch_bounds__(256) encode_crt_trans_tma_kernel(const __grid_
         int32_t c[16];
         CrtDigitsIn dg[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            c[i] = centre(residue_i32(T[(kg * 16 + i) * kTR + r], M), M);
-            dg[i] = crt_split(c[i]);
-        }
+        for (int i = 0; i < 16; ++i) c[i] = T[(kg * 16 + i) * kTR + r];
+        centre_all(c, M);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) dg[i] = crt_split(c[i]);
         ptx::mbar_arrive(&empty[s]);
         if (tid == 0 && j + kCrtStages < mine) {
             ptx::mbar_wait(&empty[s], par);

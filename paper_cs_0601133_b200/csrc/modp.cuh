@@ -37,6 +37,25 @@ __device__ __forceinline__ int32_t centre(uint32_t r, const ModP& M) {
     return r > M.half ? static_cast<int32_t>(r) - static_cast<int32_t>(M.p) : static_cast<int32_t>(r);
 }
 
+// Centred residues of N values in place.  Canonical inputs (every value already
+// in [0, p): the usual case, e.g. all five BASELINE configs) take the short path
+// -- one compare each, then centre -- and any other int32 the Barrett reduction;
+// the branch is per thread and group, so only a thread holding a non-canonical
+// value pays for the reduction.
+template <int N>
+__device__ __forceinline__ void centre_all(int32_t (&x)[N], const ModP& M) {
+    bool canon = true;
+#pragma unroll
+    for (int i = 0; i < N; ++i) canon &= static_cast<uint32_t>(x[i]) < M.p;
+    if (canon) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) x[i] = centre(static_cast<uint32_t>(x[i]), M);
+    } else {
+#pragma unroll
+        for (int i = 0; i < N; ++i) x[i] = centre(residue_i32(x[i], M), M);
+    }
+}
+
 // Intermediate write-back value: a centred-ish representative of (a * w) mod p
 // for the s32 accumulator a and w in {1, 256} (Horner scaling), with the
 // quotient estimated through the fp32 reciprocal w/p (PAPER.md l.125-127:

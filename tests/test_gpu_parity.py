@@ -120,6 +120,46 @@ def test_encoder_roundtrip(env, p, kmajor):
         assert np.abs(d).max() <= info["digit_max"][i]
 
 
+@pytest.mark.parametrize("p", CONFIG_PRIMES + [65537])
+@pytest.mark.parametrize("kmajor", [1, 0])
+@pytest.mark.parametrize("scheme", ["limb", "crt"])
+def test_encoder_mixed_canonical_groups(env, p, kmajor, scheme):
+    """The encoders' short path for canonical groups (every value in [0, p): one
+    compare, then centre) next to the Barrett path: mostly canonical inputs with
+    ~2% of the values outside [0, p) (negative, = p, >= p, int32 extremes), so
+    the groups of a warp mix both paths; limb and CRT planes, both source
+    orientations, ragged sizes."""
+    torch, ff = env
+    rng = np.random.default_rng(p % 991 + 7 * kmajor + (scheme == "crt"))
+    rows, k = 197, 1061
+    x = rng.integers(0, p, size=(rows, k), dtype=np.int64)
+    bad = rng.random((rows, k)) < 0.02
+    specials = np.array([-1, p, p + 1, 2 * p - 1, -p, -2 ** 31, 2 ** 31 - 1, -(p - 1)], dtype=np.int64)
+    x[bad] = rng.choice(specials, size=int(bad.sum()))
+    x[5, :4] = [0, p - 1, (p - 1) // 2, (p + 1) // 2]
+    x = x.astype(np.int32)
+    src = x if kmajor else np.ascontiguousarray(x.T)
+    X = _dev(torch, src)
+    r = np.mod(x.astype(np.int64), p)
+    c = np.where(r > (p - 1) // 2, r - p, r)
+    if scheme == "limb":
+        opt = _limb_opts(ff, p, k)
+        info = ff.ff_plan_query(p, k, opt)
+        out = torch.full((info["L"], rows, info["k_pad"]), 99, dtype=torch.int8, device="cuda")
+        ff.ff_encode(p, k, opt, kmajor, rows, X, src.shape[1], out)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(_decode(out.cpu().numpy(), info)[:, :k], c)
+    else:
+        opt = {"scheme": 3}
+        info = ff.ff_plan_query(p, k, opt)
+        out = torch.full((info["L"], rows, info["k_pad"]), 99, dtype=torch.int8, device="cuda")
+        ff.ff_encode(p, k, opt, kmajor, rows, X, src.shape[1], out)
+        torch.cuda.synchronize()
+        planes = out.cpu().numpy().astype(np.int64)
+        for i, q in enumerate(info["moduli"]):
+            np.testing.assert_array_equal(np.mod(planes[i, :, :k], q), np.mod(c, q), err_msg="modulus %d" % q)
+
+
 @pytest.mark.parametrize("p", CONFIG_PRIMES)
 def test_encoder_exhaustive_residues(env, p):
     """decode(encode(r)) = centre(r) for every residue r in [0, p) (p <= 2^26)."""
