@@ -154,6 +154,21 @@ __device__ __forceinline__ void for_each_step(const GemmArgs& a, int unit, int n
     }
 }
 
+// C values for beta * C: Shoup's product w * x mod p is exact for any unsigned
+// x < 2^32 (the quotient estimate errs by less than 2), so non-negative int32 C
+// (canonical C in particular) is used as it is; only a group holding a negative
+// value is reduced first (its unsigned reading would be off by 2^32).
+template <int N>
+__device__ __forceinline__ void c_nonneg(uint32_t (&o)[N], const ModP& M) {
+    uint32_t any = 0;
+#pragma unroll
+    for (int t = 0; t < N; ++t) any |= o[t];
+    if (static_cast<int32_t>(any) < 0) {
+#pragma unroll
+        for (int t = 0; t < N; ++t) o[t] = residue_i32(static_cast<int32_t>(o[t]), M);
+    }
+}
+
 // One 8-column group of the final step of a CRT tile, for one thread (one row of
 // its 64-column quarter), after the accumulator has been released: X = sum_i u_i
 // M_i - t M exactly, t = round(sum_i u_i / q_i) (|X| <= M/4), X mod p =
@@ -217,11 +232,12 @@ __device__ __forceinline__ void crt_group(const GemmArgs& a, const ModP& M, cons
 #pragma unroll
                 for (int j = 0; j < 8; ++j) o[j] = (col0 + j < a.n) ? cr[j] : 0;
             }
+            c_nonneg(o, M);
         }
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             uint32_t r = mulmod_shoup(X[j], O.a, O.a_sh, M.p);
-            if (O.b != 0) r = addmod(r, mulmod_shoup(residue_i32(static_cast<int32_t>(o[j]), M), O.b, O.b_sh, M.p), M.p);
+            if (O.b != 0) r = addmod(r, mulmod_shoup(o[j], O.b, O.b_sh, M.p), M.p);
             o[j] = r;
         }
         if (full) {
@@ -596,12 +612,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                                 for (int t = 0; t < 32; ++t) o[t] = (col0 + t < a.n) ? crow[t] : 0;
                             }
+                            c_nonneg(o, M);
                         }
 #pragma unroll
                         for (int t = 0; t < 32; ++t) {
                             uint32_t r = mulmod_shoup(v[t], O.a, O.a_sh, M.p);
-                            if (O.b != 0)
-                                r = addmod(r, mulmod_shoup(residue_i32(static_cast<int32_t>(o[t]), M), O.b, O.b_sh, M.p), M.p);
+                            if (O.b != 0) r = addmod(r, mulmod_shoup(o[t], O.b, O.b_sh, M.p), M.p);
                             o[t] = r;
                         }
                         if (full && (a.hints & 2) && qo == a.nout - 1 && a.last_use) {
