@@ -459,7 +459,8 @@ __global__ void __launch_bounds__(256) encode_crt_trans_tma_kernel(const __grid_
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int32_t* ring = reinterpret_cast<const int32_t*>(sm);
     uint8_t (*tile)[kTR][kPitch] = reinterpret_cast<uint8_t (*)[kTR][kPitch]>(sm + kCrtStages * kTmaTileBytes);
-    uint64_t* full = reinterpret_cast<uint64_t*>(sm + kCrtStages * kTmaTileBytes + kMaxMod * kTR * kPitch);
+    const int nq = C.nq;   // staging for nq planes only (dynamic SMEM sized by the launch)
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + kCrtStages * kTmaTileBytes + nq * kTR * kPitch);
     uint64_t* empty = full + kCrtStages;
     const int64_t plane = rows * k_pad;
     const int64_t tiles_r = (rows + kTR - 1) / kTR;
@@ -467,7 +468,6 @@ __global__ void __launch_bounds__(256) encode_crt_trans_tma_kernel(const __grid_
     const int64_t ntiles = tiles_r * tiles_k;
     const int tid = threadIdx.x, r = tid % kTR, kg = tid / kTR;
     const int wr = (tid / 32) * 4 + (tid % 32) / 8, wc = (tid % 8) * 16;
-    const int nq = C.nq;
     if (tid == 0) {
         for (int s = 0; s < kCrtStages; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 256); }
         ptx::fence_barrier_init();
@@ -631,9 +631,17 @@ cudaError_t launch_encode(const Plan& pl, int kmajor_src, int64_t rows, int64_t 
             if (!knobs().enc_notma && make_src_map(&map, X, rows, k, ldx)) {
                 const cudaError_t ea = set_smem_attr(reinterpret_cast<const void*>(encode_crt_trans_tma_kernel), kCrtTmaSmem);
                 if (ea != cudaSuccess) return ea;
-                const int64_t capt = (int64_t)num_sms() * 2;
+                // SMEM for this plan's nq planes only: 3 CTAs per SM for nq = 9 (2 at kMaxMod)
+                const int smem = kCrtStages * kTmaTileBytes + pl.cc.nq * kTR * kPitch + 2 * kCrtStages * 8 + 1024;
+                int per_sm = 0;
+                if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, encode_crt_trans_tma_kernel, 256, smem) !=
+                        cudaSuccess || per_sm < 1) {
+                    cudaGetLastError();
+                    per_sm = 2;
+                }
+                const int64_t capt = (int64_t)num_sms() * per_sm;
                 note_launch();
-                encode_crt_trans_tma_kernel<<<static_cast<int>(tiles < capt ? tiles : capt), 256, kCrtTmaSmem, st>>>(
+                encode_crt_trans_tma_kernel<<<static_cast<int>(tiles < capt ? tiles : capt), 256, smem, st>>>(
                     map, pl.mp, pl.cc, rows, k_pad, limbs);
                 return cudaGetLastError();
             }
