@@ -43,7 +43,7 @@ namespace {
 constexpr int kNumEpiWarps = 16;  // 4 per TMEM lane quadrant, 64 columns each
 constexpr int kThreads = 32 * (2 + kNumEpiWarps);
 constexpr int kTmemCols = 512;  // two 256-column s32 accumulators
-constexpr int kRasterDefault = 16;  // tile-rows per raster band (L2 reuse; swept on c4)
+constexpr int kRasterDefault = 12;  // tile-rows per raster band (L2 reuse; swept on c4: DESIGN.md §16)
 
 template <int kPair>
 struct Cfg {
