@@ -45,14 +45,19 @@ constexpr int kThreads = 32 * (2 + kNumEpiWarps);
 constexpr int kTmemCols = 512;  // two 256-column s32 accumulators
 constexpr int kRasterDefault = 12;  // tile-rows per raster band (L2 reuse; swept on c4: DESIGN.md §16)
 
-template <int kPair>
+// kWide (CTA pair only): 256 x 512 tiles, two N = 256 MMAs per k-step sharing the
+// A stage, one accumulator in all 512 TMEM columns (no second slot): 25% less
+// L2->SMEM operand traffic per MMA, the epilogue no longer hidden behind the
+// other slot.  Used for single-step tiles (one weight group, one k-block), where
+// the exposed epilogue is one final pass per tile.
+template <int kPair, bool kWide = false>
 struct Cfg {
     static constexpr int BM = 128 * kPair;         // tile rows (per cluster)
-    static constexpr int BN = kTileN;              // tile columns
+    static constexpr int BN = kWide ? 2 * kTileN : kTileN;   // tile columns
     static constexpr int A_BYTES = 128 * kBK;      // per CTA: 128 rows of A
-    static constexpr int B_BYTES = (BN / kPair) * kBK;  // per CTA: BN/kPair rows of B
+    static constexpr int B_BYTES = (BN / kPair) * kBK;  // per CTA: BN/kPair rows of B (wide: two 128-row halves)
     static constexpr int STAGE = A_BYTES + B_BYTES;
-    static constexpr int STAGES = kPair == 2 ? 7 : 4;
+    static constexpr int STAGES = kWide ? 4 : (kPair == 2 ? 7 : 4);
     static constexpr int SMEM = STAGES * STAGE + 256 + 1024;
 };
 
@@ -137,11 +142,11 @@ __device__ __forceinline__ void tile_coords(const GemmArgs& a, int t, int& tm, i
 // (group-outer), or k-blocks outer and all groups inner (k-outer, so a k-slice
 // of every limb is reused from L2 by all groups); the two slots innermost.
 // Tiles of this cluster: base + unit + j * nunits for j = 0, 1, ... < count.
-template <class F>
+template <bool kWide = false, class F>
 __device__ __forceinline__ void for_each_step(const GemmArgs& a, int unit, int nunits, int base, int count, F&& f) {
-    for (int t0 = unit; t0 < count; t0 += 2 * nunits) {
+    for (int t0 = unit; t0 < count; t0 += (kWide ? 1 : 2) * nunits) {
         const int t1 = t0 + nunits;
-        const int nslots = t1 < count ? 2 : 1;
+        const int nslots = (!kWide && t1 < count) ? 2 : 1;   // wide tiles use both TMEM halves
         if (a.korder == 2) {
             for (int kb = 0; kb < a.nkb; ++kb)
                 for (int g = a.G - 1; g >= 0; --g)
@@ -263,11 +268,11 @@ __device__ __forceinline__ void release_slot(Smem* sh, int slot, uint32_t lane, 
     }
 }
 
-template <int kPair, bool kTrace>
+template <int kPair, bool kTrace, bool kWide = false>
 __global__ void __launch_bounds__(kThreads, 1)
     ffgemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ GemmArgs a) {
-    using K = Cfg<kPair>;
+    using K = Cfg<kPair, kWide>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     Smem* sh = reinterpret_cast<Smem*>(smem + K::STAGES * K::STAGE);
@@ -354,7 +359,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef FF_EXPERIMENTS
             int pair_idx = 0;
 #endif
-            for_each_step(a, unit, nunits, tbase, tcount, [&](int tile, int slot, int g, int kb) {
+            for_each_step<kWide>(a, unit, nunits, tbase, tcount, [&](int tile, int slot, int g, int kb) {
 #ifdef FF_EXPERIMENTS
                 if (a.throttle && leader && slot == 0 && kb == 0 && g == a.G - 1) {
                     // soft lockstep: start tile pair j only once every cluster (on
@@ -370,7 +375,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 int tm, tn;
                 tile_coords(a, tile, tm, tn);
                 const int arow = tm * K::BM + static_cast<int>(rank) * 128;
-                const int brow = tn * K::BN + static_cast<int>(rank) * (K::BN / kPair);
+                // wide: this CTA's 128 rows of each of the two 256-row B halves
+                const int brow = tn * K::BN + static_cast<int>(rank) * (kWide ? 128 : K::BN / kPair);
                 const int ks0 = kb * a.kb_iters;
                 const int ks1 = min(ks0 + a.kb_iters, a.k_iters);
                 for (int pi = a.group_first[g]; pi < a.group_first[g] + a.group_len[g]; ++pi) {
@@ -388,6 +394,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                             const uint32_t bar = ptx::mapa(ptx::smem_u32(&sh->full[stage]), 0);
                             ptx::tma_load_3d_pair(sa, &tmA, bar, ks * kBK, arow, li, polA);
                             ptx::tma_load_3d_pair(sa + K::A_BYTES, &tmB, bar, ks * kBK, brow, lj, polB);
+                            if (kWide)
+                                ptx::tma_load_3d_pair(sa + K::A_BYTES + 128 * kBK, &tmB, bar, ks * kBK, brow + kTileN,
+                                                      lj, polB);
                         }
                         if (++stage == K::STAGES) { stage = 0; phase ^= 1; }
                     }
@@ -400,7 +409,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t stage = 0, phase = 0;
             uint32_t acc_par[2] = {0, 0};
             unsigned long long t_start = clk(), w_acc = 0, w_full = 0, nsteps = 0;
-            for_each_step(a, unit, nunits, tbase, tcount, [&](int, int slot, int g, int kb) {
+            for_each_step<kWide>(a, unit, nunits, tbase, tcount, [&](int, int slot, int g, int kb) {
                 const unsigned long long t0 = kTrace ? clk() : 0;
                 if (kPair == 2) ptx::mbar_wait_cluster(&sh->accempty[slot], acc_par[slot] ^ 1);
                 else ptx::mbar_wait(&sh->accempty[slot], acc_par[slot] ^ 1);
@@ -423,10 +432,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const uint32_t sa = ptx::smem_u32(smem + stage * K::STAGE);
                         const uint64_t da = ptx::smem_desc_sw128(sa);
                         const uint64_t db = ptx::smem_desc_sw128(sa + K::A_BYTES);
+                        const uint64_t dbh = kWide ? ptx::smem_desc_sw128(sa + K::A_BYTES + 128 * kBK) : 0;
 #pragma unroll
                         for (int kk = 0; kk < kBK / kMmaK; ++kk) {
                             if (kPair == 2) ptx::mma_i8_pair(d, da + 2 * kk, db + 2 * kk, idesc, acc);
                             else ptx::mma_i8(d, da + 2 * kk, db + 2 * kk, idesc, acc);
+                            // wide: the same A k-step against the second B half, TMEM columns 256..511
+                            if (kWide) ptx::mma_i8_pair(d + kTileN, da + 2 * kk, dbh + 2 * kk, idesc, acc);
                             acc = 1u;
                         }
                         // frees the SMEM stage (in both CTAs) when these MMAs finish
@@ -469,7 +481,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             crt_group(a, M, crt_plane(a, ps, 0) + (h * 4 * 128 + crow) * 16, row, tn * K::BN + h * 64, pend_grp[ps]);
             ++pend_grp[ps];
         };
-        for_each_step(a, unit, nunits, tbase, tcount, [&](int tile, int slot, int g, int kb) {
+        for_each_step<kWide>(a, unit, nunits, tbase, tcount, [&](int tile, int slot, int g, int kb) {
             const unsigned long long t0 = kTrace ? clk() : 0;
             if (a.crt) {
                 // this slot's pending work must finish before its scratch is reused
@@ -577,13 +589,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                 int tm, tn;
                 tile_coords(a, tile, tm, tn);
                 const int row = tm * K::BM + static_cast<int>(rank) * 128 + q * 32 + static_cast<int>(lane);
+                // 32-column chunks of this thread's quarter; wide tiles: the same quarter of
+                // both 256-column halves (TMEM columns 0..255 and 256..511)
 #pragma unroll 1
-                for (int half = 0; half < 2; ++half) {
+                for (int half = 0; half < (kWide ? 4 : 2); ++half) {
                     uint32_t v[32];
-                    ptx::tmem_ld32(tcol + half * 32, v);
+                    const int coff = (half >> 1) * kTileN + (half & 1) * 32;
+                    ptx::tmem_ld32(tcol + coff, v);
                     ptx::tmem_wait_ld();
                     if (row >= a.m) continue;
-                    const int col0 = tn * K::BN + h * 64 + half * 32;
+                    const int col0 = tn * K::BN + h * 64 + coff;
 #pragma unroll
                     for (int t = 0; t < 32; ++t) v[t] = residue_i32(static_cast<int32_t>(v[t]), M);  // exact R
 
@@ -709,11 +724,11 @@ uint32_t make_idesc(bool a_signed, bool b_signed, bool saturate, int M, int N) {
 
 uint32_t shoup_host(uint32_t w, uint32_t p) { return static_cast<uint32_t>((static_cast<uint64_t>(w) << 32) / p); }
 
-template <int kPair>
+template <int kPair, bool kWide = false>
 int launch_impl(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A_limbs, const int8_t* B_limbs,
                 const OutSpec* outs, int nout, int64_t ldc, int last_use, void* scratch, cudaStream_t st,
                 const int32_t* addend, int64_t ld_add) {
-    using K = Cfg<kPair>;
+    using K = Cfg<kPair, kWide>;
     const ff_plan_info& I = pl.info;
     if (m > INT32_MAX - K::BM || n > INT32_MAX - K::BN) return -2;
     GemmArgs a;
@@ -765,6 +780,10 @@ int launch_impl(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A
         a.korder = 1;
         a.kb_iters = static_cast<int32_t>((I.kb_max / kBK) > 0 ? I.kb_max / kBK : 1);
     }
+    if (kWide) {   // single-step tiles (the caller checked k <= kb_max and one weight group)
+        a.korder = 1;
+        a.kb_iters = a.k_iters;
+    }
     a.nkb = (a.k_iters + a.kb_iters - 1) / a.kb_iters;
     a.G = I.groups;
     for (int pi = 0; pi < pl.npairs; ++pi) {
@@ -772,7 +791,7 @@ int launch_impl(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A
         a.pair_j[pi] = static_cast<int8_t>(pl.pair_j[pi]);
         const bool sa = pl.crt || I.limb_signed[pl.pair_i[pi]] != 0;   // CRT residues are s8
         const bool sb = pl.crt || I.limb_signed[pl.pair_j[pi]] != 0;
-        a.idesc[pi] = make_idesc(sa, sb, pl.saturate, K::BM, K::BN);
+        a.idesc[pi] = make_idesc(sa, sb, pl.saturate, K::BM, kWide ? kTileN : K::BN);   // wide: two N = 256 MMAs
     }
     for (int w = 0; w < I.groups; ++w) {
         a.group_first[w] = static_cast<int8_t>(pl.group_first[w]);
@@ -832,10 +851,10 @@ int launch_impl(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A
 
     CUtensorMap mapA, mapB;
     if (!make_plane_map(&mapA, A_limbs, I.L, m, I.k_pad, 128)) return FF_ERR_CUDA;
-    if (!make_plane_map(&mapB, B_limbs, I.L, n, I.k_pad, K::BN / kPair)) return FF_ERR_CUDA;
+    if (!make_plane_map(&mapB, B_limbs, I.L, n, I.k_pad, kWide ? 128 : K::BN / kPair)) return FF_ERR_CUDA;
 
-    if (set_smem_attr(reinterpret_cast<const void*>(ffgemm_tc_kernel<kPair, false>), K::SMEM) != cudaSuccess ||
-        set_smem_attr(reinterpret_cast<const void*>(ffgemm_tc_kernel<kPair, true>), K::SMEM) != cudaSuccess)
+    if (set_smem_attr(reinterpret_cast<const void*>(ffgemm_tc_kernel<kPair, false, kWide>), K::SMEM) != cudaSuccess ||
+        set_smem_attr(reinterpret_cast<const void*>(ffgemm_tc_kernel<kPair, true, kWide>), K::SMEM) != cudaSuccess)
         return FF_ERR_CUDA;
     const int64_t units = (num_sms() - pl.reserve_sms) / kPair;
     const int grid = static_cast<int>((nt < units ? nt : units) * kPair);
@@ -857,8 +876,8 @@ int launch_impl(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A
     cfg.numAttrs = a.die_map ? 3 : 2;
     note_launch();
     prof_gemm_begin(st);
-    const cudaError_t lerr = tracing ? cudaLaunchKernelEx(&cfg, ffgemm_tc_kernel<kPair, true>, mapA, mapB, a)
-                                     : cudaLaunchKernelEx(&cfg, ffgemm_tc_kernel<kPair, false>, mapA, mapB, a);
+    const cudaError_t lerr = tracing ? cudaLaunchKernelEx(&cfg, ffgemm_tc_kernel<kPair, true, kWide>, mapA, mapB, a)
+                                     : cudaLaunchKernelEx(&cfg, ffgemm_tc_kernel<kPair, false, kWide>, mapA, mapB, a);
     prof_gemm_end(st);
     if (lerr != cudaSuccess) return FF_ERR_CUDA;
     if (tracing) {  // development aid: per-CTA cycle counters, averaged over MMA-issuing CTAs
@@ -897,6 +916,14 @@ int launch_gemm_tc_multi(const Plan& pl, int64_t m, int64_t n, int64_t k, const 
     const int64_t pair_tiles = ((m + 255) / 256) * ((n + 255) / 256);
     if (pl.force_pair == 1 || (pl.force_pair == 0 && pair_tiles * 2 < num_sms()))
         return launch_impl<1>(pl, m, n, k, A_limbs, B_limbs, outs, nout, ldc, last_use, scratch, st, addend, ld_add);
+    // 256 x 512 tiles when every tile is one step (one weight group, k within the
+    // safe k-block; a forced kb_override keeps its k-blocks) and they fill the GPU
+    const ff_plan_info& I = pl.info;
+    const int64_t wide_tiles = ((m + 255) / 256) * ((n + 511) / 512);
+    if (knobs().wide && !pl.crt && I.groups == 1 && k <= I.kb_max && (I.num_kblocks <= 1 || pl.korder_auto) &&
+        wide_tiles * 2 >= num_sms())
+        return launch_impl<2, true>(pl, m, n, k, A_limbs, B_limbs, outs, nout, ldc, last_use, scratch, st, addend,
+                                    ld_add);
     return launch_impl<2>(pl, m, n, k, A_limbs, B_limbs, outs, nout, ldc, last_use, scratch, st, addend, ld_add);
 }
 

@@ -169,6 +169,7 @@ struct Knobs {
     int korder;         // FF_KORDER: 0 default, 1 group-outer, 2 k-outer
     int64_t kbloc;      // FF_KBLOC: k-outer locality bytes (0 = default)
     bool enc_notma;     // FF_ENC_NOTMA: LSU-load transposing encoders
+    bool wide;          // !FF_NOWIDE: 256 x 512 tiles for single-step GEMMs (gemm_tc.cu)
     int throttle;       // FF_THROTTLE (FF_EXPERIMENTS builds only)
     bool die_aware;     // FF_DIE_AWARE (FF_EXPERIMENTS builds only)
 };

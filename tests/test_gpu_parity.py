@@ -430,6 +430,35 @@ def _make_config(torch, ff, name):
     return A, B, C
 
 
+@pytest.mark.parametrize("p,tA,tB,m,n,k", [(251, "N", "N", 3000, 3300, 1000),   # last tile: 2nd half empty
+                                             (251, "T", "N", 3072, 3500, 1536),   # 2nd half partial
+                                             (7, "N", "T", 2600, 3900, 777),
+                                             (2, "T", "T", 3000, 3600, 2048),
+                                             (127, "N", "N", 2560, 4096, 16500)])  # long k
+def test_wide_tiles_vs_oracle(env, p, tA, tB, m, n, k):
+    """Single-step products (one limb, k within the safe k-block) with enough
+    output tiles take the 256 x 512 CTA-pair tiles (two N = 256 MMAs per A stage,
+    the accumulator in all 512 TMEM columns): ragged m, n (second 256-column half
+    of the last tile empty or partial), all transposes, alpha/beta, sampled rows
+    against the oracle and Freivalds on the whole output."""
+    torch, ff = env
+    rng = np.random.default_rng(m + n + k + p)
+    Abuf = _stored(rng, *((m, k) if tA == "N" else (k, m)), p)
+    Bbuf = _stored(rng, *((k, n) if tB == "N" else (n, k)), p)
+    Cbuf = _stored(rng, m, n, p)
+    alpha, beta = 3 % p, (p - 1) % p
+    out = _run_gpu(torch, ff, p, tA, tB, m, n, k, alpha, Abuf, Bbuf, beta, Cbuf)
+    rows = sorted(set([0, 1, 255, 256, 511, m // 2, m - 1] + rng.integers(0, m, size=4).tolist()))
+    want = oracle.fgemm_rows(p, tA, tB, alpha, Abuf, Bbuf, beta, Cbuf[rows], rows, m, n, k)
+    np.testing.assert_array_equal(out[rows], want)
+    for t in range(3):
+        x = rng.integers(0, p, size=n).astype(np.int32)
+        lhs = oracle.matvec(p, "N", out, x).astype(np.int64)
+        abx = oracle.matvec(p, tA, Abuf, oracle.matvec(p, tB, Bbuf, x)).astype(np.int64)
+        rhs = (alpha * abx + beta * oracle.matvec(p, "N", Cbuf, x).astype(np.int64)) % p
+        np.testing.assert_array_equal(lhs, rhs)
+
+
 @pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
 def test_baseline_config_sampled_rows_and_freivalds(env, name):
     torch, ff = env
