@@ -43,6 +43,7 @@ namespace {
 constexpr int kNumEpiWarps = 16;  // 4 per TMEM lane quadrant, 64 columns each
 constexpr int kThreads = 32 * (2 + kNumEpiWarps);
 constexpr int kTmemCols = 512;  // two 256-column s32 accumulators
+constexpr int kWideDelta = 32;     // wide tiles: staggered k-steps (wide_phases; swept on c3)
 constexpr int kRasterDefault = 12;  // tile-rows per raster band (L2 reuse; swept on c4: DESIGN.md §16)
 
 // kWide (CTA pair only): 256 x 512 tiles, two N = 256 MMAs per k-step sharing the
@@ -101,7 +102,23 @@ struct GemmArgs {
     int64_t ld_add;             //   with `add` set (Winograd temporaries U2 = P1 + P6)
     CrtConsts cc;
     uint8_t* scratch;           // CRT: per CTA and slot, G byte planes of kCrtPlane bytes
+    int32_t wdelta;             // wide tiles: k-steps of the staggered halves (wide_phases)
 };
+
+// Wide tiles (kWide): the two 256-column halves are staggered by D k-steps so the
+// epilogue of one half overlaps MMAs of the other: per tile, k-steps [0, D) for
+// the low half only, [D, K) for both (one A stage feeds two MMAs), then [0, D)
+// for the high half only.  The low half completes D k-steps before the high
+// half; the next tile starts on the low half while the epilogue drains the high
+// one.  Producer and MMA walk the same (k-step, lo, hi) sequence.
+template <class F>
+__device__ __forceinline__ void wide_phases(const GemmArgs& a, F&& f) {
+    const int K = a.k_iters;
+    const int D = min(a.wdelta, K / 2);
+    for (int ks = 0; ks < D; ++ks) f(ks, true, false);
+    for (int ks = D; ks < K; ++ks) f(ks, true, true);
+    for (int ks = 0; ks < D; ++ks) f(ks, false, true);
+}
 
 // CRT residue scratch: one 128 x 256 byte plane per (CTA, slot, modulus 0..G-1),
 // laid out [h: 64-column quarter][c: 16-column chunk][row 0..127][16 bytes] so
@@ -377,6 +394,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int arow = tm * K::BM + static_cast<int>(rank) * 128;
                 // wide: this CTA's 128 rows of each of the two 256-row B halves
                 const int brow = tn * K::BN + static_cast<int>(rank) * (kWide ? 128 : K::BN / kPair);
+                if constexpr (kWide) {   // single-step tile: one limb pair (0, 0), staggered halves
+                    wide_phases(a, [&](int ks, bool lo, bool hi) {
+                        ptx::mbar_wait_sleep(&sh->empty[stage], phase ^ 1);
+                        uint8_t* sa = smem + stage * K::STAGE;
+                        const int bytes = K::A_BYTES + (lo ? 128 * kBK : 0) + (hi ? 128 * kBK : 0);
+                        if (leader) ptx::mbar_arrive_expect_tx(&sh->full[stage], 2 * bytes);
+                        const uint32_t bar = ptx::mapa(ptx::smem_u32(&sh->full[stage]), 0);
+                        ptx::tma_load_3d_pair(sa, &tmA, bar, ks * kBK, arow, 0, polA);
+                        if (lo) ptx::tma_load_3d_pair(sa + K::A_BYTES, &tmB, bar, ks * kBK, brow, 0, polB);
+                        if (hi)
+                            ptx::tma_load_3d_pair(sa + K::A_BYTES + 128 * kBK, &tmB, bar, ks * kBK, brow + kTileN, 0,
+                                                  polB);
+                        if (++stage == K::STAGES) { stage = 0; phase ^= 1; }
+                    });
+                    return;
+                }
                 const int ks0 = kb * a.kb_iters;
                 const int ks1 = min(ks0 + a.kb_iters, a.k_iters);
                 for (int pi = a.group_first[g]; pi < a.group_first[g] + a.group_len[g]; ++pi) {
@@ -394,9 +427,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                             const uint32_t bar = ptx::mapa(ptx::smem_u32(&sh->full[stage]), 0);
                             ptx::tma_load_3d_pair(sa, &tmA, bar, ks * kBK, arow, li, polA);
                             ptx::tma_load_3d_pair(sa + K::A_BYTES, &tmB, bar, ks * kBK, brow, lj, polB);
-                            if (kWide)
-                                ptx::tma_load_3d_pair(sa + K::A_BYTES + 128 * kBK, &tmB, bar, ks * kBK, brow + kTileN,
-                                                      lj, polB);
                         }
                         if (++stage == K::STAGES) { stage = 0; phase ^= 1; }
                     }
@@ -410,6 +440,48 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t acc_par[2] = {0, 0};
             unsigned long long t_start = clk(), w_acc = 0, w_full = 0, nsteps = 0;
             for_each_step<kWide>(a, unit, nunits, tbase, tcount, [&](int, int slot, int g, int kb) {
+                if constexpr (kWide) {   // staggered halves (wide_phases): slot 0 = low, 1 = high half
+                    const unsigned long long tw = kTrace ? clk() : 0;
+                    ptx::mbar_wait_cluster(&sh->accempty[0], acc_par[0] ^ 1);
+                    acc_par[0] ^= 1;
+                    if (kTrace) { w_acc += clk() - tw; ++nsteps; }
+                    ptx::tc_fence_after();
+                    uint32_t acc_lo = 0, acc_hi = 0;
+                    bool hi_ready = false;
+                    const uint32_t idesc = a.idesc[0];
+                    int done = 0;
+                    wide_phases(a, [&](int, bool lo, bool hi) {
+                        if (hi && !hi_ready) {   // first high-half MMA: its TMEM half must be free
+                            const unsigned long long th = kTrace ? clk() : 0;
+                            ptx::mbar_wait_cluster(&sh->accempty[1], acc_par[1] ^ 1);
+                            acc_par[1] ^= 1;
+                            if (kTrace) w_acc += clk() - th;
+                            ptx::tc_fence_after();
+                            hi_ready = true;
+                        }
+                        const unsigned long long t1 = kTrace ? clk() : 0;
+                        ptx::mbar_wait(&sh->full[stage], phase);
+                        if (kTrace) w_full += clk() - t1;
+                        ptx::tc_fence_after();
+                        const uint32_t sa = ptx::smem_u32(smem + stage * K::STAGE);
+                        const uint64_t da = ptx::smem_desc_sw128(sa);
+                        const uint64_t dbl = ptx::smem_desc_sw128(sa + K::A_BYTES);
+                        const uint64_t dbh = ptx::smem_desc_sw128(sa + K::A_BYTES + 128 * kBK);
+#pragma unroll
+                        for (int kk = 0; kk < kBK / kMmaK; ++kk) {
+                            if (lo) ptx::mma_i8_pair(tmem_base, da + 2 * kk, dbl + 2 * kk, idesc, acc_lo);
+                            if (hi) ptx::mma_i8_pair(tmem_base + kTileN, da + 2 * kk, dbh + 2 * kk, idesc, acc_hi);
+                            if (lo) acc_lo = 1u;
+                            if (hi) acc_hi = 1u;
+                        }
+                        ptx::tc_commit_pair(&sh->empty[stage]);
+                        if (++stage == K::STAGES) { stage = 0; phase ^= 1; }
+                        // the low half is complete after its last k-step (phase 2 end)
+                        if (++done == a.k_iters) ptx::tc_commit_pair(&sh->accfull[0]);
+                    });
+                    ptx::tc_commit_pair(&sh->accfull[1]);
+                    return;
+                }
                 const unsigned long long t0 = kTrace ? clk() : 0;
                 if (kPair == 2) ptx::mbar_wait_cluster(&sh->accempty[slot], acc_par[slot] ^ 1);
                 else ptx::mbar_wait(&sh->accempty[slot], acc_par[slot] ^ 1);
@@ -432,13 +504,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const uint32_t sa = ptx::smem_u32(smem + stage * K::STAGE);
                         const uint64_t da = ptx::smem_desc_sw128(sa);
                         const uint64_t db = ptx::smem_desc_sw128(sa + K::A_BYTES);
-                        const uint64_t dbh = kWide ? ptx::smem_desc_sw128(sa + K::A_BYTES + 128 * kBK) : 0;
 #pragma unroll
                         for (int kk = 0; kk < kBK / kMmaK; ++kk) {
                             if (kPair == 2) ptx::mma_i8_pair(d, da + 2 * kk, db + 2 * kk, idesc, acc);
                             else ptx::mma_i8(d, da + 2 * kk, db + 2 * kk, idesc, acc);
-                            // wide: the same A k-step against the second B half, TMEM columns 256..511
-                            if (kWide) ptx::mma_i8_pair(d + kTileN, da + 2 * kk, dbh + 2 * kk, idesc, acc);
                             acc = 1u;
                         }
                         // frees the SMEM stage (in both CTAs) when these MMAs finish
@@ -593,6 +662,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // both 256-column halves (TMEM columns 0..255 and 256..511)
 #pragma unroll 1
                 for (int half = 0; half < (kWide ? 4 : 2); ++half) {
+                    if (kWide && half == 2) {
+                        // low half done: hand it to the next tile's first k-steps, then
+                        // wait for the high half (wide_phases)
+                        release_slot<kPair>(sh, 0, lane, accempty_leader0, accempty_leader1);
+                        ptx::mbar_wait_sleep(&sh->accfull[1], acc_par[1]);
+                        acc_par[1] ^= 1;
+                        ptx::tc_fence_after();
+                    }
                     uint32_t v[32];
                     const int coff = (half >> 1) * kTileN + (half & 1) * 32;
                     ptx::tmem_ld32(tcol + coff, v);
@@ -651,7 +728,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
             }
-            if (!crt_final) release_slot<kPair>(sh, slot, lane, accempty_leader0, accempty_leader1);
+            if (!crt_final) release_slot<kPair>(sh, kWide ? 1 : slot, lane, accempty_leader0, accempty_leader1);
             if (kTrace) {
                 const unsigned long long t2 = clk();
                 e_wait += t1 - t0;
@@ -784,6 +861,7 @@ int launch_impl(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A
         a.korder = 1;
         a.kb_iters = a.k_iters;
     }
+    a.wdelta = knobs().wdelta > 0 ? knobs().wdelta : kWideDelta;
     a.nkb = (a.k_iters + a.kb_iters - 1) / a.kb_iters;
     a.G = I.groups;
     for (int pi = 0; pi < pl.npairs; ++pi) {

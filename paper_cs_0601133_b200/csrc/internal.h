@@ -170,6 +170,7 @@ struct Knobs {
     int64_t kbloc;      // FF_KBLOC: k-outer locality bytes (0 = default)
     bool enc_notma;     // FF_ENC_NOTMA: LSU-load transposing encoders
     bool wide;          // !FF_NOWIDE: 256 x 512 tiles for single-step GEMMs (gemm_tc.cu)
+    int wdelta;         // FF_WDELTA: staggered k-steps of the wide tiles' halves (0 = default)
     int throttle;       // FF_THROTTLE (FF_EXPERIMENTS builds only)
     bool die_aware;     // FF_DIE_AWARE (FF_EXPERIMENTS builds only)
 };
