@@ -117,7 +117,11 @@ typedef struct ff_opts {
                                size rule, 1 the mma.sync kernels whenever they apply, 2 the
                                tcgen05 split-K kernel whenever it applies, -1 never (results
                                are identical) */
-    int32_t reserved[1];
+    int32_t wide_tiles;     /* tcgen05 GEMM tile shape: 0 auto (256 x 512 CTA-pair tiles with
+                               staggered halves for one-limb plans, p < 256, when they fill
+                               the GPU), 1 256 x 512 whenever the plan's steps
+                               may run group-outer (limb schemes), -1 never.  Results are
+                               identical. */
 } ff_opts;
 
 /* The plan the library derives from (p, k, opts): host-only, no GPU needed. */

@@ -311,6 +311,7 @@ const Knobs& knobs() {
         v.enc_notma = getenv("FF_ENC_NOTMA") != nullptr;
         v.wide = getenv("FF_NOWIDE") == nullptr;
         v.wdelta = env_int("FF_WDELTA", 0);
+        v.wdelta_wb = env_int("FF_WDELTA_WB", 0);
 #ifdef FF_EXPERIMENTS
         v.throttle = env_int("FF_THROTTLE", 0);
         v.die_aware = getenv("FF_DIE_AWARE") != nullptr && getenv("FF_NO_DIE_AWARE") == nullptr;

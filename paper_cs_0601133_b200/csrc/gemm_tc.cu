@@ -43,7 +43,9 @@ namespace {
 constexpr int kNumEpiWarps = 16;  // 4 per TMEM lane quadrant, 64 columns each
 constexpr int kThreads = 32 * (2 + kNumEpiWarps);
 constexpr int kTmemCols = 512;  // two 256-column s32 accumulators
-constexpr int kWideDelta = 32;     // wide tiles: staggered k-steps (wide_phases; swept on c3)
+constexpr double kL2PlanesBytes = 192.0 * (1 << 20);   // operand planes "fit the L2" (launch_impl)
+constexpr int kWideDelta = 32;     // wide tiles: staggered k-steps before the final output (swept on c3)
+constexpr int kWideDeltaWb = 6;    //   before a TMEM write-back step (swept on c2)
 constexpr int kRasterDefault = 12;  // tile-rows per raster band (L2 reuse; swept on c4: DESIGN.md §16)
 
 // kWide (CTA pair only): 256 x 512 tiles, two N = 256 MMAs per k-step sharing the
@@ -102,22 +104,36 @@ struct GemmArgs {
     int64_t ld_add;             //   with `add` set (Winograd temporaries U2 = P1 + P6)
     CrtConsts cc;
     uint8_t* scratch;           // CRT: per CTA and slot, G byte planes of kCrtPlane bytes
-    int32_t wdelta;             // wide tiles: k-steps of the staggered halves (wide_phases)
+    int32_t wdelta;             // wide tiles: k-steps of the staggered halves (wide_phases), final steps
+    int32_t wdelta_wb;          //   the same before a write-back step
 };
 
-// Wide tiles (kWide): the two 256-column halves are staggered by D k-steps so the
-// epilogue of one half overlaps MMAs of the other: per tile, k-steps [0, D) for
-// the low half only, [D, K) for both (one A stage feeds two MMAs), then [0, D)
-// for the high half only.  The low half completes D k-steps before the high
-// half; the next tile starts on the low half while the epilogue drains the high
-// one.  Producer and MMA walk the same (k-step, lo, hi) sequence.
+// Wide tiles (kWide): the two 256-column halves are staggered by D MMA k-steps so
+// the epilogue of one half overlaps MMAs of the other.  A step's MMA k-steps are
+// its (limb pair, k-slice) list, sigma = 0 .. S-1 (pair-major); per step: sigma in
+// [0, D) for the low half only, [D, S) for both (one A stage feeds two MMAs), then
+// [0, D) for the high half only.  The low half completes D k-steps before the
+// high half; the next step (or tile) starts on the low half while the epilogue
+// drains the high one.  Producer and MMA walk the same (pair, k-slice, lo, hi)
+// sequence.  D: wdelta after the last step of a tile (final output), wdelta_wb
+// after the others (TMEM write-back only).
 template <class F>
-__device__ __forceinline__ void wide_phases(const GemmArgs& a, F&& f) {
-    const int K = a.k_iters;
-    const int D = min(a.wdelta, K / 2);
-    for (int ks = 0; ks < D; ++ks) f(ks, true, false);
-    for (int ks = D; ks < K; ++ks) f(ks, true, true);
-    for (int ks = 0; ks < D; ++ks) f(ks, false, true);
+__device__ __forceinline__ void wide_phases(const GemmArgs& a, int g, int kb, F&& f) {
+    const int ks0 = kb * a.kb_iters;
+    const int nks = min(ks0 + a.kb_iters, a.k_iters) - ks0;
+    const int S = a.group_len[g] * nks;
+    const bool final_step = (kb == a.nkb - 1) && g == 0;
+    const int D = min(final_step ? a.wdelta : a.wdelta_wb, S / 2);
+    auto run = [&](int s0, int s1, bool lo, bool hi) {   // one division per phase, not per k-step
+        int q = s0 / nks, ks = s0 - q * nks;
+        for (int sg = s0; sg < s1; ++sg) {
+            f(a.group_first[g] + q, ks0 + ks, lo, hi);
+            if (++ks == nks) { ks = 0; ++q; }
+        }
+    };
+    run(0, D, true, false);
+    run(D, S, true, true);
+    run(0, D, false, true);
 }
 
 // CRT residue scratch: one 128 x 256 byte plane per (CTA, slot, modulus 0..G-1),
@@ -394,17 +410,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int arow = tm * K::BM + static_cast<int>(rank) * 128;
                 // wide: this CTA's 128 rows of each of the two 256-row B halves
                 const int brow = tn * K::BN + static_cast<int>(rank) * (kWide ? 128 : K::BN / kPair);
-                if constexpr (kWide) {   // single-step tile: one limb pair (0, 0), staggered halves
-                    wide_phases(a, [&](int ks, bool lo, bool hi) {
+                if constexpr (kWide) {   // staggered halves (wide_phases)
+                    wide_phases(a, g, kb, [&](int pi, int ks, bool lo, bool hi) {
+                        const int li = a.pair_i[pi], lj = a.pair_j[pi];
                         ptx::mbar_wait_sleep(&sh->empty[stage], phase ^ 1);
                         uint8_t* sa = smem + stage * K::STAGE;
                         const int bytes = K::A_BYTES + (lo ? 128 * kBK : 0) + (hi ? 128 * kBK : 0);
                         if (leader) ptx::mbar_arrive_expect_tx(&sh->full[stage], 2 * bytes);
                         const uint32_t bar = ptx::mapa(ptx::smem_u32(&sh->full[stage]), 0);
-                        ptx::tma_load_3d_pair(sa, &tmA, bar, ks * kBK, arow, 0, polA);
-                        if (lo) ptx::tma_load_3d_pair(sa + K::A_BYTES, &tmB, bar, ks * kBK, brow, 0, polB);
+                        ptx::tma_load_3d_pair(sa, &tmA, bar, ks * kBK, arow, li, polA);
+                        if (lo) ptx::tma_load_3d_pair(sa + K::A_BYTES, &tmB, bar, ks * kBK, brow, lj, polB);
                         if (hi)
-                            ptx::tma_load_3d_pair(sa + K::A_BYTES + 128 * kBK, &tmB, bar, ks * kBK, brow + kTileN, 0,
+                            ptx::tma_load_3d_pair(sa + K::A_BYTES + 128 * kBK, &tmB, bar, ks * kBK, brow + kTileN, lj,
                                                   polB);
                         if (++stage == K::STAGES) { stage = 0; phase ^= 1; }
                     });
@@ -446,11 +463,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                     acc_par[0] ^= 1;
                     if (kTrace) { w_acc += clk() - tw; ++nsteps; }
                     ptx::tc_fence_after();
-                    uint32_t acc_lo = 0, acc_hi = 0;
+                    // the first step of a tile overwrites; later ones accumulate onto the write-back
+                    const uint32_t acc0 = (g == a.G - 1 && kb == 0) ? 0u : 1u;
+                    uint32_t acc_lo = acc0, acc_hi = acc0;
                     bool hi_ready = false;
-                    const uint32_t idesc = a.idesc[0];
                     int done = 0;
-                    wide_phases(a, [&](int, bool lo, bool hi) {
+                    const int ks0 = kb * a.kb_iters;
+                    const int nlo = a.group_len[g] * (min(ks0 + a.kb_iters, a.k_iters) - ks0);
+                    wide_phases(a, g, kb, [&](int pi, int, bool lo, bool hi) {
+                        const uint32_t idesc = a.idesc[pi];
                         if (hi && !hi_ready) {   // first high-half MMA: its TMEM half must be free
                             const unsigned long long th = kTrace ? clk() : 0;
                             ptx::mbar_wait_cluster(&sh->accempty[1], acc_par[1] ^ 1);
@@ -476,8 +497,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                         ptx::tc_commit_pair(&sh->empty[stage]);
                         if (++stage == K::STAGES) { stage = 0; phase ^= 1; }
-                        // the low half is complete after its last k-step (phase 2 end)
-                        if (++done == a.k_iters) ptx::tc_commit_pair(&sh->accfull[0]);
+                        // the low half is complete after its last k-step (end of the shared phase)
+                        if (lo && ++done == nlo) ptx::tc_commit_pair(&sh->accfull[0]);
                     });
                     ptx::tc_commit_pair(&sh->accfull[1]);
                     return;
@@ -632,9 +653,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::tmem_st64(tcol, v);
                 ptx::tmem_wait_st();
             } else if (!final_step) {
-                // delayed reduction between steps (+ Horner x256 before the next-lower group)
+                // delayed reduction between steps (+ Horner x256 before the next-lower group);
+                // wide tiles: the low half, hand it back, then the high half (wide_phases)
+#pragma unroll 1
+              for (int hs = 0; hs < (kWide ? 2 : 1); ++hs) {
+                if (kWide && hs == 1) {
+                    release_slot<kPair>(sh, 0, lane, accempty_leader0, accempty_leader1);
+                    ptx::mbar_wait_sleep(&sh->accfull[1], acc_par[1]);
+                    acc_par[1] ^= 1;
+                    ptx::tc_fence_after();
+                }
+                const uint32_t tcw = tcol + hs * kTileN;
                 uint32_t v[64];
-                ptx::tmem_ld64(tcol, v);
+                ptx::tmem_ld64(tcw, v);
                 ptx::tmem_wait_ld();
                 const int32_t w = horner ? 256 : 1;
                 if (M.int_wb) {
@@ -649,8 +680,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                         v[t] = static_cast<uint32_t>(reduce_approx(static_cast<int32_t>(v[t]), w, f,
                                                                    static_cast<int32_t>(M.p)));
                 }
-                ptx::tmem_st64(tcol, v);
+                ptx::tmem_st64(tcw, v);
                 ptx::tmem_wait_st();
+              }
             } else if (a.crt) {
                 pend_tile[slot] = tile;        // deferred: see pend_work
                 pend_grp[slot] = 0;
@@ -851,17 +883,17 @@ int launch_impl(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A
     // (1 GiB of planes) -5% with k-outer, c2 (100 MB) +6%, c1/c3 equal or better
     // group-outer).  Below kL2Planes the default falls back to group-outer with
     // the safe k-block.
-    constexpr double kL2Planes = 192.0 * (1 << 20);
     if (pl.korder_auto && pl.korder == 2 &&
-        static_cast<double>(I.L) * static_cast<double>(m + n) * static_cast<double>(I.k_pad) <= kL2Planes) {
+        static_cast<double>(I.L) * static_cast<double>(m + n) * static_cast<double>(I.k_pad) <= kL2PlanesBytes) {
         a.korder = 1;
         a.kb_iters = static_cast<int32_t>((I.kb_max / kBK) > 0 ? I.kb_max / kBK : 1);
     }
-    if (kWide) {   // single-step tiles (the caller checked k <= kb_max and one weight group)
+    if (kWide) {   // group-outer steps (the caller checked the order is free or group-outer)
         a.korder = 1;
-        a.kb_iters = a.k_iters;
+        if (pl.korder_auto) a.kb_iters = static_cast<int32_t>((I.kb_max / kBK) > 0 ? I.kb_max / kBK : 1);
     }
     a.wdelta = knobs().wdelta > 0 ? knobs().wdelta : kWideDelta;
+    a.wdelta_wb = knobs().wdelta_wb > 0 ? knobs().wdelta_wb : kWideDeltaWb;
     a.nkb = (a.k_iters + a.kb_iters - 1) / a.kb_iters;
     a.G = I.groups;
     for (int pi = 0; pi < pl.npairs; ++pi) {
@@ -994,12 +1026,21 @@ int launch_gemm_tc_multi(const Plan& pl, int64_t m, int64_t n, int64_t k, const 
     const int64_t pair_tiles = ((m + 255) / 256) * ((n + 255) / 256);
     if (pl.force_pair == 1 || (pl.force_pair == 0 && pair_tiles * 2 < num_sms()))
         return launch_impl<1>(pl, m, n, k, A_limbs, B_limbs, outs, nout, ldc, last_use, scratch, st, addend, ld_add);
-    // 256 x 512 tiles when every tile is one step (one weight group, k within the
-    // safe k-block; a forced kb_override keeps its k-blocks) and they fill the GPU
+    // 256 x 512 tiles (limb plans) when the steps may run group-outer -- one weight
+    // group, or operand planes that fit the L2 (else k-outer order is kept for DRAM
+    // locality, launch_impl) -- and the wide tiles fill the GPU
     const ff_plan_info& I = pl.info;
     const int64_t wide_tiles = ((m + 255) / 256) * ((n + 511) / 512);
-    if (knobs().wide && !pl.crt && I.groups == 1 && k <= I.kb_max && (I.num_kblocks <= 1 || pl.korder_auto) &&
-        wide_tiles * 2 >= num_sms())
+    const bool group_outer_ok =
+        pl.korder == 1 ||
+        (pl.korder_auto && (I.groups == 1 ||
+                            static_cast<double>(I.L) * static_cast<double>(m + n) * static_cast<double>(I.k_pad) <=
+                                kL2PlanesBytes));
+    // auto: one weight group only (c3: -4%); with several groups the write-back
+    // steps' staggered k-steps re-read A and it measured neutral (c2) or slower
+    // (ftrsm 8192 +2%), so that is opt-in (ff_opts.wide_tiles = 1)
+    const bool wide = pl.wide > 0 || (pl.wide == 0 && I.groups == 1 && wide_tiles * 2 >= num_sms());
+    if (wide && !pl.crt && group_outer_ok)
         return launch_impl<2, true>(pl, m, n, k, A_limbs, B_limbs, outs, nout, ldc, last_use, scratch, st, addend,
                                     ld_add);
     return launch_impl<2>(pl, m, n, k, A_limbs, B_limbs, outs, nout, ldc, last_use, scratch, st, addend, ld_add);

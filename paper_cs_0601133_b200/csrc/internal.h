@@ -74,6 +74,7 @@ struct Plan {
     bool canonical_ab;               // (internal callers) A, B hold canonical residues in [0, p)
     int small_mode;                  // small-field kernels: -1 size rule, 0 never, 1 mma.sync kernels
                                      // whenever valid, 2 the tcgen05 latency kernel whenever valid
+    int wide;                        // ff_opts.wide_tiles: 0 auto, 1 force, -1 never (gemm_tc.cu)
 };
 
 constexpr int64_t kKbLocalityBytes = 8192;  // L * kb per row-slice in k-outer order (swept on c4, c5)
@@ -171,6 +172,7 @@ struct Knobs {
     bool enc_notma;     // FF_ENC_NOTMA: LSU-load transposing encoders
     bool wide;          // !FF_NOWIDE: 256 x 512 tiles for single-step GEMMs (gemm_tc.cu)
     int wdelta;         // FF_WDELTA: staggered k-steps of the wide tiles' halves (0 = default)
+    int wdelta_wb;      // FF_WDELTA_WB: the same before write-back steps (0 = default)
     int throttle;       // FF_THROTTLE (FF_EXPERIMENTS builds only)
     bool die_aware;     // FF_DIE_AWARE (FF_EXPERIMENTS builds only)
 };

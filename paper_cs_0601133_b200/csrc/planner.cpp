@@ -326,6 +326,7 @@ int make_plan(uint32_t p, int64_t k, const ff_opts* opts, Plan* out) {
     if (o.korder < 0 || o.korder > 2) return FF_ERR_OPTS;
     if (o.inputs_canonical < 0 || o.inputs_canonical > 1) return FF_ERR_OPTS;
     if (o.small_path < -1 || o.small_path > 2) return FF_ERR_OPTS;
+    if (o.wide_tiles < -1 || o.wide_tiles > 1) return FF_ERR_OPTS;
 
     Plan pl;
     std::memset(&pl, 0, sizeof(pl));
@@ -333,6 +334,7 @@ int make_plan(uint32_t p, int64_t k, const ff_opts* opts, Plan* out) {
                   o.korder == 0 && o.debug_saturate == 0 && o.debug_unchecked_kb == 0;
     pl.canonical_ab = o.inputs_canonical != 0;
     pl.small_mode = o.small_path != 0 ? (o.small_path > 0 ? o.small_path : 0) : knobs().small;
+    pl.wide = knobs().wide ? o.wide_tiles : -1;
     ff_plan_info& I = pl.info;
     // Centred residues lie in [-neg, half]: neg = half for odd p, half + 1 for p = 2.
     const int64_t half = (int64_t)(p - 1) / 2;

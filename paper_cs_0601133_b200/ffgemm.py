@@ -36,7 +36,7 @@ class ff_opts(ctypes.Structure):
     _fields_ = [("winograd", _i32), ("scheme", _i32), ("kb_override", _i64),
                 ("debug_saturate", _i32), ("cta_group", _i32), ("host_block", _i32),
                 ("korder", _i32), ("debug_unchecked_kb", _i32), ("inputs_canonical", _i32),
-                ("small_path", _i32), ("reserved", _i32 * 1)]
+                ("small_path", _i32), ("wide_tiles", _i32)]
 
 
 class ff_plan_info(ctypes.Structure):

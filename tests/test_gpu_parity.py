@@ -430,24 +430,33 @@ def _make_config(torch, ff, name):
     return A, B, C
 
 
-@pytest.mark.parametrize("p,tA,tB,m,n,k", [(251, "N", "N", 3000, 3300, 1000),   # last tile: 2nd half empty
-                                             (251, "T", "N", 3072, 3500, 1536),   # 2nd half partial
-                                             (7, "N", "T", 2600, 3900, 777),
-                                             (2, "T", "T", 3000, 3600, 2048),
-                                             (127, "N", "N", 2560, 4096, 16500)])  # long k
-def test_wide_tiles_vs_oracle(env, p, tA, tB, m, n, k):
-    """Single-step products (one limb, k within the safe k-block) with enough
-    output tiles take the 256 x 512 CTA-pair tiles (two N = 256 MMAs per A stage,
-    the accumulator in all 512 TMEM columns): ragged m, n (second 256-column half
-    of the last tile empty or partial), all transposes, alpha/beta, sampled rows
-    against the oracle and Freivalds on the whole output."""
+@pytest.mark.parametrize("p,tA,tB,m,n,k,opts", [
+    (251, "N", "N", 3000, 3300, 1000, None),       # one limb; last tile: 2nd half empty
+    (251, "T", "N", 3072, 3500, 1536, None),       # 2nd half partial
+    (7, "N", "T", 2600, 3900, 777, None),
+    (2, "T", "T", 3000, 3600, 2048, None),
+    (127, "N", "N", 2560, 4096, 16500, None),      # long k
+    (65521, "N", "N", 3000, 3300, 1000, None),     # 2 limbs (T): 3 weight groups, Horner write-backs
+    (8388593, "T", "N", 3072, 3500, 1536, None),   # 3 limbs (S): 5 groups
+    (65537, "N", "T", 2600, 3900, 777, {"scheme": 1}),                  # 3 limbs, ragged
+    (65521, "N", "N", 3000, 3300, 1000, {"kb_override": 256, "korder": 1}),  # mid-k reductions
+])
+def test_wide_tiles_vs_oracle(env, p, tA, tB, m, n, k, opts):
+    """256 x 512 CTA-pair tiles (ff_opts.wide_tiles = 1; automatic for one limb):
+    two N = 256 MMAs per A stage, the accumulator in all 512 TMEM columns, halves
+    staggered through every write-back and the final output.  One to three limbs,
+    forced k-blocks, ragged m, n (second 256-column half of the last tile empty or
+    partial), all transposes, alpha/beta: bit-identical to the 256 x 256 tiles
+    (wide_tiles = -1), sampled rows against the oracle, Freivalds on the whole output."""
     torch, ff = env
     rng = np.random.default_rng(m + n + k + p)
     Abuf = _stored(rng, *((m, k) if tA == "N" else (k, m)), p)
     Bbuf = _stored(rng, *((k, n) if tB == "N" else (n, k)), p)
     Cbuf = _stored(rng, m, n, p)
     alpha, beta = 3 % p, (p - 1) % p
-    out = _run_gpu(torch, ff, p, tA, tB, m, n, k, alpha, Abuf, Bbuf, beta, Cbuf)
+    out = _run_gpu(torch, ff, p, tA, tB, m, n, k, alpha, Abuf, Bbuf, beta, Cbuf, dict(opts or {}, wide_tiles=1))
+    square = _run_gpu(torch, ff, p, tA, tB, m, n, k, alpha, Abuf, Bbuf, beta, Cbuf, dict(opts or {}, wide_tiles=-1))
+    np.testing.assert_array_equal(out, square)           # 256 x 512 and 256 x 256 tiles agree bit for bit
     rows = sorted(set([0, 1, 255, 256, 511, m // 2, m - 1] + rng.integers(0, m, size=4).tolist()))
     want = oracle.fgemm_rows(p, tA, tB, alpha, Abuf, Bbuf, beta, Cbuf[rows], rows, m, n, k)
     np.testing.assert_array_equal(out[rows], want)

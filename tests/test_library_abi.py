@@ -206,6 +206,14 @@ def test_f64_plan_is_paper_eq2(ff):
         ff.ff_plan_query(65521, 10, {"scheme": 4, "kb_override": 2 ** 23})
 
 
+def test_wide_tiles_option_rules(ff):
+    for v in (-1, 0, 1):
+        ff.ff_plan_query(251, 5000, {"wide_tiles": v})
+    for v in (-2, 2):
+        with pytest.raises(ff.FFError):
+            ff.ff_plan_query(251, 5000, {"wide_tiles": v})
+
+
 def test_struct_layouts_match_the_header(ff, tmp_path):
     """The ctypes mirrors of ff_opts and ff_plan_info (the Python binding) have
     the header's size and field offsets: compiled and measured with the host C
