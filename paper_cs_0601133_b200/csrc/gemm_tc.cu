@@ -643,15 +643,25 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (a.crt && !final_step) {
                 // (done above)
             } else if (rescale) {
+#pragma unroll 1
+              for (int hs = 0; hs < (kWide ? 2 : 1); ++hs) {   // wide: low half, hand-off, high half
+                if (kWide && hs == 1) {
+                    release_slot<kPair>(sh, 0, lane, accempty_leader0, accempty_leader1);
+                    ptx::mbar_wait_sleep(&sh->accfull[1], acc_par[1]);
+                    acc_par[1] ^= 1;
+                    ptx::tc_fence_after();
+                }
+                const uint32_t tcw = tcol + hs * kTileN;
                 uint32_t v[64];
-                ptx::tmem_ld64(tcol, v);
+                ptx::tmem_ld64(tcw, v);
                 ptx::tmem_wait_ld();
 #pragma unroll
                 for (int t = 0; t < 64; ++t)
                     v[t] = static_cast<uint32_t>(centre(mulmod_shoup(residue_i32(static_cast<int32_t>(v[t]), M),
                                                                      a.kinv, a.kinv_sh, M.p), M));
-                ptx::tmem_st64(tcol, v);
+                ptx::tmem_st64(tcw, v);
                 ptx::tmem_wait_st();
+              }
             } else if (!final_step) {
                 // delayed reduction between steps (+ Horner x256 before the next-lower group);
                 // wide tiles: the low half, hand it back, then the high half (wide_phases)
@@ -888,7 +898,7 @@ int launch_impl(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A
         a.korder = 1;
         a.kb_iters = static_cast<int32_t>((I.kb_max / kBK) > 0 ? I.kb_max / kBK : 1);
     }
-    if (kWide) {   // group-outer steps (the caller checked the order is free or group-outer)
+    if (kWide && pl.wide == 0) {   // auto (one weight group): one safe k-block, group-outer
         a.korder = 1;
         if (pl.korder_auto) a.kb_iters = static_cast<int32_t>((I.kb_max / kBK) > 0 ? I.kb_max / kBK : 1);
     }
@@ -1039,8 +1049,9 @@ int launch_gemm_tc_multi(const Plan& pl, int64_t m, int64_t n, int64_t k, const 
     // auto: one weight group only (c3: -4%); with several groups the write-back
     // steps' staggered k-steps re-read A and it measured neutral (c2) or slower
     // (ftrsm 8192 +2%), so that is opt-in (ff_opts.wide_tiles = 1)
-    const bool wide = pl.wide > 0 || (pl.wide == 0 && I.groups == 1 && wide_tiles * 2 >= num_sms());
-    if (wide && !pl.crt && group_outer_ok)
+    const bool wide = (pl.wide > 0 && !pl.crt) ||
+                      (pl.wide == 0 && !pl.crt && group_outer_ok && I.groups == 1 && wide_tiles * 2 >= num_sms());
+    if (wide)
         return launch_impl<2, true>(pl, m, n, k, A_limbs, B_limbs, outs, nout, ldc, last_use, scratch, st, addend,
                                     ld_add);
     return launch_impl<2>(pl, m, n, k, A_limbs, B_limbs, outs, nout, ldc, last_use, scratch, st, addend, ld_add);

@@ -440,6 +440,8 @@ def _make_config(torch, ff, name):
     (8388593, "T", "N", 3072, 3500, 1536, None),   # 3 limbs (S): 5 groups
     (65537, "N", "T", 2600, 3900, 777, {"scheme": 1}),                  # 3 limbs, ragged
     (65521, "N", "N", 3000, 3300, 1000, {"kb_override": 256, "korder": 1}),  # mid-k reductions
+    (65521, "T", "N", 3000, 3300, 1000, {"kb_override": 256, "korder": 2}),  # k-outer: rescaled write-backs
+    (8388593, "N", "N", 2600, 3600, 900, {"kb_override": 384, "korder": 2}),
 ])
 def test_wide_tiles_vs_oracle(env, p, tA, tB, m, n, k, opts):
     """256 x 512 CTA-pair tiles (ff_opts.wide_tiles = 1; automatic for one limb):
