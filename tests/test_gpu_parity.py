@@ -556,6 +556,28 @@ def test_row_panel_virtual_ranks_match_single_gpu(env, world, name):
 
 # ---------------------------------------------------------------- one Winograd level (row a7)
 
+@pytest.mark.parametrize("p", [251, 65521, 8388593, 65537])
+def test_winograd_products_on_wide_tiles(env, p):
+    """The Winograd products' multi-output epilogues (raw temporaries, addends,
+    two read-modify-written quadrants) on the 256 x 512 tiles (wide_tiles = 1,
+    limb schemes): bit-identical to the square tiles and to the classical path,
+    and exact against the oracle."""
+    torch, ff = env
+    rng = np.random.default_rng(p % 997)
+    m, n, k = 1536, 2048, 768
+    Abuf = _stored(rng, m, k, p, 1)
+    Bbuf = _stored(rng, k, n, p, 2)
+    Cbuf = _stored(rng, m, n, p, 3)
+    alpha, beta = p - 1, 1
+    base = {"winograd": 1, "scheme": 1}
+    wide = _run_gpu(torch, ff, p, "N", "N", m, n, k, alpha, Abuf, Bbuf, beta, Cbuf, dict(base, wide_tiles=1))
+    square = _run_gpu(torch, ff, p, "N", "N", m, n, k, alpha, Abuf, Bbuf, beta, Cbuf, dict(base, wide_tiles=-1))
+    np.testing.assert_array_equal(wide, square)
+    classic = _run_gpu(torch, ff, p, "N", "N", m, n, k, alpha, Abuf, Bbuf, beta, Cbuf, {"winograd": -1})
+    np.testing.assert_array_equal(wide, classic)
+    _check(p, "N", "N", m, n, k, alpha, Abuf, Bbuf, beta, Cbuf, wide)
+
+
 @pytest.mark.parametrize("p", CONFIG_PRIMES + [2, 3, 2 ** 31 - 1])
 @pytest.mark.parametrize("tA,tB", [("N", "N"), ("T", "N"), ("N", "T"), ("T", "T")])
 def test_winograd_level_vs_oracle(env, p, tA, tB):
