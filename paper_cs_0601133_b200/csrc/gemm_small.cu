@@ -178,13 +178,15 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int byt
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(bytes) : "memory");
 }
 
-__global__ void __launch_bounds__(kSThreads) small_gemm_canon_kernel(const __grid_constant__ SmallArgs a) {
-    extern __shared__ __align__(16) uint32_t csm[];
+// The 64 x 64 output tile (m0, n0) of one canonical product: byte-split partial
+// products accumulated in P (compute), then recombined, alpha/beta applied and
+// stored (store).  Split so that a kernel may put a grid barrier in between
+// (in-place products) or run several products in phases (small_chain_kernel).
+__device__ __forceinline__ void canon_compute(const SmallArgs& a, int m0, int n0, int (&P)[4][4][4], uint32_t* csm) {
     uint32_t* As = csm;                                  // [kCStages][kSM][kCApitch]
     uint32_t* Bs = csm + kCStages * kSM * kCApitch;      // [kCStages][kSK][kCBpitch]
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
     const int wm = warp & 3, wn = warp >> 2;
-    const int m0 = blockIdx.y * kSM, n0 = blockIdx.x * kSN;
     const int nsl = (a.k + kSK - 1) / kSK;
     auto issue = [&](int sl) {
         if (sl < nsl) {
@@ -208,7 +210,6 @@ __global__ void __launch_bounds__(kSThreads) small_gemm_canon_kernel(const __gri
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    int P[4][4][4];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -262,7 +263,12 @@ __global__ void __launch_bounds__(kSThreads) small_gemm_canon_kernel(const __gri
         }
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
-    if (a.alias) cooperative_groups::this_grid().sync();   // every CTA has read its A, B before C is written
+    __syncthreads();                                     // the shared stages may be reused by the caller
+}
+
+__device__ __forceinline__ void canon_store(const SmallArgs& a, int m0, int n0, const int (&P)[4][4][4]) {
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+    const int wm = warp & 3, wn = warp >> 2;
     const uint32_t p = a.M.p;
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt)
@@ -281,6 +287,48 @@ __global__ void __launch_bounds__(kSThreads) small_gemm_canon_kernel(const __gri
             *cp = static_cast<int32_t>(x);
         }
 }
+
+__global__ void __launch_bounds__(kSThreads) small_gemm_canon_kernel(const __grid_constant__ SmallArgs a) {
+    extern __shared__ __align__(16) uint32_t csm[];
+    const int m0 = blockIdx.y * kSM, n0 = blockIdx.x * kSN;
+    int P[4][4][4];
+    canon_compute(a, m0, n0, P, csm);
+    if (a.alias) cooperative_groups::this_grid().sync();   // every CTA has read its A, B before C is written
+    canon_store(a, m0, n0, P);
+}
+
+// LQUP's panel chain in one cooperative launch (lqup.cu): phase 1
+// runs products 0 and 1 (both in place: every CTA computes its tile, a grid
+// barrier, then stores), phase 2 product 2, which reads their outputs.  Each
+// product is at most 128 x 128 (four 64 x 64 tiles): CTAs 0-3 take product 0's
+// tiles, 4-7 product 1's, and CTAs 0-3 product 2's.
+struct ChainArgs {
+    SmallArgs p[3];
+};
+
+__global__ void __launch_bounds__(kSThreads) small_chain_kernel(const __grid_constant__ ChainArgs c) {
+    extern __shared__ __align__(16) uint32_t csm[];
+    const int b = blockIdx.x;
+    int P[4][4][4];
+    {
+        const SmallArgs& a = c.p[b >> 2];
+        const int m0 = ((b >> 1) & 1) * kSM, n0 = (b & 1) * kSN;
+        const bool live = m0 < a.m && n0 < a.n;
+        if (live) canon_compute(a, m0, n0, P, csm);
+        cooperative_groups::this_grid().sync();            // products 0, 1 read before they are written
+        if (live) canon_store(a, m0, n0, P);
+    }
+    cooperative_groups::this_grid().sync();                // their outputs are product 2's operands
+    if (b < 4) {
+        const SmallArgs& a = c.p[2];
+        const int m0 = (b >> 1) * kSM, n0 = (b & 1) * kSN;
+        if (m0 < a.m && n0 < a.n) {
+            canon_compute(a, m0, n0, P, csm);
+            canon_store(a, m0, n0, P);
+        }
+    }
+}
+
 
 // Wider fields (2^16 <= p < 2^31), canonical operands: L = 3 or 4 bytes per
 // residue and all L^2 byte products per K slice (each exact in s32 for K <= 33025),
@@ -475,6 +523,38 @@ int launch_gemm_small_canon(const Plan& pl, int64_t m, int64_t n, int64_t k, con
     a.alias = alias ? 1 : 0;
     a.reduce = reduce ? 1 : 0;
     return launch_small(reinterpret_cast<const void*>(small_gemm_canon_kernel), grid, kCSmem, a, alias, st);
+}
+
+int launch_small_chain(const Plan& pl0, const Plan& pl2, const SmallChainProduct (&pr)[3], cudaStream_t st) {
+    ChainArgs c;
+    for (int i = 0; i < 3; ++i) {
+        const Plan& pl = i < 2 ? pl0 : pl2;
+        SmallArgs& a = c.p[i];
+        if (pr[i].m > 2 * kSM || pr[i].n > 2 * kSN || pr[i].m < 0 || pr[i].n < 0 || pr[i].k <= 0 || pr[i].k > 32768 ||
+            !small_canon_ok(pl, false, false, pr[i].m > 0 ? pr[i].m : 1, pr[i].n > 0 ? pr[i].n : 1, pr[i].k, pr[i].A,
+                            pr[i].lda, pr[i].B, pr[i].ldb))
+            return FF_ERR_INTERNAL;
+        a.M = pl.mp;
+        a.mu64 = static_cast<unsigned long long>((static_cast<unsigned __int128>(1) << 64) / pl.mp.p);
+        a.A = pr[i].A; a.B = pr[i].B; a.C = pr[i].C;
+        a.lda = pr[i].lda; a.ldb = pr[i].ldb; a.ldc = pr[i].ldc;
+        a.m = static_cast<int32_t>(pr[i].m); a.n = static_cast<int32_t>(pr[i].n); a.k = static_cast<int32_t>(pr[i].k);
+        a.tA = 0; a.tB = 0;
+        a.alias = 1;
+        a.reduce = 0;
+    }
+    const void* fn = reinterpret_cast<const void*>(small_chain_kernel);
+    if (set_smem_attr(fn, kCSmem) != cudaSuccess) return FF_ERR_CUDA;
+    void* args[] = {&c};
+    note_launch();
+    prof_gemm_begin(st);
+    const cudaError_t le = cudaLaunchCooperativeKernel(fn, dim3(8), dim3(kSThreads), args, static_cast<size_t>(kCSmem), st);
+    prof_gemm_end(st);
+    if (le != cudaSuccess) {
+        cudaGetLastError();
+        return FF_ERR_CUDA;
+    }
+    return 0;
 }
 
 bool small_stream_ok(const Plan& pl, bool tA, bool tB, int64_t m, int64_t n, int64_t k, const int32_t* A, int64_t lda,

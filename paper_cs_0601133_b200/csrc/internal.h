@@ -99,6 +99,20 @@ int launch_gemm_small(const Plan& pl, bool tA, bool tB, int64_t m, int64_t n, in
 
 bool small_canon_ok(const Plan& pl, bool tA, bool tB, int64_t m, int64_t n, int64_t k, const int32_t* A, int64_t lda,
                     const int32_t* B, int64_t ldb);
+// LQUP's panel chain (three canonical products of at most 128 x 128, p < 2^16, the
+// third reading the first two's outputs; products 0 and 1 in place) in one
+// cooperative launch; FF_ERR_INTERNAL if it does not apply (the caller then runs
+// the three products one by one).
+struct SmallChainProduct {
+    int64_t m, n, k;
+    const int32_t* A;
+    int64_t lda;
+    const int32_t* B;
+    int64_t ldb;
+    int32_t* C;
+    int64_t ldc;
+};
+int launch_small_chain(const Plan& pl01, const Plan& pl2, const SmallChainProduct (&pr)[3], cudaStream_t st);
 // alias: C overlaps A or B (in-place products): a cooperative launch with a grid barrier between the
 // reads and the writes; FF_ERR_INTERNAL if the grid cannot be co-resident
 // reduce: A, B are raw int32 (any value), reduced per slice in shared memory (small_stream_ok)

@@ -1119,6 +1119,7 @@ int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t* A, int64_t lda, int64_
     }();
     int npend = 0;
     int64_t pi0 = 0, pc0 = 0;
+    static const bool chain_fuse = getenv("FF_LQUP_NOCHAIN") == nullptr;   // A/B knob
     // rows [ra, rb) x columns [ca, cb) -= A[ra.., pc0 .. pc0 + K) A[pi0 .. pi0 + K, ca..cb)
     auto upd = [&](int64_t ra, int64_t rb, int64_t ca, int64_t cb, int64_t K, int reserve) -> int {
         rb = std::min<int64_t>(rb, m_active);
@@ -1279,14 +1280,36 @@ int ff_lqup_ex(uint32_t p, int64_t m, int64_t n, int32_t* A, int64_t lda, int64_
                 int32_t* X = A + ra * lda + c;
                 return gemm_plain(p, opts, 'N', 'N', rb - ra, kk, kk, 1, X, lda, Uinv, kH, 0, X, lda, gws, st, 0, i0 > 0);
             };
-            if ((e = urest(c1, cw))) return e;
-            if (tl) cudaEventRecord(tl_ev.back()[4], st);
             if (npend == 0) { pi0 = i0; pc0 = c; }
             ++npend;
             const int64_t K = c1 - pc0;
-            if ((e = gmul(r1, rn))) return e;
-            if (tl) cudaEventRecord(tl_ev.back()[5], st);
-            if ((e = upd(r1, rn, c1, cw, K, 0))) return e;                      // the next window
+            // The three chain products in one cooperative launch when they take the
+            // small-field path anyway (p < 2^16, canonical operands): U_rest's window,
+            // G of the next rows (both in place), then the window's update from them.
+            int fused = FF_ERR_INTERNAL;
+            if (chain_fuse && i0 > 0 && !tl && kk == kH) {
+                const int64_t rnm = std::min<int64_t>(rn, m_active);
+                SmallChainProduct pr[3] = {
+                    {kk, cw - c1, kk, Linv, kH, A + i0 * lda + c1, lda, A + i0 * lda + c1, lda},
+                    {rnm - r1, kk, kk, A + r1 * lda + c, lda, Uinv, kH, A + r1 * lda + c, lda},
+                    {rnm - r1, cw - c1, K, A + r1 * lda + pc0, lda, A + pi0 * lda + c1, lda, A + r1 * lda + c1, lda}};
+                Plan p01, p2;
+                if (cw > c1 && rnm > r1 && make_plan(p, kk, opts, &p01) == 0 && make_plan(p, K, opts, &p2) == 0 &&
+                    p01.all_auto && p2.all_auto) {
+                    set_scalars(&p01, 1, 0);
+                    set_scalars(&p2, neg1, 1);
+                    p01.canonical_ab = p2.canonical_ab = true;
+                    fused = launch_small_chain(p01, p2, pr, st);
+                    if (fused != 0 && fused != FF_ERR_INTERNAL) return fused;
+                }
+            }
+            if (fused != 0) {
+                if ((e = urest(c1, cw))) return e;
+                if (tl) cudaEventRecord(tl_ev.back()[4], st);
+                if ((e = gmul(r1, rn))) return e;
+                if (tl) cudaEventRecord(tl_ev.back()[5], st);
+                if ((e = upd(r1, rn, c1, cw, K, 0))) return e;                  // the next window
+            }
             if (cudaEventRecord(ev_ready, st) != cudaSuccess) return fail_cuda();
             // the wide U_rest and G products: out of place (a small-field product may not
             // run in place without a grid barrier, which these grids are too large for),
