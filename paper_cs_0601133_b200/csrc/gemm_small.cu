@@ -343,14 +343,14 @@ __device__ __forceinline__ uint32_t pack_byte(uint32_t x, uint32_t y, uint32_t z
     return __byte_perm(__byte_perm(x, y, s), __byte_perm(z, w, s), 0x5410);
 }
 
+// The 64 x 16 tile (m0, n0) of one wide-field product, split into compute and
+// store like canon_compute / canon_store.
 template <int L>
-__global__ void __launch_bounds__(kSThreads) small_gemm_wide_kernel(const __grid_constant__ SmallArgs a) {
-    extern __shared__ __align__(16) uint32_t wsm[];
+__device__ __forceinline__ void wide_compute(const SmallArgs& a, int m0, int n0, int (&P)[L * L][4], uint32_t* wsm) {
     uint32_t* As = wsm;                                  // [kCStages][kSM][kCApitch]
     uint32_t* Bs = wsm + kCStages * kSM * kCApitch;      // [kCStages][kSK][kWBpitch]
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
     const int wm = warp & 3, wn = warp >> 2;
-    const int m0 = blockIdx.y * kSM, n0 = blockIdx.x * kWN;
     const int nsl = (a.k + kSK - 1) / kSK;
     auto issue = [&](int sl) {
         if (sl < nsl) {
@@ -373,7 +373,6 @@ __global__ void __launch_bounds__(kSThreads) small_gemm_wide_kernel(const __grid
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    int P[L * L][4];
 #pragma unroll
     for (int q = 0; q < L * L; ++q)
 #pragma unroll
@@ -414,7 +413,13 @@ __global__ void __launch_bounds__(kSThreads) small_gemm_wide_kernel(const __grid
         }
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
-    if (a.alias) cooperative_groups::this_grid().sync();   // every CTA has read its A, B before C is written
+    __syncthreads();                                     // the shared stages may be reused by the caller
+}
+
+template <int L>
+__device__ __forceinline__ void wide_store(const SmallArgs& a, int m0, int n0, const int (&P)[L * L][4]) {
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+    const int wm = warp & 3, wn = warp >> 2;
     const uint32_t p = a.M.p;
     uint32_t w[2 * L - 1];                               // 256^s mod p
     w[0] = 1u % p;
@@ -437,6 +442,42 @@ __global__ void __launch_bounds__(kSThreads) small_gemm_wide_kernel(const __grid
         int32_t* cp = a.C + static_cast<int64_t>(r) * a.ldc + cc;
         if (a.M.beta) x = addmod(x, mulmod_shoup(residue_i32(*cp, a.M), a.M.beta, a.M.beta_sh, p), p);
         *cp = static_cast<int32_t>(x);
+    }
+}
+
+template <int L>
+__global__ void __launch_bounds__(kSThreads) small_gemm_wide_kernel(const __grid_constant__ SmallArgs a) {
+    extern __shared__ __align__(16) uint32_t wsm[];
+    const int m0 = blockIdx.y * kSM, n0 = blockIdx.x * kWN;
+    int P[L * L][4];
+    wide_compute<L>(a, m0, n0, P, wsm);
+    if (a.alias) cooperative_groups::this_grid().sync();   // every CTA has read its A, B before C is written
+    wide_store<L>(a, m0, n0, P);
+}
+
+// small_chain_kernel for 2^16 <= p < 2^31: 64 x 16 tiles, 16 per 128 x 128
+// product; CTAs 0-15 product 0, 16-31 product 1, then CTAs 0-15 product 2.
+template <int L>
+__global__ void __launch_bounds__(kSThreads) small_chain_wide_kernel(const __grid_constant__ ChainArgs c) {
+    extern __shared__ __align__(16) uint32_t wsm[];
+    const int b = blockIdx.x;
+    int P[L * L][4];
+    {
+        const SmallArgs& a = c.p[b >> 4];
+        const int m0 = ((b >> 3) & 1) * kSM, n0 = (b & 7) * kWN;
+        const bool live = m0 < a.m && n0 < a.n;
+        if (live) wide_compute<L>(a, m0, n0, P, wsm);
+        cooperative_groups::this_grid().sync();
+        if (live) wide_store<L>(a, m0, n0, P);
+    }
+    cooperative_groups::this_grid().sync();
+    if (b < 16) {
+        const SmallArgs& a = c.p[2];
+        const int m0 = (b >> 3) * kSM, n0 = (b & 7) * kWN;
+        if (m0 < a.m && n0 < a.n) {
+            wide_compute<L>(a, m0, n0, P, wsm);
+            wide_store<L>(a, m0, n0, P);
+        }
     }
 }
 
@@ -530,9 +571,12 @@ int launch_small_chain(const Plan& pl0, const Plan& pl2, const SmallChainProduct
     for (int i = 0; i < 3; ++i) {
         const Plan& pl = i < 2 ? pl0 : pl2;
         SmallArgs& a = c.p[i];
+        const int64_t mm = pr[i].m > 0 ? pr[i].m : 1, nn = pr[i].n > 0 ? pr[i].n : 1;
+        const bool ok = pl.mp.p < 65536u
+                            ? small_canon_ok(pl, false, false, mm, nn, pr[i].k, pr[i].A, pr[i].lda, pr[i].B, pr[i].ldb)
+                            : small_wide_ok(pl, false, false, mm, nn, pr[i].k, pr[i].A, pr[i].lda, pr[i].B, pr[i].ldb);
         if (pr[i].m > 2 * kSM || pr[i].n > 2 * kSN || pr[i].m < 0 || pr[i].n < 0 || pr[i].k <= 0 || pr[i].k > 32768 ||
-            !small_canon_ok(pl, false, false, pr[i].m > 0 ? pr[i].m : 1, pr[i].n > 0 ? pr[i].n : 1, pr[i].k, pr[i].A,
-                            pr[i].lda, pr[i].B, pr[i].ldb))
+            !ok || (pl.mp.p < 65536u) != (pl0.mp.p < 65536u))
             return FF_ERR_INTERNAL;
         a.M = pl.mp;
         a.mu64 = static_cast<unsigned long long>((static_cast<unsigned __int128>(1) << 64) / pl.mp.p);
@@ -543,12 +587,17 @@ int launch_small_chain(const Plan& pl0, const Plan& pl2, const SmallChainProduct
         a.alias = 1;
         a.reduce = 0;
     }
-    const void* fn = reinterpret_cast<const void*>(small_chain_kernel);
-    if (set_smem_attr(fn, kCSmem) != cudaSuccess) return FF_ERR_CUDA;
+    const bool narrow = pl0.mp.p < 65536u;
+    const void* fn = narrow ? reinterpret_cast<const void*>(small_chain_kernel)
+                   : pl0.mp.p < (1u << 24) ? reinterpret_cast<const void*>(small_chain_wide_kernel<3>)
+                                           : reinterpret_cast<const void*>(small_chain_wide_kernel<4>);
+    const int smem = narrow ? kCSmem : kWSmem;
+    if (set_smem_attr(fn, smem) != cudaSuccess) return FF_ERR_CUDA;
     void* args[] = {&c};
     note_launch();
     prof_gemm_begin(st);
-    const cudaError_t le = cudaLaunchCooperativeKernel(fn, dim3(8), dim3(kSThreads), args, static_cast<size_t>(kCSmem), st);
+    const cudaError_t le = cudaLaunchCooperativeKernel(fn, dim3(narrow ? 8 : 32), dim3(kSThreads), args,
+                                                       static_cast<size_t>(smem), st);
     prof_gemm_end(st);
     if (le != cudaSuccess) {
         cudaGetLastError();
