@@ -24,7 +24,8 @@
 // computes 256 x 256 tiles with tcgen05.mma.cta_group::2 (M = 256): each CTA
 // stages its own 128 rows of A and 128 of the 256 rows of B, the leader CTA
 // issues the MMAs, each CTA's TMEM holds its 128 output rows.  This halves
-// the SMEM operand traffic per MMA versus kPair = 1 (128 x 256 tiles).
+// the SMEM operand traffic per MMA versus kPair = 1 (128 x 256 tiles).  The
+// kWide variant (Cfg) widens the pair's tile to 256 x 512.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -49,10 +50,10 @@ constexpr int kWideDeltaWb = 6;    //   before a TMEM write-back step (swept on 
 constexpr int kRasterDefault = 12;  // tile-rows per raster band (L2 reuse; swept on c4: DESIGN.md §16)
 
 // kWide (CTA pair only): 256 x 512 tiles, two N = 256 MMAs per k-step sharing the
-// A stage, one accumulator in all 512 TMEM columns (no second slot): 25% less
-// L2->SMEM operand traffic per MMA, the epilogue no longer hidden behind the
-// other slot.  Used for single-step tiles (one weight group, one k-block), where
-// the exposed epilogue is one final pass per tile.
+// A stage, one accumulator in all 512 TMEM columns (no second slot): up to 25%
+// less L2->SMEM operand traffic per MMA; the two halves are staggered
+// (wide_phases) so each half's epilogue overlaps MMAs of the other.  Default for
+// one-limb plans (c3), ff_opts.wide_tiles = 1 for any limb plan.
 template <int kPair, bool kWide = false>
 struct Cfg {
     static constexpr int BM = 128 * kPair;         // tile rows (per cluster)
