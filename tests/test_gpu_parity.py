@@ -366,7 +366,8 @@ def test_identity_permutation_on_gpu(env):
 
 @pytest.mark.parametrize("tA,tB,beta,block,p", [("T", "N", 1, 0, 8388593), ("N", "N", 0, 256, 8388593),
                                                  ("T", "T", 5, 256, 8388593), ("N", "T", 0, 512, 8388593),
-                                                 ("N", "N", 3, 256, 67108859), ("T", "N", 0, 0, 67108859)])
+                                                 ("N", "N", 3, 256, 67108859), ("T", "N", 0, 0, 67108859),
+                                                 ("T", "N", 1, 0, 251), ("N", "T", 0, 256, 251)])
 def test_host_entry_point(env, tA, tB, beta, block, p):
     """ff_gemm_host: host buffers, pipelined over blocks of C (block=256 forces
     several row panels and column chunks, with ragged last blocks); p = 67108859
@@ -381,6 +382,27 @@ def test_host_entry_point(env, tA, tB, beta, block, p):
     ff.ff_gemm_host(p, tA, tB, m, n, k, 3, A, A.shape[1], B, B.shape[1], beta, out, out.shape[1],
                     {"host_block": block})
     _check(p, tA, tB, m, n, k, 3, A, B, beta, C, out)
+
+
+def test_host_entry_point_wide_blocks(env):
+    """ff_gemm_host with blocks large enough for the 256 x 512 tiles (p = 251:
+    one limb): sampled rows against the oracle, Freivalds on the whole output."""
+    torch, ff = env
+    p, m, n, k = 251, 5000, 4700, 1500
+    rng = np.random.default_rng(17)
+    A = _stored(rng, k, m, p)          # transA = T
+    B = _stored(rng, k, n, p)
+    C = _stored(rng, m, n, p)
+    out = C.copy()
+    ff.ff_gemm_host(p, "T", "N", m, n, k, 7, A, m, B, n, 2, out, n, None)
+    rows = [0, 1, 2047, 4095, 4096, m - 1]
+    want = oracle.fgemm_rows(p, "T", "N", 7, A, B, 2, C[rows], rows, m, n, k)
+    np.testing.assert_array_equal(out[rows], want)
+    x = rng.integers(0, p, size=n).astype(np.int32)
+    lhs = oracle.matvec(p, "N", out, x).astype(np.int64)
+    rhs = (7 * oracle.matvec(p, "T", A, oracle.matvec(p, "N", B, x)).astype(np.int64) +
+           2 * oracle.matvec(p, "N", C, x).astype(np.int64)) % p
+    np.testing.assert_array_equal(lhs, rhs)
 
 
 def test_split_entry_points_chunked_B(env):
