@@ -119,9 +119,9 @@ typedef struct ff_opts {
                                are identical) */
     int32_t wide_tiles;     /* tcgen05 GEMM tile shape: 0 auto (256 x 512 CTA-pair tiles with
                                staggered halves for one-limb plans, p < 256, when they fill
-                               the GPU), 1 256 x 512 whenever the plan's steps
-                               may run group-outer (limb schemes), -1 never.  Results are
-                               identical. */
+                               the GPU), 1 256 x 512 for every limb plan on the
+                               CTA-pair kernel (ignored for CRT plans and with cta_group = 1),
+                               -1 never (256 x 256).  Results are identical. */
 } ff_opts;
 
 /* The plan the library derives from (p, k, opts): host-only, no GPU needed. */
