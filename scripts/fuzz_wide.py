@@ -24,6 +24,8 @@ for case in range(n_cases):
     m, n, k = (int(rng.integers(1, 2600)), int(rng.integers(1, 2600)), int(rng.integers(1, 3000)))
     tA, tB = str(rng.choice(["N", "T"])), str(rng.choice(["N", "T"]))
     opts = {"scheme": int(rng.choice([0, 1, 2])), "small_path": -1}
+    if rng.random() < 0.5:
+        opts["cta_group"] = 2          # the pair kernel (and so the wide tiles) even for small outputs
     if rng.random() < 0.3:
         opts["korder"] = int(rng.choice([1, 2]))
         info = ff.ff_plan_query(p, k, {"scheme": opts["scheme"]})

@@ -326,6 +326,33 @@ def test_crt_dot_product_at_the_bound(env, p, k):
             assert (C == X % p).all().item(), (p, k, va, vb, grp)
 
 
+@pytest.mark.parametrize("p", [251, 65521, 8388593])
+def test_wide_tiles_tiny_and_degenerate(env, p):
+    """Forced 256 x 512 tiles on shapes far below one tile (1 x 1 x 1, a single row
+    or column, k = 1, k = 129 across one k-slice boundary, n just past 256 and
+    512), plus the quick returns (k = 0, alpha = 0), against the oracle and the
+    square tiles."""
+    torch, ff = env
+    rng = np.random.default_rng(p % 101)
+    for (m, n, k) in [(1, 1, 1), (1, 700, 33), (300, 1, 129), (5, 257, 1), (256, 513, 128), (257, 511, 255)]:
+        A = _stored(rng, m, k, p, 1)
+        B = _stored(rng, k, n, p, 2)
+        C = _stored(rng, m, n, p, 3)
+        alpha, beta = int(rng.integers(0, p)), int(rng.integers(0, p))
+        opts = {"scheme": 1, "small_path": -1, "cta_group": 2}    # the pair kernel even for tiny outputs
+        wide = _run_gpu(torch, ff, p, "N", "N", m, n, k, alpha, A, B, beta, C, dict(opts, wide_tiles=1))
+        square = _run_gpu(torch, ff, p, "N", "N", m, n, k, alpha, A, B, beta, C, dict(opts, wide_tiles=-1))
+        np.testing.assert_array_equal(wide, square, err_msg="m=%d n=%d k=%d" % (m, n, k))
+        _check(p, "N", "N", m, n, k, alpha, A, B, beta, C, wide)
+    C = _stored(rng, 40, 600, p)
+    A = _stored(rng, 40, 8, p)
+    B = _stored(rng, 8, 600, p)
+    got = _run_gpu(torch, ff, p, "N", "N", 40, 600, 0, 3, A, B, 5, C, {"wide_tiles": 1, "cta_group": 2})
+    np.testing.assert_array_equal(got[:, :600], (5 * C[:, :600].astype(np.int64)) % p)
+    got = _run_gpu(torch, ff, p, "N", "N", 40, 600, 8, 0, A, B, 5, C, {"wide_tiles": 1, "cta_group": 2})
+    np.testing.assert_array_equal(got[:, :600], (5 * C[:, :600].astype(np.int64)) % p)
+
+
 def test_quick_returns_and_degenerate(env):
     torch, ff = env
     p = 65521
