@@ -29,3 +29,30 @@ def test_reference_arm_other_ranks_exit_quietly():
                         "--config", "c1", "--steps", "1"], capture_output=True, text=True, timeout=300,
                        cwd=ROOT, env=env)
     assert r.returncode == 0 and r.stdout.strip() == ""
+
+
+import pytest  # noqa: E402
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg", ["c1", "c5"])
+def test_multi_rank_bench_path_on_one_gpu(cfg):
+    """bench.py's N > 1 path (row-panel sharding, sharded.py) launched as the driver
+    does (torch.distributed.run, 2 ranks), here both ranks on cuda:0 over gloo
+    (FF_BENCH_SHARE_GPU=1; the real run is NCCL, one GPU per rank): one JSON line
+    from rank 0, every rank's panel verified bit-exact.  c1: encoded B planes
+    broadcast; c5: int32 B broadcast, per-rank CRT encode, one Winograd level per
+    panel."""
+    env = dict(os.environ, FF_BENCH_SHARE_GPU="1")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29533" if cfg == "c1" else "29534",
+                        os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "2", "--warmup", "3",
+                        "--config", cfg, "--no-e2e"],
+                       capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.strip().splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["scaling"] == "strong"
+    assert line["verify"]["ok"] and line["verify"]["all_ranks_ok"]
+    assert line["gpu_launches"] > 0 and line["value"] > 0
