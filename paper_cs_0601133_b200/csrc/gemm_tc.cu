@@ -103,6 +103,7 @@ struct GemmArgs {
     int32_t crt;                // 1: groups are CRT moduli
     const int32_t* addend;      // optional: residues in [0, p) added to R (mod p) for the outputs
     int64_t ld_add;             //   with `add` set (Winograd temporaries U2 = P1 + P6)
+    int32_t add_vec;            //   1 if the addend's rows are 16-byte aligned
     CrtConsts cc;
     uint8_t* scratch;           // CRT: per CTA and slot, G byte planes of kCrtPlane bytes
     int32_t wdelta;             // wide tiles: k-steps of the staggered halves (wide_phases), final steps
@@ -257,9 +258,17 @@ __device__ __forceinline__ void crt_group(const GemmArgs& a, const ModP& M, cons
         const bool full = O.vec && (col0 + 8 <= a.n);
         if (O.add && !added) {
             const int32_t* ad = a.addend + static_cast<int64_t>(row) * a.ld_add + col0;
+            if (a.add_vec && col0 + 8 <= a.n) {   // two 16-byte loads instead of eight scalar ones
+                const int4 y0 = *reinterpret_cast<const int4*>(ad), y1 = *reinterpret_cast<const int4*>(ad + 4);
+                const uint32_t y[8] = {(uint32_t)y0.x, (uint32_t)y0.y, (uint32_t)y0.z, (uint32_t)y0.w,
+                                       (uint32_t)y1.x, (uint32_t)y1.y, (uint32_t)y1.z, (uint32_t)y1.w};
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
-                if (col0 + j < a.n) X[j] = addmod(X[j], static_cast<uint32_t>(ad[j]), M.p);
+                for (int j = 0; j < 8; ++j) X[j] = addmod(X[j], y[j], M.p);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (col0 + j < a.n) X[j] = addmod(X[j], static_cast<uint32_t>(ad[j]), M.p);
+            }
             added = true;
         }
         uint32_t o[8];
@@ -877,6 +886,7 @@ int launch_impl(const Plan& pl, int64_t m, int64_t n, int64_t k, const int8_t* A
     }
     a.addend = addend;
     a.ld_add = ld_add;
+    a.add_vec = (addend && (ld_add % 4) == 0 && (reinterpret_cast<uintptr_t>(addend) & 15) == 0) ? 1 : 0;
     a.last_use = last_use;
     a.ldc = ldc;
     a.m = static_cast<int32_t>(m);
