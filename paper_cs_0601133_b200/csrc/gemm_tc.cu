@@ -139,8 +139,9 @@ __device__ __forceinline__ void wide_phases(const GemmArgs& a, int g, int kb, F&
 }
 
 // CRT residue scratch: one 128 x 256 byte plane per (CTA, slot, modulus 0..G-1),
-// laid out [h: 64-column quarter][c: 16-column chunk][row 0..127][16 bytes] so
-// that a warp's 32 rows store / load 512 contiguous bytes per instruction.
+// laid out [h: 64-column quarter][grp: 8-column group][row 0..127][8 bytes] so
+// that a warp's 32 rows store / load 256 contiguous bytes per instruction, and
+// the final step's per-group reads (crt_group) use every byte of their sectors.
 constexpr int kCrtPlane = 128 * kTileN;
 constexpr int kCrtBatch = 5;    // scratch bytes of this many moduli loaded together in the final step
 
@@ -219,7 +220,7 @@ __device__ __forceinline__ void crt_group(const GemmArgs& a, const ModP& M, cons
                                           int grp) {
     if (row >= a.m) return;
     const int col0 = col_q + grp * 8;
-    const uint8_t* src = plane0 + (grp >> 1) * 128 * 16 + (grp & 1) * 8;
+    const uint8_t* src = plane0 + grp * 128 * 8;
     unsigned long long S[8];
     uint32_t F[8];
 #pragma unroll
@@ -578,7 +579,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tile_coords(a, pend_tile[ps], tm, tn);
             const int row = tm * K::BM + static_cast<int>(rank) * 128 + q * 32 + static_cast<int>(lane);
             const int crow = q * 32 + static_cast<int>(lane);
-            crt_group(a, M, crt_plane(a, ps, 0) + (h * 4 * 128 + crow) * 16, row, tn * K::BN + h * 64, pend_grp[ps]);
+            crt_group(a, M, crt_plane(a, ps, 0) + (h * 8 * 128 + crow) * 8, row, tn * K::BN + h * 64, pend_grp[ps]);
             ++pend_grp[ps];
         };
         for_each_step<kWide>(a, unit, nunits, tbase, tcount, [&](int tile, int slot, int g, int kb) {
@@ -632,7 +633,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::tmem_wait_st();
                 } else {
                     const uint32_t vg = a.cc.v[g];
-                    uint8_t* dst = crt_plane(a, slot, g) + (h * 4 * 128 + crow) * 16;
+                    uint8_t* dst = crt_plane(a, slot, g) + (h * 8 * 128 + crow) * 8;
 #pragma unroll
                     for (int c = 0; c < 4; ++c) {
                         uint32_t w[4];
@@ -645,7 +646,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 w[j] |= mulmod_small(r, vg, qg, mu) << (8 * b);
                             }
                         }
-                        *reinterpret_cast<uint4*>(dst + c * 128 * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+                        // columns 16c .. 16c+15 = groups 2c and 2c+1 of this quarter
+                        *reinterpret_cast<uint2*>(dst + (2 * c) * 128 * 8) = make_uint2(w[0], w[1]);
+                        *reinterpret_cast<uint2*>(dst + (2 * c + 1) * 128 * 8) = make_uint2(w[2], w[3]);
                     }
                 }
             }
